@@ -1,0 +1,318 @@
+/*
+ * sgdb.h — C-ABI of the B200-native GLM SGD engine (libsgdb_b200.so).
+ *
+ * Drop-in boundary for the reference's training path. The reference
+ * (/root/reference/proj, C++20, CPU-only) exposes no FFI: its boundary is the
+ * C++ API in proj/include/sgdbench/{sync_engine,async_engine,linalg,glm,
+ * dataset,fixtures}.hpp, called by harness::run_engine_once
+ * (proj/src/harness.cpp:75-124). This header re-expresses that API as plain C
+ * (opaque handles, plain pointers and sizes, integer status codes) so that the
+ * C++ host engine in this library, a C++ adapter for the reference harness
+ * (INTEGRATION.md), and Python (ctypes) all bind the same entry points.
+ *
+ * Layers:
+ *   1. device ops    — context, device-resident dataset/model, one sync epoch,
+ *                      one Hogwild epoch, replica averaging, loss. Each
+ *                      launches hand-written sm_100a kernels.
+ *   2. whole runs    — sgdb_sync_train / sgdb_hogwild_train /
+ *                      sgdb_numa_dual_train: the reference's epoch loops
+ *                      (host C++: schedule, timing, hooks, budget, divergence)
+ *                      over layer 1.
+ *   3. host helpers  — fixtures, LIBSVM parsing, binary cache, layout
+ *                      conversion, worker assignment, plan grammar, the
+ *                      mini-batch schedule. Pure host code, no GPU needed.
+ *
+ * Errors: every function returns sgdb_status; on failure
+ * sgdb_last_error() (thread-local) holds the message. The codes map 1:1 onto
+ * the reference's exception types (std::invalid_argument, std::domain_error,
+ * ParseError, CapacityError, std::runtime_error). Divergence is NOT an error:
+ * it is reported in-band in sgdb_trace, as LossTrace does
+ * (proj/src/sync_engine.cpp:107-113).
+ *
+ * Precision: the interface is fp64 like the reference (dataset.hpp:46-48);
+ * device storage and per-example arithmetic are fp32, reductions and the
+ * synchronous master model fp64.
+ */
+#ifndef SGDB_H_
+#define SGDB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------- */
+typedef int32_t sgdb_status;
+#define SGDB_OK 0
+#define SGDB_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument           */
+#define SGDB_ERR_DOMAIN 2           /* std::domain_error                */
+#define SGDB_ERR_PARSE 3            /* sgdbench::ParseError (dataset.hpp:22-26) */
+#define SGDB_ERR_CAPACITY 4         /* sgdbench::CapacityError (dataset.hpp:28-30) */
+#define SGDB_ERR_RUNTIME 5          /* std::runtime_error (I/O)         */
+#define SGDB_ERR_CUDA 6             /* CUDA runtime / launch failure    */
+#define SGDB_ERR_UNSUPPORTED 7      /* plan/layout combination not built on the device */
+
+/* ---- enums (same numbering as the reference enums) ---------------------- */
+typedef enum { SGDB_TASK_LR = 0, SGDB_TASK_SVM = 1 } sgdb_task;           /* glm.hpp:15 */
+typedef enum {                                                             /* dataset.hpp:13 */
+  SGDB_LAYOUT_DENSE_ROW = 0,
+  SGDB_LAYOUT_DENSE_COL = 1,
+  SGDB_LAYOUT_CSR = 2,
+  SGDB_LAYOUT_PADDED = 3
+} sgdb_layout;
+typedef enum { SGDB_STRATEGY_ROUND_ROBIN = 0, SGDB_STRATEGY_CHUNK = 1 } sgdb_strategy; /* dataset.hpp:133 */
+typedef enum {                                                             /* async_engine.hpp:17 */
+  SGDB_ACCESS_ROW_RR = 0,
+  SGDB_ACCESS_ROW_CH = 1,
+  SGDB_ACCESS_COL_RR = 2,
+  SGDB_ACCESS_COL_CH = 3
+} sgdb_access_path;
+typedef enum {                                                             /* async_engine.hpp:21 */
+  SGDB_REPL_KERNEL = 0,
+  SGDB_REPL_BLOCK = 1,
+  SGDB_REPL_THREAD = 2,
+  SGDB_REPL_EXAMPLE = 3
+} sgdb_replication;
+
+/* ---- plain structs ------------------------------------------------------- */
+
+/* Borrowed host view of a dataset; field-for-field sgdbench::Dataset
+ * (dataset.hpp:42-61). row_offsets is size_t in the reference: uint64 here. */
+typedef struct sgdb_dataset_view {
+  uint64_t n_examples;
+  uint64_t n_features;
+  int32_t layout; /* sgdb_layout */
+  const double* labels;         /* n_examples, each +1/-1 */
+  const double* values;         /* n_values */
+  uint64_t n_values;
+  const uint32_t* indices;      /* n_indices (Csr / PaddedDense) */
+  uint64_t n_indices;
+  const uint64_t* row_offsets;  /* n_examples + 1 (Csr) */
+  uint64_t n_row_offsets;
+  uint64_t padded_width;        /* PaddedDense */
+} sgdb_dataset_view;
+
+/* Hyperparams (glm.hpp:22-35). step_size(e) = alpha * step_decay^(e-1). */
+typedef struct sgdb_hyperparams {
+  double alpha;
+  uint64_t batch_b;
+  uint64_t epochs;
+  int32_t task; /* sgdb_task */
+  double step_decay;
+} sgdb_hyperparams;
+
+/* ExecutionPlan (async_engine.hpp:25-33). On the device a "worker" is a lane
+ * group (one warp by default) walking its assign()
+ * list; workers, group_size, k keep the reference's meaning. */
+typedef struct sgdb_plan {
+  int32_t access_path; /* sgdb_access_path */
+  int32_t replication; /* sgdb_replication */
+  uint64_t data_replication_k;
+  uint64_t workers;
+  uint64_t group_size;
+  int32_t circular_offsets;
+  uint64_t merge_period_epochs;
+  int32_t lanes_per_worker; /* device-only knob: 0 = auto, else 1/2/4/8/16/32 */
+} sgdb_plan;
+
+/* EpochRecord (trace.hpp:21-25). */
+typedef struct sgdb_epoch_record {
+  uint64_t epoch; /* 1-based */
+  double loss;
+  double seconds; /* compute-only, loss evaluation excluded */
+} sgdb_epoch_record;
+
+/* LossTrace (trace.hpp:27-49) + Result::evals_per_epoch (async_engine.hpp:84-88).
+ * The caller owns the arrays; capacity bounds both. */
+typedef struct sgdb_trace {
+  sgdb_epoch_record* epochs;
+  uint64_t* evals_per_epoch; /* may be NULL; Hogwild only */
+  uint64_t capacity;
+  uint64_t count;
+  int32_t diverged;
+  char divergence_note[160];
+} sgdb_trace;
+
+typedef double (*sgdb_clock_fn)(void* user);                               /* Clock (trace.hpp:14-19) */
+typedef void (*sgdb_epoch_hook_fn)(void* user, uint64_t epoch, double loss);
+
+/* TrainOptions (sync_engine.hpp:15-25) / hogwild::Options (async_engine.hpp:77-82). */
+typedef struct sgdb_train_options {
+  uint32_t workers; /* accepted for signature parity; the device ignores it */
+  int32_t shuffle;  /* sync only */
+  double max_seconds;
+  const double* initial_model; /* NULL or n_features doubles */
+  uint64_t initial_model_len;
+  sgdb_clock_fn clock;        /* NULL = steady clock */
+  void* clock_user;
+  sgdb_epoch_hook_fn epoch_hook; /* NULL = none */
+  void* hook_user;
+} sgdb_train_options;
+
+/* Collective hook for multi-GPU runs: called by the engine at each exchange
+ * step with a device buffer to SUM-reduce in place across ranks on `stream`
+ * (dtype 0 = float32, 1 = float64). Provided by the host's process group
+ * (torch.distributed / NCCL); the engine never owns a communicator. */
+typedef int32_t (*sgdb_allreduce_fn)(void* user, void* device_buffer, uint64_t count,
+                                     int32_t dtype, void* stream);
+
+/* ---- opaque handles ------------------------------------------------------ */
+typedef struct sgdb_ctx sgdb_ctx;
+typedef struct sgdb_dataset sgdb_dataset;           /* device-resident */
+typedef struct sgdb_model sgdb_model;               /* device-resident */
+typedef struct sgdb_host_dataset sgdb_host_dataset; /* library-owned host arrays */
+typedef struct sgdb_schedule sgdb_schedule;
+
+/* ======================================================================== */
+/* 1. device ops                                                            */
+/* ======================================================================== */
+
+const char* sgdb_last_error(void);
+const char* sgdb_version(void);
+
+/* Device context: device ordinal + the CUDA stream every op is queued on
+ * (NULL = the context creates its own). One host thread per context. */
+sgdb_status sgdb_ctx_create(int32_t device, void* cuda_stream, sgdb_ctx** out);
+sgdb_status sgdb_ctx_destroy(sgdb_ctx* ctx);
+sgdb_status sgdb_ctx_stream(sgdb_ctx* ctx, void** stream_out);
+sgdb_status sgdb_ctx_synchronize(sgdb_ctx* ctx);
+/* Number of this library's kernels launched on the context so far. */
+sgdb_status sgdb_ctx_launch_count(sgdb_ctx* ctx, uint64_t* out);
+sgdb_status sgdb_ctx_set_allreduce(sgdb_ctx* ctx, sgdb_allreduce_fn fn, void* user);
+/* Worker geometry the Hogwild kernels resolve for `lanes` lanes per worker
+ * (0 = auto for this dataset): the number of concurrently resident workers. */
+sgdb_status sgdb_ctx_resident_workers(sgdb_ctx* ctx, const sgdb_dataset* ds,
+                                      int32_t lanes_per_worker, uint64_t* out);
+
+/* Upload (untimed setup): fp64 host values -> fp32 device
+ * storage. Dense layouts are stored row-major, PaddedDense/Csr as CSR (plus
+ * the original slot-major padded arrays for the column access paths).
+ * row_base / n_global describe a row shard of a larger logical dataset
+ * (multi-GPU); pass 0 / n_examples for a whole dataset. */
+sgdb_status sgdb_dataset_upload(sgdb_ctx* ctx, const sgdb_dataset_view* view, uint64_t row_base,
+                                uint64_t n_global, sgdb_dataset** out);
+/* Re-copy host arrays of the same shape into an existing device dataset
+ * (the e2e leg of bench.py): fp32 values/labels straight from (pinned) host
+ * buffers, asynchronously on the context stream. indices/row_offsets may be
+ * NULL to keep the device copies. */
+sgdb_status sgdb_dataset_refresh_f32(sgdb_ctx* ctx, sgdb_dataset* ds, const float* values,
+                                     const float* labels, const uint32_t* indices,
+                                     const uint32_t* row_offsets32);
+sgdb_status sgdb_dataset_free(sgdb_dataset* ds);
+/* Algorithmic bytes of one sweep: CSR nnz*8 + (N+1)*4 + N*4;
+ * dense N*d*4 + N*4. */
+sgdb_status sgdb_dataset_sweep_bytes(const sgdb_dataset* ds, uint64_t* out);
+sgdb_status sgdb_dataset_shape(const sgdb_dataset* ds, uint64_t* n_local, uint64_t* d,
+                               uint64_t* nnz, uint64_t* row_base, uint64_t* n_global);
+
+sgdb_status sgdb_model_create(sgdb_ctx* ctx, uint64_t d, const double* init, sgdb_model** out);
+sgdb_status sgdb_model_set(sgdb_ctx* ctx, sgdb_model* m, const double* w);
+sgdb_status sgdb_model_get(sgdb_ctx* ctx, sgdb_model* m, double* w_out);
+/* Device pointers of the fp32 working copy (d+1 floats, guard slot d == 0)
+ * and of the fp64 master (d doubles). */
+sgdb_status sgdb_model_device_ptrs(sgdb_model* m, float** w32, double** w64);
+sgdb_status sgdb_model_free(sgdb_model* m);
+
+/* One synchronous epoch (sync_engine.cpp:86-100): the ids in `order`
+ * (host; NULL = ascending 0..n_global-1) taken as consecutive mini-batches of
+ * batch_b; per batch g = X_B^T c(X_B w) then w -= alpha*g. With
+ * batch_b >= n_global the epoch is one full-batch step and `order` is not
+ * read. *finite_out = 0 if any gradient entry was non-finite (the epoch stops
+ * after that batch, as the reference does). */
+sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
+                            double alpha, const uint32_t* order, uint64_t batch_b,
+                            int32_t* finite_out);
+/* sync::batch_gradient (sync_engine.hpp:33-36): g over `rows` (global ids;
+ * n_rows == 0 = all) at the host model w. No update. */
+sgdb_status sgdb_batch_gradient(sgdb_ctx* ctx, sgdb_dataset* ds, int32_t task,
+                                const uint32_t* rows, uint64_t n_rows, const double* w,
+                                double* g_out);
+/* sync::epoch_batch (sync_engine.hpp:40-41): one B=N step, returns ||g||_2. */
+sgdb_status sgdb_epoch_batch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
+                             double alpha, double* grad_norm_out);
+
+/* One Hogwild epoch of `plan` (async_engine.cpp:244-254 + 372-396): replica
+ * prepare, the workers' passes, replica merge. *evals_out = n + T_nonempty*k. */
+sgdb_status sgdb_hogwild_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
+                               double alpha, const sgdb_plan* plan, uint64_t* evals_out);
+/* merge_models (async_engine.cpp:133-156) over device models: out = weighted
+ * mean (weights NULL = unweighted); when refresh != 0 every input is set to it. */
+sgdb_status sgdb_models_average(sgdb_ctx* ctx, sgdb_model* const* models, uint64_t count,
+                                const double* weights, sgdb_model* out, int32_t refresh);
+
+/* dataset_loss (glm.cpp:85-94): sum of point losses, fp64. With an allreduce
+ * hook set the per-shard sum is reduced across ranks. */
+sgdb_status sgdb_loss(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
+                      double* loss_out);
+
+/* ======================================================================== */
+/* 2. whole runs (host C++ epoch loops over layer 1)                        */
+/* ======================================================================== */
+
+/* sync::train (sync_engine.hpp:51-52). */
+sgdb_status sgdb_sync_train(sgdb_ctx* ctx, sgdb_dataset* ds, const sgdb_hyperparams* hyper,
+                            uint64_t seed, const sgdb_train_options* options, double* model_out,
+                            sgdb_trace* trace);
+/* hogwild::train (async_engine.hpp:96-97). */
+sgdb_status sgdb_hogwild_train(sgdb_ctx* ctx, sgdb_dataset* ds, const sgdb_hyperparams* hyper,
+                               const sgdb_plan* plan, uint64_t seed,
+                               const sgdb_train_options* options, double* model_out,
+                               sgdb_trace* trace);
+/* hogwild::numa_dual_train (async_engine.hpp:102-104): two full-data
+ * replicas averaged every merge_period_epochs. */
+sgdb_status sgdb_numa_dual_train(sgdb_ctx* ctx, sgdb_dataset* ds, const sgdb_hyperparams* hyper,
+                                 const sgdb_plan* plan, uint64_t seed,
+                                 const sgdb_train_options* options, double* model_out,
+                                 sgdb_trace* trace);
+
+/* ======================================================================== */
+/* 3. host helpers (no GPU)                                                 */
+/* ======================================================================== */
+
+/* fixtures::dense_classification / sparse_classification (fixtures.hpp:12-19). */
+sgdb_status sgdb_fixture_dense(uint64_t n, uint64_t d, uint64_t seed, double label_noise,
+                               sgdb_host_dataset** out);
+sgdb_status sgdb_fixture_sparse(uint64_t n, uint64_t d, double avg_nnz, uint64_t seed,
+                                double label_noise, sgdb_host_dataset** out);
+/* parse_libsvm (dataset.hpp:101). declared_d < 0 = none. On SGDB_ERR_PARSE
+ * *error_line is the 1-based line number. */
+sgdb_status sgdb_parse_libsvm(const char* text, uint64_t len, int64_t declared_d,
+                              sgdb_host_dataset** out, uint64_t* error_line);
+/* write_libsvm (dataset.hpp:104): *len_out = bytes needed; text written when cap suffices. */
+sgdb_status sgdb_write_libsvm(const sgdb_dataset_view* view, char* buf, uint64_t cap,
+                              uint64_t* len_out);
+/* save_binary / load_binary (dataset.hpp:107-109), magic "sgdbds01". */
+sgdb_status sgdb_save_binary(const sgdb_dataset_view* view, const char* path);
+sgdb_status sgdb_load_binary(const char* path, sgdb_host_dataset** out);
+/* convert_layout (dataset.hpp:117-118); max_dense_bytes 0 = 2 GiB default. */
+sgdb_status sgdb_convert_layout(const sgdb_dataset_view* view, int32_t target,
+                                uint64_t max_dense_bytes, sgdb_host_dataset** out);
+/* Dataset::validate (dataset.hpp:56). */
+sgdb_status sgdb_validate_dataset(const sgdb_dataset_view* view);
+sgdb_status sgdb_host_dataset_view(const sgdb_host_dataset* h, sgdb_dataset_view* out);
+sgdb_status sgdb_host_dataset_free(sgdb_host_dataset* h);
+
+/* assign (dataset.hpp:153): lists flattened in worker order; offsets has
+ * workers+1 entries. Pass NULL arrays to query *total. */
+sgdb_status sgdb_assign(uint64_t n, uint64_t workers, int32_t strategy, uint64_t k,
+                        uint32_t* ids_out, uint64_t* offsets_out, uint64_t* total);
+/* parse_plan / plan_to_string / validate_plan (async_engine.hpp:40-47).
+ * Parsing fills the reference defaults (workers 1, group 32, offsets on,
+ * merge period 1, lanes auto). */
+sgdb_status sgdb_parse_plan(const char* text, sgdb_plan* out);
+sgdb_status sgdb_plan_to_string(const sgdb_plan* plan, char* buf, uint64_t cap);
+sgdb_status sgdb_validate_plan(const sgdb_plan* plan, int32_t layout);
+
+/* The mini-batch schedule of sync::train (sync_engine.cpp:75-84):
+ * mt19937_64(seed), iota, one std::shuffle per epoch when shuffle != 0. */
+sgdb_status sgdb_schedule_create(uint64_t seed, uint64_t n, int32_t shuffle, sgdb_schedule** out);
+sgdb_status sgdb_schedule_next(sgdb_schedule* s, uint32_t* order_out);
+sgdb_status sgdb_schedule_free(sgdb_schedule* s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SGDB_H_ */

@@ -1,0 +1,573 @@
+// Layer 1 of include/sgdb.h: device context, device-resident dataset and
+// model, and the per-epoch device ops (sync epoch, batch gradient, Hogwild
+// epoch, replica averaging, loss). Host code only; kernels live in
+// kernels_sync.cu / kernels_hogwild.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "device.hpp"
+#include "errors.hpp"
+
+using namespace sgdb::dev;
+
+namespace sgdb::detail {
+namespace {
+thread_local std::string g_last_error;
+thread_local uint64_t g_parse_line = 0;
+}  // namespace
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+void set_parse_line(uint64_t line) { g_parse_line = line; }
+uint64_t parse_line() { return g_parse_line; }
+}  // namespace sgdb::detail
+
+namespace {
+
+void require(bool cond, const char* msg) {
+  if (!cond) throw std::invalid_argument(msg);
+}
+
+template <class T>
+void h2d(T* dst, const T* src, uint64_t count, cudaStream_t s) {
+  if (count) check(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+}
+
+// CSC of a CSR matrix by counting sort; rows stay ascending inside a column.
+void csc_from_csr(uint64_t n, uint64_t d, const std::vector<uint32_t>& rowptr,
+                  const std::vector<uint32_t>& idx, const std::vector<float>& val,
+                  std::vector<uint32_t>& colptr, std::vector<uint32_t>& crow,
+                  std::vector<float>& cval) {
+  const uint64_t nnz = idx.size();
+  colptr.assign(d + 1, 0);
+  for (uint64_t s = 0; s < nnz; ++s) ++colptr[idx[s] + 1];
+  for (uint64_t j = 0; j < d; ++j) colptr[j + 1] += colptr[j];
+  std::vector<uint32_t> next(colptr.begin(), colptr.end() - 1);
+  crow.resize(nnz);
+  cval.resize(nnz);
+  for (uint64_t r = 0; r < n; ++r)
+    for (uint32_t s = rowptr[r]; s < rowptr[r + 1]; ++s) {
+      const uint32_t pos = next[idx[s]]++;
+      crow[pos] = static_cast<uint32_t>(r);
+      cval[pos] = val[s];
+    }
+}
+
+void upload_csr(sgdb_dataset* ds, std::vector<uint32_t>& rowptr, std::vector<uint32_t>& idx,
+                std::vector<float>& val) {
+  cudaStream_t s = ds->ctx->stream;
+  ds->kind = Kind::Csr;
+  ds->nnz = idx.size();
+  ds->val.alloc(std::max<uint64_t>(1, ds->nnz));
+  ds->idx.alloc(std::max<uint64_t>(1, ds->nnz));
+  ds->rowptr.alloc(ds->n + 1);
+  h2d(ds->val.p, val.data(), ds->nnz, s);
+  h2d(ds->idx.p, idx.data(), ds->nnz, s);
+  h2d(ds->rowptr.p, rowptr.data(), ds->n + 1, s);
+  std::vector<uint32_t> colptr, crow;
+  std::vector<float> cval;
+  csc_from_csr(ds->n, ds->d, rowptr, idx, val, colptr, crow, cval);
+  ds->cval.alloc(std::max<uint64_t>(1, ds->nnz));
+  ds->crow.alloc(std::max<uint64_t>(1, ds->nnz));
+  ds->colptr.alloc(ds->d + 1);
+  h2d(ds->cval.p, cval.data(), ds->nnz, s);
+  h2d(ds->crow.p, crow.data(), ds->nnz, s);
+  h2d(ds->colptr.p, colptr.data(), ds->d + 1, s);
+  ds->csc_built = true;
+  ds->coef.alloc(std::max<uint64_t>(1, ds->n));
+  check(cudaStreamSynchronize(s), "upload sync");  // host vectors die with the caller
+}
+
+uint64_t nonempty_workers(uint64_t n, uint64_t T, bool rr) {
+  if (rr) return std::min(n, T);
+  const uint64_t chunk = (n + T - 1) / T;
+  return (n + chunk - 1) / chunk;
+}
+
+void set_finite(sgdb_model* m) {
+  static const int one = 1;
+  check(cudaMemcpyAsync(m->finite.p, &one, sizeof(int), cudaMemcpyHostToDevice, m->ctx->stream),
+        "set finite");
+}
+
+int read_finite(sgdb_model* m) {
+  int f = 0;
+  check(cudaMemcpyAsync(&f, m->finite.p, sizeof(int), cudaMemcpyDeviceToHost, m->ctx->stream),
+        "read finite");
+  check(cudaStreamSynchronize(m->ctx->stream), "sync");
+  return f;
+}
+
+void call_allreduce(Ctx& c, void* ptr, uint64_t count, int dtype) {
+  if (!c.allreduce) return;
+  if (c.allreduce(c.allreduce_user, ptr, count, dtype, c.stream) != 0)
+    throw std::runtime_error("allreduce hook failed");
+}
+
+void validate_device_plan(const sgdb_plan& p, int layout) {
+  sgdb_status st = sgdb_validate_plan(&p, layout);
+  if (st != SGDB_OK) throw std::invalid_argument(sgdb_last_error());
+}
+
+void model_init(sgdb_model* m, Ctx* c, uint64_t d) {
+  m->ctx = c;
+  m->d = d;
+  m->w32.alloc(d + 1);
+  m->w64.alloc(std::max<uint64_t>(1, d));
+  m->g64.alloc(std::max<uint64_t>(1, d));
+  m->ticket.alloc(1);
+  m->finite.alloc(1);
+  m->scal.alloc(2);
+  m->w32.zero(c->stream);
+  m->w64.zero(c->stream);
+  m->g64.zero(c->stream);
+  m->ticket.zero(c->stream);
+  m->scal.zero(c->stream);
+  set_finite(m);
+}
+
+void model_set(sgdb_model* m, const double* w) {
+  Ctx& c = *m->ctx;
+  std::vector<float> w32(m->d + 1, 0.f);
+  for (uint64_t j = 0; j < m->d; ++j) w32[j] = static_cast<float>(w[j]);
+  h2d(m->w64.p, w, m->d, c.stream);
+  h2d(m->w32.p, w32.data(), m->d + 1, c.stream);
+  check(cudaStreamSynchronize(c.stream), "model_set sync");
+}
+
+void full_step(sgdb_dataset* ds, sgdb_model* m, const StepArgs& a) {
+  if (ds->kind == Kind::Dense) dense_full_step(*ds, *m, a);
+  else csr_full_step(*ds, *m, a);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sgdb_last_error(void) { return sgdb::detail::g_last_error.c_str(); }
+const char* sgdb_version(void) { return "sgdb_b200 0.1 (sm_100a)"; }
+
+sgdb_status sgdb_ctx_create(int32_t device, void* cuda_stream, sgdb_ctx** out) {
+  return sgdb_guard([&] {
+    require(out != nullptr, "out is null");
+    check(cudaSetDevice(device), "cudaSetDevice");
+    auto* c = new sgdb_ctx();
+    c->device = device;
+    cudaDeviceProp prop{};
+    check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major < 10)
+      throw sgdb::detail::UnsupportedError("sgdb_b200 is built for sm_100a (Blackwell); found sm_" +
+                                           std::to_string(prop.major * 10 + prop.minor));
+    c->num_sms = prop.multiProcessorCount;
+    c->max_threads_per_sm = prop.maxThreadsPerMultiProcessor;
+    c->max_smem_optin = prop.sharedMemPerBlockOptin;
+    if (cuda_stream) {
+      c->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+      check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      c->own_stream = true;
+    }
+    c->loss_out.alloc(2);
+    c->tickets.alloc(4);
+    c->tickets.zero(c->stream);
+    *out = c;
+  });
+}
+
+sgdb_status sgdb_ctx_destroy(sgdb_ctx* ctx) {
+  return sgdb_guard([&] {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+sgdb_status sgdb_ctx_stream(sgdb_ctx* ctx, void** stream_out) {
+  return sgdb_guard([&] { *stream_out = ctx->stream; });
+}
+
+sgdb_status sgdb_ctx_synchronize(sgdb_ctx* ctx) {
+  return sgdb_guard([&] { check(cudaStreamSynchronize(ctx->stream), "synchronize"); });
+}
+
+sgdb_status sgdb_ctx_launch_count(sgdb_ctx* ctx, uint64_t* out) {
+  return sgdb_guard([&] { *out = ctx->launches; });
+}
+
+sgdb_status sgdb_ctx_set_allreduce(sgdb_ctx* ctx, sgdb_allreduce_fn fn, void* user) {
+  return sgdb_guard([&] {
+    ctx->allreduce = fn;
+    ctx->allreduce_user = user;
+  });
+}
+
+sgdb_status sgdb_ctx_resident_workers(sgdb_ctx* ctx, const sgdb_dataset* ds, int32_t lanes,
+                                      uint64_t* out) {
+  return sgdb_guard([&] {
+    int g = lanes > 0 ? lanes : hogwild_auto_lanes(*ds, SGDB_ACCESS_ROW_CH);
+    *out = hogwild_resident_workers(*ctx, g);
+  });
+}
+
+sgdb_status sgdb_dataset_upload(sgdb_ctx* ctx, const sgdb_dataset_view* v, uint64_t row_base,
+                                uint64_t n_global, sgdb_dataset** out) {
+  return sgdb_guard([&] {
+    require(ctx && v && out, "null argument");
+    const uint64_t n = v->n_examples, d = v->n_features;
+    require(n == 0 || v->labels != nullptr, "labels missing");
+    if (n_global == 0) n_global = n;
+    require(row_base + n <= n_global, "shard exceeds n_global");
+    require(n_global <= 0xFFFFFFFFull, "example ids must fit in 32 bits");
+    auto* ds = new sgdb_dataset();
+    std::unique_ptr<sgdb_dataset> guard(ds);
+    ds->ctx = ctx;
+    ds->n = n;
+    ds->d = d;
+    ds->row_base = row_base;
+    ds->n_global = n_global;
+    ds->layout_in = v->layout;
+    cudaStream_t s = ctx->stream;
+
+    const uint64_t nlab = ((n + 3) & ~uint64_t(3)) + 8;
+    std::vector<float> lab(nlab, 0.f);
+    for (uint64_t e = 0; e < n; ++e) lab[e] = static_cast<float>(v->labels[e]);
+    ds->labels.alloc(nlab);
+    h2d(ds->labels.p, lab.data(), nlab, s);
+
+    switch (v->layout) {
+      case SGDB_LAYOUT_DENSE_ROW:
+      case SGDB_LAYOUT_DENSE_COL: {
+        require(v->n_values == n * d, "dense storage size mismatch");
+        const bool colmajor = v->layout == SGDB_LAYOUT_DENSE_COL;
+        if (d <= 1024) {
+          ds->kind = Kind::Dense;
+          ds->nnz = n * d;
+          std::vector<float> x(n * d + 8, 0.f);
+          for (uint64_t e = 0; e < n; ++e)
+            for (uint64_t j = 0; j < d; ++j)
+              x[e * d + j] = static_cast<float>(colmajor ? v->values[j * n + e] : v->values[e * d + j]);
+          ds->x.alloc(x.size());
+          h2d(ds->x.p, x.data(), x.size(), s);
+          check(cudaStreamSynchronize(s), "upload sync");
+        } else {
+          // Wide dense data: CSR with every coordinate stored (zeros kept so the
+          // dot products visit all d slots as for_example does).
+          require(n * d < 0xFFFFFFFFull, "dense matrix too large for 32-bit offsets");
+          std::vector<uint32_t> rowptr(n + 1), idx(n * d);
+          std::vector<float> val(n * d);
+          for (uint64_t e = 0; e < n; ++e) {
+            rowptr[e] = static_cast<uint32_t>(e * d);
+            for (uint64_t j = 0; j < d; ++j) {
+              idx[e * d + j] = static_cast<uint32_t>(j);
+              val[e * d + j] =
+                  static_cast<float>(colmajor ? v->values[j * n + e] : v->values[e * d + j]);
+            }
+          }
+          rowptr[n] = static_cast<uint32_t>(n * d);
+          upload_csr(ds, rowptr, idx, val);
+        }
+        break;
+      }
+      case SGDB_LAYOUT_CSR: {
+        require(v->n_row_offsets == n + 1 && v->row_offsets, "csr row_offsets size mismatch");
+        require(v->n_indices == v->n_values, "csr index/value size mismatch");
+        const uint64_t nnz = v->n_values;
+        require(nnz < 0xFFFFFFFFull, "nnz must fit in 32-bit row offsets");
+        std::vector<uint32_t> rowptr(n + 1), idx(v->indices, v->indices + nnz);
+        std::vector<float> val(nnz);
+        for (uint64_t e = 0; e <= n; ++e) rowptr[e] = static_cast<uint32_t>(v->row_offsets[e]);
+        for (uint64_t s2 = 0; s2 < nnz; ++s2) {
+          require(idx[s2] < d, "csr feature index out of range");
+          val[s2] = static_cast<float>(v->values[s2]);
+        }
+        upload_csr(ds, rowptr, idx, val);
+        break;
+      }
+      case SGDB_LAYOUT_PADDED: {
+        const uint64_t pw = v->padded_width;
+        require(v->n_values == n * pw && v->n_indices == n * pw, "padded storage size mismatch");
+        std::vector<uint32_t> rowptr(n + 1, 0), idx;
+        std::vector<float> val;
+        for (uint64_t e = 0; e < n; ++e) {
+          for (uint64_t sl = 0; sl < pw; ++sl) {
+            const uint32_t j = v->indices[sl * n + e];
+            if (j == d) continue;  // sentinel
+            require(j < d, "padded feature index out of range");
+            idx.push_back(j);
+            val.push_back(static_cast<float>(v->values[sl * n + e]));
+          }
+          rowptr[e + 1] = static_cast<uint32_t>(idx.size());
+        }
+        std::vector<float> pval(std::max<uint64_t>(1, n * pw));
+        for (uint64_t i = 0; i < n * pw; ++i) pval[i] = static_cast<float>(v->values[i]);
+        ds->pw = pw;
+        ds->pval.alloc(pval.size());
+        ds->pidx.alloc(std::max<uint64_t>(1, n * pw));
+        h2d(ds->pval.p, pval.data(), n * pw, s);
+        h2d(ds->pidx.p, v->indices, n * pw, s);
+        ds->col_built = true;
+        upload_csr(ds, rowptr, idx, val);
+        break;
+      }
+      default:
+        throw std::invalid_argument("unknown layout");
+    }
+    ds->order.alloc(std::max<uint64_t>(1, n_global));
+    check(cudaStreamSynchronize(s), "upload sync");
+    *out = guard.release();
+  });
+}
+
+sgdb_status sgdb_dataset_refresh_f32(sgdb_ctx* ctx, sgdb_dataset* ds, const float* values,
+                                     const float* labels, const uint32_t* indices,
+                                     const uint32_t* row_offsets32) {
+  return sgdb_guard([&] {
+    cudaStream_t s = ctx->stream;
+    if (labels) h2d(ds->labels.p, labels, ds->n, s);
+    if (ds->kind == Kind::Dense) {
+      if (values) h2d(ds->x.p, values, ds->n * ds->d, s);
+    } else {
+      if (values) h2d(ds->val.p, values, ds->nnz, s);
+      if (indices) h2d(ds->idx.p, indices, ds->nnz, s);
+      if (row_offsets32) h2d(ds->rowptr.p, row_offsets32, ds->n + 1, s);
+    }
+  });
+}
+
+sgdb_status sgdb_dataset_free(sgdb_dataset* ds) {
+  return sgdb_guard([&] {
+    if (!ds) return;
+    cudaStreamSynchronize(ds->ctx->stream);
+    delete ds;
+  });
+}
+
+sgdb_status sgdb_dataset_sweep_bytes(const sgdb_dataset* ds, uint64_t* out) {
+  return sgdb_guard([&] {
+    if (ds->kind == Kind::Dense) *out = ds->n * ds->d * 4 + ds->n * 4;
+    else *out = ds->nnz * 8 + (ds->n + 1) * 4 + ds->n * 4;
+  });
+}
+
+sgdb_status sgdb_dataset_shape(const sgdb_dataset* ds, uint64_t* n_local, uint64_t* d,
+                               uint64_t* nnz, uint64_t* row_base, uint64_t* n_global) {
+  return sgdb_guard([&] {
+    if (n_local) *n_local = ds->n;
+    if (d) *d = ds->d;
+    if (nnz) *nnz = ds->nnz;
+    if (row_base) *row_base = ds->row_base;
+    if (n_global) *n_global = ds->n_global;
+  });
+}
+
+sgdb_status sgdb_model_create(sgdb_ctx* ctx, uint64_t d, const double* init, sgdb_model** out) {
+  return sgdb_guard([&] {
+    auto* m = new sgdb_model();
+    std::unique_ptr<sgdb_model> guard(m);
+    model_init(m, ctx, d);
+    if (init) model_set(m, init);
+    check(cudaStreamSynchronize(ctx->stream), "model sync");
+    *out = guard.release();
+  });
+}
+
+sgdb_status sgdb_model_set(sgdb_ctx*, sgdb_model* m, const double* w) {
+  return sgdb_guard([&] { model_set(m, w); });
+}
+
+sgdb_status sgdb_model_get(sgdb_ctx*, sgdb_model* m, double* w_out) {
+  return sgdb_guard([&] {
+    Ctx& c = *m->ctx;
+    if (m->d)
+      check(cudaMemcpyAsync(w_out, m->w64.p, m->d * sizeof(double), cudaMemcpyDeviceToHost,
+                            c.stream),
+            "D2H model");
+    check(cudaStreamSynchronize(c.stream), "model_get sync");
+  });
+}
+
+sgdb_status sgdb_model_device_ptrs(sgdb_model* m, float** w32, double** w64) {
+  return sgdb_guard([&] {
+    if (w32) *w32 = m->w32.p;
+    if (w64) *w64 = m->w64.p;
+  });
+}
+
+sgdb_status sgdb_model_free(sgdb_model* m) {
+  return sgdb_guard([&] {
+    if (!m) return;
+    cudaStreamSynchronize(m->ctx->stream);
+    delete m;
+  });
+}
+
+sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
+                            double alpha, const uint32_t* order, uint64_t batch_b,
+                            int32_t* finite_out) {
+  return sgdb_guard([&] {
+    require(ctx && ds && m, "null argument");
+    require(m->d == ds->d, "model/dataset dim mismatch");
+    require(batch_b >= 1, "batch size must be in [1, N]");
+    Ctx& c = *ctx;
+    set_finite(m);
+    const bool hook = c.allreduce != nullptr;
+    StepArgs a;
+    a.task = task;
+    a.alpha = alpha;
+    a.apply = !hook;
+    if (batch_b >= ds->n_global) {
+      full_step(ds, m, a);
+      if (hook) {
+        call_allreduce(c, m->g64.p, m->d, 1);
+        apply_update(*m, alpha, false);
+      }
+    } else {
+      const uint64_t ng = ds->n_global;
+      if (order) {
+        h2d(ds->order.p, order, ng, c.stream);
+      } else {
+        std::vector<uint32_t> iota(ng);
+        std::iota(iota.begin(), iota.end(), 0u);
+        h2d(ds->order.p, iota.data(), ng, c.stream);
+        check(cudaStreamSynchronize(c.stream), "order sync");
+      }
+      for (uint64_t lo = 0; lo < ng; lo += batch_b) {
+        const uint64_t nb = std::min(batch_b, ng - lo);
+        const uint32_t* ids = ds->order.p + lo;
+        if (ds->kind == Kind::Dense) dense_batch_step(*ds, *m, ids, nb, a);
+        else csr_batch_step(*ds, *m, ids, nb, a);
+        if (hook) {
+          call_allreduce(c, m->g64.p, m->d, 1);
+          apply_update(*m, alpha, false);
+        }
+      }
+    }
+    const int f = read_finite(m);
+    if (finite_out) *finite_out = f;
+  });
+}
+
+sgdb_status sgdb_batch_gradient(sgdb_ctx* ctx, sgdb_dataset* ds, int32_t task,
+                                const uint32_t* rows, uint64_t n_rows, const double* w,
+                                double* g_out) {
+  return sgdb_guard([&] {
+    require(ctx && ds && w && g_out, "null argument");
+    Ctx& c = *ctx;
+    sgdb_model tmp;
+    model_init(&tmp, ctx, ds->d);
+    model_set(&tmp, w);
+    StepArgs a;
+    a.task = task;
+    a.apply = false;
+    if (n_rows == 0) {
+      full_step(ds, &tmp, a);
+    } else {
+      DBuf<uint32_t> ids;
+      ids.alloc(n_rows);
+      h2d(ids.p, rows, n_rows, c.stream);
+      if (ds->kind == Kind::Dense) dense_batch_step(*ds, tmp, ids.p, n_rows, a);
+      else csr_batch_step(*ds, tmp, ids.p, n_rows, a);
+      check(cudaStreamSynchronize(c.stream), "batch_gradient sync");
+    }
+    call_allreduce(c, tmp.g64.p, ds->d, 1);
+    if (ds->d)
+      check(cudaMemcpyAsync(g_out, tmp.g64.p, ds->d * sizeof(double), cudaMemcpyDeviceToHost,
+                            c.stream),
+            "D2H gradient");
+    check(cudaStreamSynchronize(c.stream), "batch_gradient sync");
+  });
+}
+
+sgdb_status sgdb_epoch_batch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
+                             double alpha, double* grad_norm_out) {
+  return sgdb_guard([&] {
+    require(m->d == ds->d, "model/dataset dim mismatch");
+    Ctx& c = *ctx;
+    check(cudaMemsetAsync(m->scal.p, 0, sizeof(double), c.stream), "memset norm");
+    StepArgs a;
+    a.task = task;
+    a.alpha = alpha;
+    a.apply = c.allreduce == nullptr;
+    a.want_norm = true;
+    set_finite(m);
+    full_step(ds, m, a);
+    if (c.allreduce) {
+      call_allreduce(c, m->g64.p, m->d, 1);
+      apply_update(*m, alpha, true);
+    }
+    double sq = 0.0;
+    check(cudaMemcpyAsync(&sq, m->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+          "D2H norm");
+    check(cudaStreamSynchronize(c.stream), "epoch_batch sync");
+    if (grad_norm_out) *grad_norm_out = std::sqrt(sq);
+  });
+}
+
+sgdb_status sgdb_hogwild_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
+                               double alpha, const sgdb_plan* plan, uint64_t* evals_out) {
+  return sgdb_guard([&] {
+    require(ctx && ds && m && plan, "null argument");
+    require(m->d == ds->d, "model/dataset dim mismatch");
+    require(ds->n >= 1, "cannot train on an empty dataset");
+    validate_device_plan(*plan, ds->layout_in);
+    HogwildArgs a;
+    a.task = task;
+    a.alpha = static_cast<float>(alpha);
+    a.access = plan->access_path;
+    a.replication = plan->replication;
+    a.k = plan->data_replication_k;
+    a.workers = plan->workers;
+    a.group_size = plan->group_size;
+    a.offsets = plan->circular_offsets != 0;
+    a.lanes = plan->lanes_per_worker > 0 ? plan->lanes_per_worker
+                                         : hogwild_auto_lanes(*ds, plan->access_path);
+    require(a.lanes == 1 || a.lanes == 2 || a.lanes == 4 || a.lanes == 8 || a.lanes == 16 ||
+                a.lanes == 32,
+            "lanes_per_worker must be 1, 2, 4, 8, 16 or 32");
+    hogwild_epoch(*ds, *m, a);
+    check(cudaStreamSynchronize(ctx->stream), "hogwild sync");
+    if (evals_out) {
+      const bool rr = plan->access_path == SGDB_ACCESS_ROW_RR || plan->access_path == SGDB_ACCESS_COL_RR;
+      *evals_out = ds->n + nonempty_workers(ds->n, plan->workers, rr) * plan->data_replication_k;
+    }
+  });
+}
+
+sgdb_status sgdb_models_average(sgdb_ctx* ctx, sgdb_model* const* models, uint64_t count,
+                                const double* weights, sgdb_model* out, int32_t refresh) {
+  return sgdb_guard([&] {
+    require(count > 0, "merge_models: no replicas");
+    std::vector<Model*> ms(count);
+    for (uint64_t i = 0; i < count; ++i) ms[i] = models[i];
+    average_models(*ctx, ms.data(), count, weights, *out, refresh != 0);
+  });
+}
+
+sgdb_status sgdb_loss(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
+                      double* loss_out) {
+  return sgdb_guard([&] {
+    require(m->d == ds->d, "model/dataset dim mismatch");
+    Ctx& c = *ctx;
+    loss_launch(*ds, *m, task);
+    call_allreduce(c, c.loss_out.p, 1, 1);
+    double l = 0.0;
+    check(cudaMemcpyAsync(&l, c.loss_out.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+          "D2H loss");
+    check(cudaStreamSynchronize(c.stream), "loss sync");
+    *loss_out = l;
+  });
+}
+
+}  // extern "C"
+
+namespace sgdb::dev {
+void build_csc(Dataset& ds) {
+  if (!ds.csc_built) throw Unsupported("CSC copy missing (dataset was not uploaded as CSR)");
+}
+}  // namespace sgdb::dev

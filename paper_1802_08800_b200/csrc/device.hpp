@@ -1,0 +1,167 @@
+// Internal device-side objects behind the C-ABI handles of include/sgdb.h and
+// the kernel launchers (kernels_*.cu). Host-only header (no device code).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "errors.hpp"
+#include "sgdb.h"
+
+namespace sgdb::dev {
+
+using CudaError = sgdb::detail::DeviceError;
+using Unsupported = sgdb::detail::UnsupportedError;
+
+inline void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Owning device allocation.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  uint64_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(uint64_t count) {
+    if (count <= n && p) return;
+    release();
+    check(cudaMalloc(&p, (count ? count : 1) * sizeof(T)), "cudaMalloc");
+    n = count;
+  }
+  void zero(cudaStream_t s) {
+    if (p) check(cudaMemsetAsync(p, 0, n * sizeof(T), s), "cudaMemsetAsync");
+  }
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  int max_threads_per_sm = 2048;
+  size_t max_smem_optin = 227 * 1024;
+  uint64_t launches = 0;
+  sgdb_allreduce_fn allreduce = nullptr;
+  void* allreduce_user = nullptr;
+  DBuf<double> loss_partials;  // per-block loss sums
+  DBuf<double> loss_out;       // [0] loss, [1] scratch
+  DBuf<unsigned> tickets;      // [0] loss ticket
+};
+
+// Device storage kind chosen at upload.
+enum class Kind { Dense, Csr };
+
+struct Dataset {
+  Ctx* ctx = nullptr;
+  uint64_t n = 0;  // local rows
+  uint64_t d = 0;
+  uint64_t row_base = 0, n_global = 0;
+  int layout_in = SGDB_LAYOUT_CSR;
+  Kind kind = Kind::Csr;
+  uint64_t nnz = 0;  // stored entries (CSR) or n*d (dense)
+  DBuf<float> labels;  // n (padded to a multiple of 4 + tile slack)
+  // Dense row-major fp32, n*d (+ slack so bulk copies may round up to 16 B).
+  DBuf<float> x;
+  // CSR.
+  DBuf<float> val;
+  DBuf<uint32_t> idx;
+  DBuf<uint32_t> rowptr;
+  // CSC of the local rows (built lazily for full-batch sparse gradients).
+  bool csc_built = false;
+  DBuf<float> cval;
+  DBuf<uint32_t> crow;
+  DBuf<uint32_t> colptr;
+  // Column-major copies for the col-* access paths (built lazily).
+  bool col_built = false;
+  DBuf<float> xcol;    // dense: d*n
+  DBuf<float> pval;    // padded slot-major: pw*n
+  DBuf<uint32_t> pidx;
+  uint64_t pw = 0;
+  // Host copies kept for lazy builds (CSR arrays, only when needed).
+  std::vector<float> h_val;
+  std::vector<uint32_t> h_idx;
+  std::vector<uint32_t> h_rowptr;
+  std::vector<float> h_xcol;
+  // Scratch.
+  DBuf<float> coef;        // per local row coefficient (sparse full batch)
+  DBuf<uint32_t> order;    // n_global ids of the current epoch
+};
+
+struct Model {
+  Ctx* ctx = nullptr;
+  uint64_t d = 0;
+  DBuf<float> w32;       // d+1 (guard slot d == 0)
+  DBuf<double> w64;      // d, master
+  DBuf<double> g64;      // d, gradient accumulator (kept zeroed between steps)
+  DBuf<double> partials; // per-block gradient partials, deterministic full batch
+  DBuf<unsigned> ticket; // [0] grad ticket
+  DBuf<int> finite;      // [0] 1 while every gradient entry was finite
+  DBuf<double> scal;     // [0] ||g||^2
+  DBuf<float> replicas;  // Hogwild replicas, R x ld
+  uint64_t n_replicas = 0, replica_ld = 0;
+};
+
+// ---- launchers (kernels_*.cu) -------------------------------------------------
+
+struct StepArgs {
+  int task = 0;
+  double alpha = 0.0;
+  bool apply = true;      // fuse w -= alpha*g (else g64 holds the gradient)
+  bool want_norm = false; // accumulate ||g||^2 into model.scal[0]
+};
+
+// Dense, all local rows: one full-batch gradient (deterministic).
+void dense_full_step(Dataset& ds, Model& m, const StepArgs& a);
+// Dense, rows = global ids ids[0..nb) (device pointer), mini-batch gradient.
+void dense_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb,
+                      const StepArgs& a);
+// Sparse, all local rows: margin/coef pass + CSC gradient pass.
+void csr_full_step(Dataset& ds, Model& m, const StepArgs& a);
+// Sparse mini-batch: scatter with fp64 atomics, then apply.
+void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, const StepArgs& a);
+// w -= alpha*g64; w32 = w64; finite; g64 = 0.
+void apply_update(Model& m, double alpha, bool want_norm);
+// fp64 loss over all local rows; result left in ctx.loss_out[0] (device).
+void loss_launch(Dataset& ds, Model& m, int task);
+// w64 = (double) w32[0..d)
+void sync_w64_from_w32(Model& m);
+// Weighted mean of models (w64) -> out; refresh copies it back to each input.
+void average_models(Ctx& c, Model* const* models, uint64_t count, const double* weights,
+                    Model& out, bool refresh);
+
+struct HogwildArgs {
+  int task = 0;
+  float alpha = 0.f;
+  int access = 0;        // sgdb_access_path
+  int replication = 0;   // sgdb_replication
+  uint64_t k = 0, workers = 1, group_size = 32;
+  bool offsets = true;
+  int lanes = 0;         // resolved lanes per worker
+};
+int hogwild_auto_lanes(const Dataset& ds, int access);
+uint64_t hogwild_resident_workers(const Ctx& c, int lanes);
+void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a);
+
+void build_csc(Dataset& ds);
+void build_col(Dataset& ds);
+
+}  // namespace sgdb::dev
+
+// Opaque C handles are the internal objects.
+struct sgdb_ctx : sgdb::dev::Ctx {};
+struct sgdb_dataset : sgdb::dev::Dataset {};
+struct sgdb_model : sgdb::dev::Model {};

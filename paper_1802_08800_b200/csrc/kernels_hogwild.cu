@@ -1,0 +1,470 @@
+// Asynchronous Hogwild kernels (sm_100a) — the paper's accelerator
+// contribution (§5 "do in parallel" Alg. 3).
+//
+// Replaces hogwild::Instance::worker_loop + process_examples
+// (proj/src/async_engine.cpp:178-195, :372-396) and the replica prepare /
+// merge (:293-331, merge_models :133-156). A reference "worker" walking its
+// assign() list (proj/src/dataset.cpp:470-503) is a group of G lanes here
+// (G = 32: one warp per example); the group gathers the model at the
+// example's support, reduces the margin with shuffles, and writes the update
+// back without locks. Lost updates between workers are allowed by design
+// (async_engine.hpp:49-52); within a group every lane owns distinct
+// coordinates.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "common.cuh"
+#include "device.hpp"
+
+namespace sgdb::dev {
+
+namespace {
+
+constexpr int kKindDenseRow = 0;  // row-major dense, idx implicit
+constexpr int kKindCsr = 1;       // CSR rows
+constexpr int kKindDenseCol = 2;  // column-major dense (stride n)
+constexpr int kKindPaddedCol = 3; // slot-major padded (stride n, sentinel d)
+
+constexpr int kScopeShared = 0;   // one model in global memory (kernel scope)
+constexpr int kScopeGlobalRep = 1;// replicas in global memory, replica = worker / gs
+
+struct HogParams {
+  const float* val;
+  const uint32_t* idx;
+  const uint32_t* rowptr;
+  const float* y;
+  uint64_t n;
+  uint64_t d;
+  uint64_t pw;
+  uint64_t T;
+  uint64_t k;
+  int rr;
+  uint64_t gs;
+  int offsets;
+  float* model;
+  uint64_t ld;
+  float alpha;
+};
+
+template <int G>
+__device__ __forceinline__ unsigned group_mask() {
+  if (G == 32) return 0xffffffffu;
+  const unsigned lane = threadIdx.x & 31;
+  return ((1u << G) - 1u) << (lane & ~(G - 1u));
+}
+
+template <int G>
+__device__ __forceinline__ float group_sum_m(float v, unsigned mask) {
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) v += __shfl_xor_sync(mask, v, off);
+  return v;
+}
+
+struct GlobalModel {
+  float* m;
+  __device__ float load(uint64_t j) const { return ld_model(m + j); }
+  __device__ void store(uint64_t j, float v) const { st_model(m + j, v); }
+};
+struct SmemModel {
+  volatile float* m;
+  __device__ float load(uint64_t j) const { return m[j]; }
+  __device__ void store(uint64_t j, float v) const { m[j] = v; }
+};
+
+// One example (process_examples body). Slot s of example e: value / index.
+template <int G, int TASK, int KIND, class M>
+__device__ __forceinline__ void process_example(const HogParams& p, const M& m, uint64_t e,
+                                                uint64_t wid, int lg, unsigned mask) {
+  uint64_t base, len, stride;
+  if (KIND == kKindCsr) {
+    base = p.rowptr[e];
+    len = p.rowptr[e + 1] - base;
+    stride = 1;
+  } else if (KIND == kKindDenseRow) {
+    base = e * p.d;
+    len = p.d;
+    stride = 1;
+  } else if (KIND == kKindDenseCol) {
+    base = e;
+    len = p.d;
+    stride = p.n;
+  } else {
+    base = e;
+    len = p.pw;
+    stride = p.n;
+  }
+  auto index = [&](uint64_t s) -> uint64_t {
+    if (KIND == kKindCsr) return __ldg(p.idx + base + s);
+    if (KIND == kKindPaddedCol) return __ldg(p.idx + base + s * stride);
+    return s;
+  };
+  auto value = [&](uint64_t s) -> float { return __ldg(p.val + base + s * stride); };
+
+  float z = 0.f;
+  for (uint64_t s = lg; s < len; s += G) z = fmaf(value(s), m.load(index(s)), z);
+  z = group_sum_m<G>(z, mask);
+  const float c = coef_f<TASK>(z, __ldg(p.y + e));
+  if (c == 0.f || len == 0) return;  // w - alpha*(0*x) == w: skip the no-op stores
+  const float ac = p.alpha;
+  if (G == 1 && p.offsets) {
+    // Circular offsets (async_engine.cpp:188-193): start at wid mod len.
+    uint64_t s = wid % len;
+    for (uint64_t i = 0; i < len; ++i) {
+      const uint64_t j = index(s);
+      m.store(j, m.load(j) - ac * (c * value(s)));
+      if (++s == len) s = 0;
+    }
+  } else {
+    for (uint64_t s = lg; s < len; s += G) {
+      const uint64_t j = index(s);
+      m.store(j, m.load(j) - ac * (c * value(s)));
+    }
+  }
+}
+
+// Worker w's assign() list (dataset.cpp:470-503), generated on the fly:
+// base ids then k wrapped extras after the last base id.
+struct WorkerList {
+  uint64_t first, step, cnt, total, last;
+};
+__device__ __forceinline__ WorkerList worker_list(const HogParams& p, uint64_t w) {
+  WorkerList l;
+  if (p.rr) {
+    l.cnt = w < p.n ? (p.n - 1 - w) / p.T + 1 : 0;
+    l.first = w;
+    l.step = p.T;
+  } else {
+    const uint64_t chunk = (p.n + p.T - 1) / p.T;
+    const uint64_t b = w * chunk, e = min(p.n, b + chunk);
+    l.cnt = e > b ? e - b : 0;
+    l.first = b;
+    l.step = 1;
+  }
+  l.total = l.cnt ? l.cnt + p.k : 0;
+  l.last = l.cnt ? l.first + (l.cnt - 1) * l.step : 0;
+  return l;
+}
+__device__ __forceinline__ uint64_t list_at(const HogParams& p, const WorkerList& l, uint64_t i) {
+  return i < l.cnt ? l.first + i * l.step : (l.last + 1 + (i - l.cnt)) % p.n;
+}
+
+// K5 (kernel scope, shared model) and the global-replica variant (block scope
+// with replicas too large for shared memory, thread scope).
+template <int G, int TASK, int KIND, int SCOPE>
+__global__ void __launch_bounds__(256) hogwild_kernel(HogParams p) {
+  const int lg = threadIdx.x % G;
+  const unsigned mask = group_mask<G>();
+  const uint64_t hg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const uint64_t HG = ((uint64_t)gridDim.x * blockDim.x) / G;
+  for (uint64_t w = hg; w < p.T; w += HG) {
+    GlobalModel m{SCOPE == kScopeShared ? p.model : p.model + (w / p.gs) * p.ld};
+    const WorkerList l = worker_list(p, w);
+    for (uint64_t i = 0; i < l.total; ++i)
+      process_example<G, TASK, KIND>(p, m, list_at(p, l, i), w, lg, mask);
+  }
+}
+
+// K6 (block scope): CTA r owns replica r in shared memory, loaded from the
+// global snapshot at epoch start (async_engine.cpp:298-301) and written to
+// replicas[r] at the end for K7. Workers r*gs .. r*gs+gs-1 run in the CTA.
+template <int G, int TASK, int KIND>
+__global__ void __launch_bounds__(1024) hogwild_smem_kernel(HogParams p, const float* w32,
+                                                            uint64_t R) {
+  extern __shared__ float rep[];
+  const int lg = threadIdx.x % G;
+  const unsigned mask = group_mask<G>();
+  const uint64_t gi = threadIdx.x / G, NG = blockDim.x / G;
+  for (uint64_t r = blockIdx.x; r < R; r += gridDim.x) {
+    for (uint64_t j = threadIdx.x; j <= p.d; j += blockDim.x) rep[j] = j < p.d ? w32[j] : 0.f;
+    __syncthreads();
+    SmemModel m{rep};
+    for (uint64_t t = gi; t < p.gs; t += NG) {
+      const uint64_t w = r * p.gs + t;
+      if (w >= p.T) break;
+      const WorkerList l = worker_list(p, w);
+      for (uint64_t i = 0; i < l.total; ++i)
+        process_example<G, TASK, KIND>(p, m, list_at(p, l, i), w, lg, mask);
+    }
+    __syncthreads();
+    for (uint64_t j = threadIdx.x; j < p.d; j += blockDim.x) p.model[r * p.ld + j] = rep[j];
+    __syncthreads();
+  }
+}
+
+// Replica prepare for the global-replica scope: every replica <- snapshot.
+__global__ void replicas_fill_kernel(float* reps, uint64_t R, uint64_t ld, uint64_t d,
+                                     const float* w32) {
+  const uint64_t total = R * ld;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = i % ld;
+    reps[i] = j < d ? w32[j] : 0.f;
+  }
+}
+
+// K7: global = unweighted mean of the replicas, summed in replica order in
+// fp64 (merge_models, async_engine.cpp:148-153).
+__global__ void replicas_merge_kernel(const float* reps, uint64_t R, uint64_t ld, uint64_t d,
+                                      double* w64, float* w32) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (uint64_t r = 0; r < R; ++r) s += 1.0 * static_cast<double>(reps[r * ld + j]);
+    const double v = s / static_cast<double>(R);
+    w64[j] = v;
+    w32[j] = static_cast<float>(v);
+  }
+}
+
+// Weighted mean over models' fp64 masters (merge_models with weights).
+__global__ void models_mean_kernel(const double* const* ws, const double* wts, uint64_t count,
+                                   double total, uint64_t d, double* out64, float* out32) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (uint64_t r = 0; r < count; ++r) s += (wts ? wts[r] : 1.0) * ws[r][j];
+    const double v = s / total;
+    out64[j] = v;
+    out32[j] = static_cast<float>(v);
+  }
+}
+
+__global__ void copy_model_kernel(uint64_t d, const double* src64, double* dst64, float* dst32) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    dst64[j] = src64[j];
+    dst32[j] = static_cast<float>(src64[j]);
+  }
+}
+
+// K8: dense row-major -> column-major (32x32 tiles through shared memory).
+__global__ void transpose_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                 uint64_t rows, uint64_t cols) {
+  __shared__ float tile[32][33];
+  const uint64_t bx = (uint64_t)blockIdx.x * 32, by = (uint64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const uint64_t r = by + i, c = bx + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const uint64_t c = bx + i, r = by + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
+void after_launch(Ctx& c, const char* what) {
+  ++c.launches;
+  check(cudaGetLastError(), what);
+}
+
+template <class Fn>
+void dispatch_lanes(int g, Fn&& fn) {
+  switch (g) {
+    case 1: fn.template operator()<1>(); break;
+    case 2: fn.template operator()<2>(); break;
+    case 4: fn.template operator()<4>(); break;
+    case 8: fn.template operator()<8>(); break;
+    case 16: fn.template operator()<16>(); break;
+    default: fn.template operator()<32>(); break;
+  }
+}
+
+template <class Fn>
+void dispatch_kind(int kind, Fn&& fn) {
+  switch (kind) {
+    case kKindDenseRow: fn.template operator()<kKindDenseRow>(); break;
+    case kKindCsr: fn.template operator()<kKindCsr>(); break;
+    case kKindDenseCol: fn.template operator()<kKindDenseCol>(); break;
+    default: fn.template operator()<kKindPaddedCol>(); break;
+  }
+}
+
+}  // namespace
+
+int hogwild_auto_lanes(const Dataset& ds, int access) {
+  if (access == SGDB_ACCESS_COL_RR || access == SGDB_ACCESS_COL_CH) return 1;
+  const double avg = ds.kind == Kind::Dense
+                         ? static_cast<double>(ds.d)
+                         : (ds.n ? static_cast<double>(ds.nnz) / static_cast<double>(ds.n) : 1.0);
+  if (avg <= 6.0) return 4;
+  if (avg <= 12.0) return 8;
+  if (avg <= 24.0) return 16;
+  return 32;
+}
+
+uint64_t hogwild_resident_workers(const Ctx& c, int lanes) {
+  return static_cast<uint64_t>(c.num_sms) * c.max_threads_per_sm / std::max(1, lanes);
+}
+
+void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
+  Ctx& c = *ds.ctx;
+  const bool col = a.access == SGDB_ACCESS_COL_RR || a.access == SGDB_ACCESS_COL_CH;
+  const bool rr = a.access == SGDB_ACCESS_ROW_RR || a.access == SGDB_ACCESS_COL_RR;
+  if (a.replication == SGDB_REPL_EXAMPLE)
+    throw Unsupported("example-scope replication is not implemented on the device");
+  if (ds.n_global != ds.n || ds.row_base != 0)
+    throw Unsupported("Hogwild epochs run on whole (replicated) datasets");
+
+  HogParams p{};
+  int kind;
+  if (col) {
+    build_col(ds);
+    if (ds.layout_in == SGDB_LAYOUT_PADDED) {
+      kind = kKindPaddedCol;
+      p.val = ds.pval.p;
+      p.idx = ds.pidx.p;
+      p.pw = ds.pw;
+    } else {
+      kind = kKindDenseCol;
+      p.val = ds.xcol.p;
+    }
+  } else if (ds.kind == Kind::Dense) {
+    kind = kKindDenseRow;
+    p.val = ds.x.p;
+  } else {
+    kind = kKindCsr;
+    p.val = ds.val.p;
+    p.idx = ds.idx.p;
+    p.rowptr = ds.rowptr.p;
+  }
+  p.y = ds.labels.p;
+  p.n = ds.n;
+  p.d = ds.d;
+  p.T = a.workers;
+  p.k = a.k;
+  p.rr = rr ? 1 : 0;
+  p.offsets = a.offsets ? 1 : 0;
+  p.alpha = a.alpha;
+  const int G = a.lanes;
+
+  const uint64_t resident_threads = static_cast<uint64_t>(c.num_sms) * c.max_threads_per_sm;
+  auto grid_threads = [&](uint64_t workers) {
+    const uint64_t threads = std::min<uint64_t>(workers * G, resident_threads);
+    return static_cast<unsigned>(std::max<uint64_t>(1, (threads + 255) / 256));
+  };
+
+  if (a.replication == SGDB_REPL_KERNEL) {
+    p.model = m.w32.p;
+    p.gs = 1;
+    p.ld = 0;
+    const unsigned grid = grid_threads(a.workers);
+    dispatch_lanes(G, [&]<int GL>() {
+      dispatch_kind(kind, [&]<int KD>() {
+        if (a.task == kTaskLR) hogwild_kernel<GL, kTaskLR, KD, kScopeShared><<<grid, 256, 0, c.stream>>>(p);
+        else hogwild_kernel<GL, kTaskSVM, KD, kScopeShared><<<grid, 256, 0, c.stream>>>(p);
+      });
+    });
+    after_launch(c, "hogwild_kernel");
+    sync_w64_from_w32(m);
+    return;
+  }
+
+  // Block (group_size workers per replica) or thread (one per worker) scope.
+  const uint64_t gs = a.replication == SGDB_REPL_THREAD ? 1 : a.group_size;
+  const uint64_t R = (a.workers + gs - 1) / gs;
+  const uint64_t ld = (ds.d + 1 + 31) & ~uint64_t(31);
+  m.replicas.alloc(R * ld);
+  m.n_replicas = R;
+  m.replica_ld = ld;
+  p.gs = gs;
+  p.ld = ld;
+  p.model = m.replicas.p;
+  const size_t rep_bytes = (ds.d + 1) * sizeof(float);
+  const bool smem_ok = a.replication == SGDB_REPL_BLOCK && rep_bytes + 1024 <= c.max_smem_optin;
+  if (smem_ok) {
+    uint64_t threads = std::min<uint64_t>(1024, gs * G);
+    threads = std::max<uint64_t>(32, (threads + 31) & ~uint64_t(31));
+    int blocks_per_sm = static_cast<int>(std::max<size_t>(1, (c.max_smem_optin) / (rep_bytes + 1024)));
+    blocks_per_sm = std::min<int>(blocks_per_sm, static_cast<int>(c.max_threads_per_sm / threads));
+    blocks_per_sm = std::max(1, blocks_per_sm);
+    const unsigned grid = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>(R, static_cast<uint64_t>(c.num_sms) * blocks_per_sm)));
+    dispatch_lanes(G, [&]<int GL>() {
+      dispatch_kind(kind, [&]<int KD>() {
+        auto kern = a.task == kTaskLR ? hogwild_smem_kernel<GL, kTaskLR, KD>
+                                      : hogwild_smem_kernel<GL, kTaskSVM, KD>;
+        check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(rep_bytes)),
+              "cudaFuncSetAttribute(hogwild_smem)");
+        kern<<<grid, static_cast<unsigned>(threads), rep_bytes, c.stream>>>(p, m.w32.p, R);
+      });
+    });
+    after_launch(c, "hogwild_smem_kernel");
+  } else {
+    const unsigned fill_grid = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>((R * ld + 255) / 256, c.num_sms * 8ull)));
+    replicas_fill_kernel<<<fill_grid, 256, 0, c.stream>>>(m.replicas.p, R, ld, ds.d, m.w32.p);
+    after_launch(c, "replicas_fill_kernel");
+    const unsigned grid = grid_threads(a.workers);
+    dispatch_lanes(G, [&]<int GL>() {
+      dispatch_kind(kind, [&]<int KD>() {
+        if (a.task == kTaskLR) hogwild_kernel<GL, kTaskLR, KD, kScopeGlobalRep><<<grid, 256, 0, c.stream>>>(p);
+        else hogwild_kernel<GL, kTaskSVM, KD, kScopeGlobalRep><<<grid, 256, 0, c.stream>>>(p);
+      });
+    });
+    after_launch(c, "hogwild_kernel(replicas)");
+  }
+  const unsigned mgrid = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>((ds.d + 255) / 256, c.num_sms * 8ull)));
+  replicas_merge_kernel<<<mgrid, 256, 0, c.stream>>>(m.replicas.p, R, ld, ds.d, m.w64.p, m.w32.p);
+  after_launch(c, "replicas_merge_kernel");
+}
+
+void average_models(Ctx& c, Model* const* models, uint64_t count, const double* weights,
+                    Model& out, bool refresh) {
+  const uint64_t d = out.d;
+  std::vector<const double*> ptrs(count);
+  double total = 0.0;
+  for (uint64_t i = 0; i < count; ++i) {
+    if (models[i]->d != d) throw std::invalid_argument("merge_models: dimension mismatch");
+    ptrs[i] = models[i]->w64.p;
+    total += weights ? weights[i] : 1.0;
+  }
+  if (weights && total == 0.0) throw std::invalid_argument("merge_models: zero total weight");
+  DBuf<const double*> dptrs;
+  dptrs.alloc(count);
+  DBuf<double> dw;
+  check(cudaMemcpyAsync(dptrs.p, ptrs.data(), count * sizeof(double*), cudaMemcpyHostToDevice,
+                        c.stream),
+        "H2D model ptrs");
+  if (weights) {
+    dw.alloc(count);
+    check(cudaMemcpyAsync(dw.p, weights, count * sizeof(double), cudaMemcpyHostToDevice, c.stream),
+          "H2D weights");
+  }
+  const unsigned grid =
+      static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((d + 255) / 256, c.num_sms * 8ull)));
+  models_mean_kernel<<<grid, 256, 0, c.stream>>>(dptrs.p, weights ? dw.p : nullptr, count, total, d,
+                                                 out.w64.p, out.w32.p);
+  after_launch(c, "models_mean_kernel");
+  if (refresh) {
+    for (uint64_t i = 0; i < count; ++i) {
+      if (models[i] == &out) continue;
+      copy_model_kernel<<<grid, 256, 0, c.stream>>>(d, out.w64.p, models[i]->w64.p, models[i]->w32.p);
+      after_launch(c, "copy_model_kernel");
+    }
+  }
+  // dptrs / dw are freed on scope exit; make sure the kernels consumed them.
+  check(cudaStreamSynchronize(c.stream), "average_models sync");
+}
+
+void build_col(Dataset& ds) {
+  if (ds.col_built) return;
+  Ctx& c = *ds.ctx;
+  if (ds.layout_in == SGDB_LAYOUT_PADDED) {
+    if (!ds.pval.p) throw Unsupported("padded column arrays were not uploaded");
+  } else if (ds.kind == Kind::Dense) {
+    ds.xcol.alloc(ds.n * ds.d);
+    dim3 grid(static_cast<unsigned>((ds.d + 31) / 32), static_cast<unsigned>((ds.n + 31) / 32));
+    transpose_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(ds.x.p, ds.xcol.p, ds.n, ds.d);
+    after_launch(c, "transpose_kernel");
+  } else {
+    throw std::invalid_argument("column access paths on sparse data require the padded dense layout");
+  }
+  ds.col_built = true;
+}
+
+}  // namespace sgdb::dev

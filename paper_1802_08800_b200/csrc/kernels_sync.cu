@@ -1,0 +1,745 @@
+// Synchronous mini-batch SGD kernels (sm_100a).
+//
+// Replaces the reference's §4 primitive chain for one mini-batch
+// (proj/src/sync_engine.cpp:22-42): matvec (linalg.cpp:30-44) -> elementwise
+// LR/SVM derivative (linalg.cpp:124-174) -> matvec_transposed
+// (linalg.cpp:50-109) -> axpy (linalg.cpp:176-181) + the finite scan
+// (sync_engine.cpp:97-98), fused so each batch is one (dense) or two
+// (sparse full batch) HBM sweeps. See DESIGN.md §Kernels for the rooflines.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "common.cuh"
+#include "device.hpp"
+
+namespace sgdb::dev {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Shared tail: fixed-order fp64 reduction of per-block gradient partials by
+// the last block to finish, then the fused update.
+// ---------------------------------------------------------------------------
+struct GradTail {
+  double* partials;  // [gridDim.x][d]
+  unsigned* ticket;
+  int d;
+  double alpha;
+  int apply;
+  int want_norm;
+  double* w64;
+  float* w32;
+  double* g64;
+  int* finite;
+  double* norm2;
+};
+
+__device__ __forceinline__ double block_sum_d(double v, double* sh) {
+  v = warp_sum_d(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh[i];
+  return t;  // valid in thread 0
+}
+
+// Called by every thread of every block after its partial is in
+// partials[blockIdx.x]. Returns after the last block applied the tail.
+__device__ void grad_tail(const GradTail& t) {
+  __shared__ unsigned s_last;
+  __shared__ double s_red[32];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(t.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double nrm = 0.0;
+  int bad = 0;
+  for (int j = threadIdx.x; j < t.d; j += blockDim.x) {
+    double g = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) g += __ldcg(&t.partials[(size_t)b * t.d + j]);
+    if (!isfinite(g)) bad = 1;
+    if (t.apply) {
+      double w = t.w64[j] - t.alpha * g;
+      t.w64[j] = w;
+      t.w32[j] = static_cast<float>(w);
+    } else {
+      t.g64[j] = g;
+    }
+    nrm += g * g;
+  }
+  if (bad) *t.finite = 0;
+  if (t.want_norm) {
+    double s = block_sum_d(nrm, s_red);
+    if (threadIdx.x == 0) *t.norm2 += s;
+  }
+  if (threadIdx.x == 0) *t.ticket = 0u;
+}
+
+// ---------------------------------------------------------------------------
+// K1: dense row-major, all local rows (full batch). Persistent CTAs, one per
+// SM; warp 0 lane 0 streams contiguous row tiles (rows x d floats + labels)
+// into a shared-memory ring with cp.async.bulk (1-D TMA) on mbarriers; WC
+// consumer warps map L lanes to a row (F features per lane, feature
+// q + L*k), keep the model slice and the gradient accumulators in
+// registers, so each nonzero is read from HBM exactly once.
+// ---------------------------------------------------------------------------
+struct DenseFullParams {
+  const float* x;
+  const float* y;
+  uint64_t n;
+  int d;
+  int R;          // rows per tile (multiple of 4)
+  int S;          // pipeline stages
+  uint64_t ntiles;
+  uint32_t x_floats;      // R*d
+  uint32_t stage_floats;  // x_floats + R, rounded to 32
+  const float* w32;
+  GradTail tail;
+};
+
+template <int L, int F, int TASK, int WC>
+__global__ void __launch_bounds__(32 * (WC + 1), 1) dense_full_kernel(DenseFullParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + p.S;
+  float* stages = reinterpret_cast<float*>(smem + 128 * ((16 * p.S + 127) / 128));
+  float* red = stages + (size_t)p.S * p.stage_floats;  // [WC][d]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = p.d;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], WC);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint64_t i = 0;
+      for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+        const int s = static_cast<int>(i % p.S);
+        if (i >= (uint64_t)p.S) mbar_wait(&empty[s], static_cast<uint32_t>(((i / p.S) - 1) & 1));
+        const uint64_t r0 = t * p.R;
+        const uint64_t rows = min(static_cast<uint64_t>(p.R), p.n - r0);
+        const uint32_t xb = round_up16(rows * d * 4ull), yb = round_up16(rows * 4ull);
+        float* st = stages + (size_t)s * p.stage_floats;
+        mbar_arrive_expect_tx(&full[s], xb + yb);
+        bulk_g2s(st, p.x + r0 * d, xb, &full[s]);
+        bulk_g2s(st + p.x_floats, p.y + r0, yb, &full[s]);
+      }
+    }
+  } else {
+    constexpr int RS = 32 / L;
+    const int cw = warp - 1, q = lane % L, slot = lane / L;
+    float wr[F], acc[F];
+#pragma unroll
+    for (int k = 0; k < F; ++k) {
+      const int j = q + L * k;
+      wr[k] = j < d ? p.w32[j] : 0.f;
+      acc[k] = 0.f;
+    }
+    uint64_t i = 0;
+    for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
+      const int s = static_cast<int>(i % p.S);
+      mbar_wait(&full[s], static_cast<uint32_t>((i / p.S) & 1));
+      const float* xs = stages + (size_t)s * p.stage_floats;
+      const float* ys = xs + p.x_floats;
+      const int rows = static_cast<int>(min(static_cast<uint64_t>(p.R), p.n - t * p.R));
+      for (int rb = cw * RS; rb < rows; rb += WC * RS) {
+        const int r = rb + slot;
+        const bool valid = r < rows;
+        float xv[F];
+        float z = 0.f;
+#pragma unroll
+        for (int k = 0; k < F; ++k) {
+          const int j = q + L * k;
+          xv[k] = (valid && j < d) ? xs[r * d + j] : 0.f;
+          z = fmaf(xv[k], wr[k], z);
+        }
+        z = group_sum<L>(z);
+        const float c = valid ? coef_f<TASK>(z, ys[r]) : 0.f;
+#pragma unroll
+        for (int k = 0; k < F; ++k) acc[k] = fmaf(c, xv[k], acc[k]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+#pragma unroll
+    for (int k = 0; k < F; ++k) acc[k] = cross_group_sum<L>(acc[k]);
+    if (slot == 0) {
+#pragma unroll
+      for (int k = 0; k < F; ++k) {
+        const int j = q + L * k;
+        if (j < d) red[cw * d + j] = acc[k];
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < WC; ++w) s += red[w * d + j];
+    p.tail.partials[(size_t)blockIdx.x * d + j] = s;
+  }
+  grad_tail(p.tail);
+}
+
+// ---------------------------------------------------------------------------
+// K1b: dense row-major, rows gathered from a list of global ids (mini-batch).
+// Block partials are folded into g64 with fp64 atomics; the last block
+// applies the update and re-zeroes g64.
+// ---------------------------------------------------------------------------
+struct DenseBatchParams {
+  const float* x;
+  const float* y;
+  uint64_t n_local, row_base;
+  int d;
+  const uint32_t* ids;
+  uint64_t nb;
+  const float* w32;
+  double* g64;
+  unsigned* ticket;
+  int* finite;
+  double* w64;
+  float* w32_out;
+  double* norm2;
+  double alpha;
+  int apply;
+  int want_norm;
+};
+
+template <int L, int F, int TASK, int W>
+__global__ void __launch_bounds__(32 * W) dense_batch_kernel(DenseBatchParams p) {
+  extern __shared__ __align__(16) float red[];  // [W][d]
+  __shared__ unsigned s_last;
+  __shared__ double s_red[32];
+  if (p.apply && *p.finite == 0) return;  // the epoch already stopped
+  constexpr int RS = 32 / L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = lane % L, slot = lane / L, d = p.d;
+  const uint64_t gw = (uint64_t)blockIdx.x * W + warp, tw = (uint64_t)gridDim.x * W;
+  float wr[F], acc[F];
+#pragma unroll
+  for (int k = 0; k < F; ++k) {
+    const int j = q + L * k;
+    wr[k] = j < d ? p.w32[j] : 0.f;
+    acc[k] = 0.f;
+  }
+  for (uint64_t pb = gw * RS; pb < p.nb; pb += tw * RS) {
+    const uint64_t pos = pb + slot;
+    uint64_t row = 0;
+    bool valid = pos < p.nb;
+    if (valid) {
+      row = static_cast<uint64_t>(p.ids[pos]) - p.row_base;
+      valid = row < p.n_local;
+    }
+    const float* xr = p.x + row * d;
+    float xv[F];
+    float z = 0.f;
+#pragma unroll
+    for (int k = 0; k < F; ++k) {
+      const int j = q + L * k;
+      xv[k] = (valid && j < d) ? __ldg(xr + j) : 0.f;
+      z = fmaf(xv[k], wr[k], z);
+    }
+    z = group_sum<L>(z);
+    const float c = valid ? coef_f<TASK>(z, __ldg(p.y + row)) : 0.f;
+#pragma unroll
+    for (int k = 0; k < F; ++k) acc[k] = fmaf(c, xv[k], acc[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < F; ++k) acc[k] = cross_group_sum<L>(acc[k]);
+  if (slot == 0) {
+#pragma unroll
+    for (int k = 0; k < F; ++k) {
+      const int j = q + L * k;
+      if (j < d) red[warp * d + j] = acc[k];
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < W; ++w) s += red[w * d + j];
+    if (s != 0.0) atomicAdd(&p.g64[j], s);
+  }
+  if (!p.apply) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(p.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double nrm = 0.0;
+  int bad = 0;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    const double g = __ldcg(&p.g64[j]);
+    if (!isfinite(g)) bad = 1;
+    const double w = p.w64[j] - p.alpha * g;
+    p.w64[j] = w;
+    p.w32_out[j] = static_cast<float>(w);
+    p.g64[j] = 0.0;
+    nrm += g * g;
+  }
+  if (bad) *p.finite = 0;
+  if (p.want_norm) {
+    double s = block_sum_d(nrm, s_red);
+    if (threadIdx.x == 0) *p.norm2 += s;
+  }
+  if (threadIdx.x == 0) *p.ticket = 0u;
+}
+
+// ---------------------------------------------------------------------------
+// K2: sparse margins + coefficients for all local rows. G lanes per row,
+// coalesced val/idx, model gathered from L2 (d <= 1.4M floats stays resident).
+// ---------------------------------------------------------------------------
+template <int G, int TASK>
+__global__ void __launch_bounds__(256) csr_coef_kernel(const float* __restrict__ val,
+                                                       const uint32_t* __restrict__ idx,
+                                                       const uint32_t* __restrict__ rowptr,
+                                                       const float* __restrict__ y, uint64_t n,
+                                                       const float* __restrict__ w32,
+                                                       float* __restrict__ coef) {
+  constexpr int RW = 32 / G;
+  const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t base = gw * RW; base < n; base += tw * RW) {
+    const uint64_t row = base + grp;
+    float z = 0.f;
+    if (row < n) {
+      const uint32_t b = rowptr[row], e = rowptr[row + 1];
+      for (uint32_t s = b + lg; s < e; s += G) z = fmaf(__ldg(val + s), __ldg(w32 + __ldg(idx + s)), z);
+    }
+    z = group_sum<G>(z);
+    if (row < n && lg == 0) coef[row] = coef_f<TASK>(z, y[row]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: g_j = sum over column j of the CSC copy of c[row] * x_ij (fp64
+// accumulation), fused with w_j -= alpha*g_j (one writer per coordinate, so
+// the result is deterministic) and the finite flag.
+// ---------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(256) csc_grad_kernel(const float* __restrict__ cval,
+                                                       const uint32_t* __restrict__ crow,
+                                                       const uint32_t* __restrict__ colptr,
+                                                       uint64_t d, const float* __restrict__ coef,
+                                                       double alpha, int apply, int want_norm,
+                                                       double* w64, float* w32, double* g64,
+                                                       int* finite, double* norm2) {
+  constexpr int CW = 32 / G;
+  const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  double nrm = 0.0;
+  int bad = 0;
+  for (uint64_t base = gw * CW; base < d; base += tw * CW) {
+    const uint64_t j = base + grp;
+    double acc = 0.0;
+    if (j < d) {
+      const uint32_t b = colptr[j], e = colptr[j + 1];
+      for (uint32_t s = b + lg; s < e; s += G)
+        acc += static_cast<double>(__ldg(cval + s) * __ldg(coef + __ldg(crow + s)));
+    }
+    acc = group_sum<G>(acc);
+    if (j < d && lg == 0) {
+      if (!isfinite(acc)) bad = 1;
+      if (apply) {
+        const double w = w64[j] - alpha * acc;
+        w64[j] = w;
+        w32[j] = static_cast<float>(w);
+      } else {
+        g64[j] = acc;
+      }
+      nrm += acc * acc;
+    }
+  }
+  if (bad) *finite = 0;
+  if (want_norm) {
+    nrm = warp_sum_d(nrm);
+    if (lane == 0 && nrm != 0.0) atomicAdd(norm2, nrm);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3b: sparse mini-batch: margin, coefficient and scatter of c*x into g64
+// with fp64 atomics (red.global.add.f64) — order effects ~1e-16, invisible
+// after fp32 rounding.
+// ---------------------------------------------------------------------------
+template <int G, int TASK>
+__global__ void __launch_bounds__(256) csr_batch_kernel(
+    const float* __restrict__ val, const uint32_t* __restrict__ idx,
+    const uint32_t* __restrict__ rowptr, const float* __restrict__ y, uint64_t n_local,
+    uint64_t row_base, const uint32_t* __restrict__ ids, uint64_t nb,
+    const float* __restrict__ w32, double* g64, const int* finite, int check_finite) {
+  if (check_finite && *finite == 0) return;
+  constexpr int RW = 32 / G;
+  const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t base = gw * RW; base < nb; base += tw * RW) {
+    const uint64_t pos = base + grp;
+    uint64_t row = 0;
+    bool valid = pos < nb;
+    if (valid) {
+      row = static_cast<uint64_t>(ids[pos]) - row_base;
+      valid = row < n_local;
+    }
+    uint32_t b = 0, e = 0;
+    if (valid) {
+      b = rowptr[row];
+      e = rowptr[row + 1];
+    }
+    float z = 0.f;
+    for (uint32_t s = b + lg; s < e; s += G) z = fmaf(__ldg(val + s), __ldg(w32 + __ldg(idx + s)), z);
+    z = group_sum<G>(z);
+    if (!valid) continue;
+    const float c = coef_f<TASK>(z, y[row]);
+    if (c == 0.f) continue;
+    for (uint32_t s = b + lg; s < e; s += G)
+      atomicAdd(&g64[__ldg(idx + s)], static_cast<double>(c * __ldg(val + s)));
+  }
+}
+
+__global__ void apply_kernel(uint64_t d, double alpha, double* w64, float* w32, double* g64,
+                             int* finite, double* norm2, int want_norm) {
+  double nrm = 0.0;
+  int bad = 0;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const double g = g64[j];
+    if (!isfinite(g)) bad = 1;
+    const double w = w64[j] - alpha * g;
+    w64[j] = w;
+    w32[j] = static_cast<float>(w);
+    g64[j] = 0.0;
+    nrm += g * g;
+  }
+  if (bad) *finite = 0;
+  if (want_norm) {
+    nrm = warp_sum_d(nrm);
+    if ((threadIdx.x & 31) == 0 && nrm != 0.0) atomicAdd(norm2, nrm);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: loss (untimed, fp64): per-row margin in fp64 against the fp64 master,
+// per-block partials, fixed-order final sum by the last block.
+// ---------------------------------------------------------------------------
+struct LossTail {
+  double* partials;
+  unsigned* ticket;
+  double* out;
+};
+
+__device__ void loss_tail(double v, const LossTail& t) {
+  __shared__ double s_red[32];
+  __shared__ unsigned s_last;
+  double s = block_sum_d(v, s_red);
+  if (threadIdx.x == 0) t.partials[blockIdx.x] = s;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(t.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) tot += __ldcg(&t.partials[b]);
+    *t.out = tot;
+    *t.ticket = 0u;
+  }
+}
+
+template <int L, int F>
+__global__ void __launch_bounds__(256) dense_loss_kernel(const float* __restrict__ x,
+                                                         const float* __restrict__ y, uint64_t n,
+                                                         int d, const double* __restrict__ w64,
+                                                         int task, LossTail t) {
+  constexpr int RS = 32 / L;
+  const int lane = threadIdx.x & 31, q = lane % L, slot = lane / L;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  double wr[F];
+#pragma unroll
+  for (int k = 0; k < F; ++k) wr[k] = (q + L * k) < d ? w64[q + L * k] : 0.0;
+  double lsum = 0.0;
+  for (uint64_t base = gw * RS; base < n; base += tw * RS) {
+    const uint64_t row = base + slot;
+    const bool valid = row < n;
+    double z = 0.0;
+#pragma unroll
+    for (int k = 0; k < F; ++k) {
+      const int j = q + L * k;
+      if (valid && j < d) z += static_cast<double>(__ldg(x + row * d + j)) * wr[k];
+    }
+    z = group_sum<L>(z);
+    if (valid && q == 0) lsum += loss_d(task, z, static_cast<double>(y[row]));
+  }
+  loss_tail(lsum, t);
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) csr_loss_kernel(const float* __restrict__ val,
+                                                       const uint32_t* __restrict__ idx,
+                                                       const uint32_t* __restrict__ rowptr,
+                                                       const float* __restrict__ y, uint64_t n,
+                                                       const double* __restrict__ w64, int task,
+                                                       LossTail t) {
+  constexpr int RW = 32 / G;
+  const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  double lsum = 0.0;
+  for (uint64_t base = gw * RW; base < n; base += tw * RW) {
+    const uint64_t row = base + grp;
+    double z = 0.0;
+    if (row < n) {
+      const uint32_t b = rowptr[row], e = rowptr[row + 1];
+      for (uint32_t s = b + lg; s < e; s += G)
+        z += static_cast<double>(__ldg(val + s)) * __ldg(w64 + __ldg(idx + s));
+    }
+    z = group_sum<G>(z);
+    if (row < n && lg == 0) lsum += loss_d(task, z, static_cast<double>(y[row]));
+  }
+  loss_tail(lsum, t);
+}
+
+__global__ void w64_from_w32_kernel(uint64_t d, const float* w32, double* w64) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    w64[j] = static_cast<double>(w32[j]);
+}
+
+// ---- host-side dispatch -----------------------------------------------------
+
+int lanes_for(double avg) {
+  if (avg <= 6.0) return 4;
+  if (avg <= 16.0) return 8;
+  if (avg <= 40.0) return 16;
+  return 32;
+}
+
+unsigned grid_for(const Ctx& c, uint64_t items_per_block_unit, uint64_t units, unsigned per_sm) {
+  uint64_t want = (units + items_per_block_unit - 1) / items_per_block_unit;
+  uint64_t cap = static_cast<uint64_t>(c.num_sms) * per_sm;
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min(want, cap)));
+}
+
+void after_launch(Ctx& c, const char* what) {
+  ++c.launches;
+  check(cudaGetLastError(), what);
+}
+
+template <int L, int F, int TASK>
+void launch_dense_full_LF(Dataset& ds, Model& m, const StepArgs& a) {
+  Ctx& c = *ds.ctx;
+  constexpr int WC = 8;
+  const int d = static_cast<int>(ds.d);
+  const int row_bytes = d * 4;
+  int R = std::max(4, (32768 / row_bytes) & ~3);
+  DenseFullParams p{};
+  p.x = ds.x.p;
+  p.y = ds.labels.p;
+  p.n = ds.n;
+  p.d = d;
+  p.R = R;
+  p.ntiles = (ds.n + R - 1) / R;
+  p.x_floats = static_cast<uint32_t>(R * d);
+  p.stage_floats = (p.x_floats + R + 31) & ~31u;
+  const size_t red_bytes = static_cast<size_t>(WC) * d * 4;
+  const size_t budget = std::min<size_t>(c.max_smem_optin, 220 * 1024) - red_bytes - 256;
+  int S = static_cast<int>(std::min<size_t>(8, budget / (p.stage_floats * 4ull)));
+  if (S < 2) throw Unsupported("dense tile does not fit shared memory");
+  p.S = S;
+  const size_t smem = 128 * ((16 * S + 127) / 128) + (size_t)S * p.stage_floats * 4 + red_bytes;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(p.ntiles, c.num_sms));
+  m.partials.alloc(static_cast<uint64_t>(grid) * d);
+  p.w32 = m.w32.p;
+  p.tail = GradTail{m.partials.p, m.ticket.p, d, a.alpha, a.apply ? 1 : 0, a.want_norm ? 1 : 0,
+                    m.w64.p, m.w32.p, m.g64.p, m.finite.p, m.scal.p};
+  auto kern = dense_full_kernel<L, F, TASK, WC>;
+  check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)),
+        "cudaFuncSetAttribute(dense_full)");
+  kern<<<grid, 32 * (WC + 1), smem, c.stream>>>(p);
+  after_launch(c, "dense_full_kernel");
+}
+
+template <int L, int F, int TASK>
+void launch_dense_batch_LF(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb,
+                           const StepArgs& a) {
+  Ctx& c = *ds.ctx;
+  constexpr int W = 8;
+  constexpr int RS = 32 / L;
+  const int d = static_cast<int>(ds.d);
+  DenseBatchParams p{ds.x.p,  ds.labels.p, ds.n,     ds.row_base, d,
+                     ids,     nb,          m.w32.p,  m.g64.p,     m.ticket.p,
+                     m.finite.p, m.w64.p,  m.w32.p,  m.scal.p,    a.alpha,
+                     a.apply ? 1 : 0, a.want_norm ? 1 : 0};
+  const unsigned grid = grid_for(c, static_cast<uint64_t>(W) * RS * 2, nb, 8);
+  const size_t smem = static_cast<size_t>(W) * d * 4;
+  auto kern = dense_batch_kernel<L, F, TASK, W>;
+  if (smem > 48 * 1024)
+    check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)),
+          "cudaFuncSetAttribute(dense_batch)");
+  kern<<<grid, 32 * W, smem, c.stream>>>(p);
+  after_launch(c, "dense_batch_kernel");
+}
+
+template <int L, int F>
+void launch_dense_loss_LF(Dataset& ds, Model& m, int task) {
+  Ctx& c = *ds.ctx;
+  constexpr int RS = 32 / L;
+  const unsigned grid = grid_for(c, 8ull * RS * 4, ds.n, 8);
+  c.loss_partials.alloc(grid);
+  dense_loss_kernel<L, F><<<grid, 256, 0, c.stream>>>(
+      ds.x.p, ds.labels.p, ds.n, static_cast<int>(ds.d), m.w64.p, task,
+      LossTail{c.loss_partials.p, c.tickets.p, c.loss_out.p});
+  after_launch(c, "dense_loss_kernel");
+}
+
+// (L, F) per d: L lanes per row, F features per lane, L*F >= d.
+template <class Fn>
+void dispatch_dense(uint64_t d, Fn&& fn) {
+  if (d <= 32) fn.template operator()<4, 8>();
+  else if (d <= 64) fn.template operator()<8, 8>();
+  else if (d <= 128) fn.template operator()<16, 8>();
+  else if (d <= 256) fn.template operator()<32, 8>();
+  else if (d <= 512) fn.template operator()<32, 16>();
+  else if (d <= 1024) fn.template operator()<32, 32>();
+  else throw Unsupported("dense kernels handle d <= 1024 (wider data is stored as CSR)");
+}
+
+template <int G, int TASK>
+void launch_csr_coef_G(Dataset& ds, Model& m) {
+  Ctx& c = *ds.ctx;
+  const unsigned grid = grid_for(c, 8ull * (32 / G) * 4, ds.n, 8);
+  csr_coef_kernel<G, TASK><<<grid, 256, 0, c.stream>>>(ds.val.p, ds.idx.p, ds.rowptr.p,
+                                                       ds.labels.p, ds.n, m.w32.p, ds.coef.p);
+  after_launch(c, "csr_coef_kernel");
+}
+
+template <int G>
+void launch_csc_grad_G(Dataset& ds, Model& m, const StepArgs& a) {
+  Ctx& c = *ds.ctx;
+  const unsigned grid = grid_for(c, 8ull * (32 / G) * 4, ds.d, 8);
+  csc_grad_kernel<G><<<grid, 256, 0, c.stream>>>(ds.cval.p, ds.crow.p, ds.colptr.p, ds.d,
+                                                 ds.coef.p, a.alpha, a.apply ? 1 : 0,
+                                                 a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p,
+                                                 m.finite.p, m.scal.p);
+  after_launch(c, "csc_grad_kernel");
+}
+
+template <int G, int TASK>
+void launch_csr_batch_G(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, bool check) {
+  Ctx& c = *ds.ctx;
+  const unsigned grid = grid_for(c, 8ull * (32 / G) * 2, nb, 8);
+  csr_batch_kernel<G, TASK><<<grid, 256, 0, c.stream>>>(
+      ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p, ds.n, ds.row_base, ids, nb, m.w32.p,
+      m.g64.p, m.finite.p, check ? 1 : 0);
+  after_launch(c, "csr_batch_kernel");
+}
+
+template <int G>
+void launch_csr_loss_G(Dataset& ds, Model& m, int task) {
+  Ctx& c = *ds.ctx;
+  const unsigned grid = grid_for(c, 8ull * (32 / G) * 4, ds.n, 8);
+  c.loss_partials.alloc(grid);
+  csr_loss_kernel<G><<<grid, 256, 0, c.stream>>>(
+      ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p, ds.n, m.w64.p, task,
+      LossTail{c.loss_partials.p, c.tickets.p, c.loss_out.p});
+  after_launch(c, "csr_loss_kernel");
+}
+
+template <class Fn>
+void dispatch_G(int g, Fn&& fn) {
+  switch (g) {
+    case 4: fn.template operator()<4>(); break;
+    case 8: fn.template operator()<8>(); break;
+    case 16: fn.template operator()<16>(); break;
+    default: fn.template operator()<32>(); break;
+  }
+}
+
+}  // namespace
+
+void dense_full_step(Dataset& ds, Model& m, const StepArgs& a) {
+  if (ds.n == 0) return;
+  dispatch_dense(ds.d, [&]<int L, int F>() {
+    if (a.task == kTaskLR) launch_dense_full_LF<L, F, kTaskLR>(ds, m, a);
+    else launch_dense_full_LF<L, F, kTaskSVM>(ds, m, a);
+  });
+}
+
+void dense_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb,
+                      const StepArgs& a) {
+  dispatch_dense(ds.d, [&]<int L, int F>() {
+    if (a.task == kTaskLR) launch_dense_batch_LF<L, F, kTaskLR>(ds, m, ids, nb, a);
+    else launch_dense_batch_LF<L, F, kTaskSVM>(ds, m, ids, nb, a);
+  });
+}
+
+void csr_full_step(Dataset& ds, Model& m, const StepArgs& a) {
+  build_csc(ds);
+  if (ds.n > 0) {
+    const int g = lanes_for(static_cast<double>(ds.nnz) / static_cast<double>(ds.n));
+    dispatch_G(g, [&]<int G>() {
+      if (a.task == kTaskLR) launch_csr_coef_G<G, kTaskLR>(ds, m);
+      else launch_csr_coef_G<G, kTaskSVM>(ds, m);
+    });
+  }
+  const int gc = lanes_for(static_cast<double>(ds.nnz) / static_cast<double>(std::max<uint64_t>(1, ds.d)));
+  dispatch_G(gc, [&]<int G>() { launch_csc_grad_G<G>(ds, m, a); });
+}
+
+void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, const StepArgs& a) {
+  const int g = lanes_for(ds.n ? static_cast<double>(ds.nnz) / static_cast<double>(ds.n) : 1.0);
+  dispatch_G(g, [&]<int G>() {
+    if (a.task == kTaskLR) launch_csr_batch_G<G, kTaskLR>(ds, m, ids, nb, a.apply);
+    else launch_csr_batch_G<G, kTaskSVM>(ds, m, ids, nb, a.apply);
+  });
+  if (a.apply) apply_update(m, a.alpha, a.want_norm);
+}
+
+void apply_update(Model& m, double alpha, bool want_norm) {
+  Ctx& c = *m.ctx;
+  const unsigned grid = grid_for(c, 256ull * 4, m.d, 8);
+  apply_kernel<<<grid, 256, 0, c.stream>>>(m.d, alpha, m.w64.p, m.w32.p, m.g64.p, m.finite.p,
+                                           m.scal.p, want_norm ? 1 : 0);
+  after_launch(c, "apply_kernel");
+}
+
+void loss_launch(Dataset& ds, Model& m, int task) {
+  Ctx& c = *ds.ctx;
+  if (ds.n == 0) {
+    check(cudaMemsetAsync(c.loss_out.p, 0, sizeof(double), c.stream), "memset loss");
+    return;
+  }
+  if (ds.kind == Kind::Dense) {
+    dispatch_dense(ds.d, [&]<int L, int F>() { launch_dense_loss_LF<L, F>(ds, m, task); });
+  } else {
+    const int g = lanes_for(static_cast<double>(ds.nnz) / static_cast<double>(ds.n));
+    dispatch_G(g, [&]<int G>() { launch_csr_loss_G<G>(ds, m, task); });
+  }
+}
+
+void sync_w64_from_w32(Model& m) {
+  Ctx& c = *m.ctx;
+  const unsigned grid = grid_for(c, 256ull * 4, m.d, 8);
+  w64_from_w32_kernel<<<grid, 256, 0, c.stream>>>(m.d, m.w32.p, m.w64.p);
+  after_launch(c, "w64_from_w32_kernel");
+}
+
+}  // namespace sgdb::dev

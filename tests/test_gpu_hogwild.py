@@ -1,0 +1,183 @@
+"""GPU parity of the Hogwild kernels against the CPU oracle.
+
+Mirrors proj/tests/test_async_engine.cpp and acceptance criteria 4-6
+(proj/tests/acceptance.cpp:170-312). One worker (one lane group) reproduces
+sequential Alg. 3 up to fp32 arithmetic; independent replicas (thread scope,
+dual instances) are deterministic and match the serialized oracle; racing
+workers are checked on the loss curve (acceptance 5's template).
+
+Tolerances: model rel-L2 <= 1e-4 and loss rel <= 1e-5 for deterministic
+schedules (the device keeps the Hogwild model in fp32, as the paper's GPU
+kernel does, so rounding accumulates per update; measured ~1e-6).
+"""
+import numpy as np
+import pytest
+
+from conftest import rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+MODEL_TOL = 1e-4
+LOSS_TOL = 1e-5
+
+RR = {"row-rr": 1, "row-ch": 0, "col-rr": 1, "col-ch": 0}
+REPL = {"kernel": 0, "block": 1, "thread": 2}
+
+
+def _inc(S, task, alpha, epochs, decay=1.0):
+    return S.Hyperparams(alpha=alpha, batch_b=1, epochs=epochs, task=task, step_decay=decay)
+
+
+@pytest.fixture(scope="module")
+def datasets(sgdb):
+    S = sgdb
+    csr = S.fixtures.sparse_classification(60, 20, 4.0, 3).rounded_f32()
+    dense_row = S.fixtures.dense_classification(50, 7, 4).rounded_f32()
+    return {
+        "csr": csr,
+        "padded": S.convert_layout(csr, S.Layout.PaddedDense),
+        "dense_row": dense_row,
+        "dense_col": S.convert_layout(dense_row, S.Layout.DenseColMajor),
+    }
+
+
+CASES = [("csr", "row-rr:kernel:0"), ("csr", "row-ch:kernel:0"), ("csr", "row-rr:thread:0"),
+         ("csr", "row-ch:block:0"), ("padded", "col-rr:kernel:0"), ("padded", "col-ch:kernel:0"),
+         ("dense_row", "row-rr:kernel:0"), ("dense_row", "row-ch:thread:0"),
+         ("dense_col", "col-rr:kernel:0"), ("dense_col", "col-ch:block:0"),
+         ("csr", "row-ch:kernel:3"), ("dense_row", "row-rr:block:2")]
+
+
+@pytest.mark.parametrize("name,plan_text", CASES)
+@pytest.mark.parametrize("task", [0, 1])
+@pytest.mark.parametrize("lanes", [0, 1, 32])
+def test_one_worker_equals_sequential(sgdb, dev, orc, datasets, name, plan_text, task, lanes):
+    """test_async_engine.cpp:99-128 / acceptance 4 (bitwise there, fp32 tolerance here)."""
+    S = sgdb
+    ds = datasets[name]
+    plan = S.parse_plan(plan_text)
+    plan.workers = 1
+    plan.lanes_per_worker = lanes
+    r = S.hogwild.train(S.Task(task), ds, _inc(S, S.Task(task), 0.05, 3), plan, 0, device=dev)
+    access, repl, k = plan_text.split(":")
+    om, ol, ev = orc.hogwild_serial(ds, task, 0.05, 3, RR[access], REPL[repl], int(k), 1)
+    assert rel_l2(r.model, om[-1]) <= MODEL_TOL
+    for e in range(3):
+        assert rel(r.trace.epochs[e].loss, ol[e]) <= LOSS_TOL
+    assert r.evals_per_epoch == [int(x) for x in ev]
+
+
+@pytest.mark.parametrize("workers,gs", [(2, 32), (7, 32), (64, 8), (300, 32)])
+def test_thread_scope_equals_serialized_partitions(sgdb, dev, orc, workers, gs):
+    """test_async_engine.cpp:187-215: per-worker replicas never interact within an
+    epoch, so T workers equal T sequential partition runs merged by mean."""
+    S = sgdb
+    ds = S.fixtures.sparse_classification(2000, 300, 12.0, 8).rounded_f32()
+    plan = S.parse_plan("row-ch:thread:0")
+    plan.workers = workers
+    r = S.hogwild.train(S.Task.LR, ds, _inc(S, S.Task.LR, 0.07, 3), plan, 0, device=dev)
+    om, ol, _ = orc.hogwild_serial(ds, 0, 0.07, 3, 0, 2, 0, workers)
+    assert rel_l2(r.model, om[-1]) <= MODEL_TOL
+    for e in range(3):
+        assert rel(r.trace.epochs[e].loss, ol[e]) <= LOSS_TOL
+
+
+@pytest.mark.parametrize("plan_text", ["row-ch:block:0", "row-rr:block:2"])
+def test_block_scope_one_worker_per_group_is_deterministic(sgdb, dev, orc, plan_text):
+    """group_size 1: every replica has a single worker -> equals the serialized oracle."""
+    S = sgdb
+    ds = S.fixtures.sparse_classification(3000, 47236 // 4, 30.0, 9).rounded_f32()
+    plan = S.parse_plan(plan_text)
+    plan.workers, plan.group_size = 40, 1
+    r = S.hogwild.train(S.Task.SVM, ds, _inc(S, S.Task.SVM, 0.05, 2), plan, 0, device=dev)
+    om, ol, _ = orc.hogwild_serial(ds, 1, 0.05, 2, RR[plan_text.split(":")[0]], 1,
+                                   int(plan_text.split(":")[2]), 40, group_size=1)
+    assert rel_l2(r.model, om[-1]) <= MODEL_TOL
+    assert rel(r.trace.final_loss(), ol[-1]) <= LOSS_TOL
+
+
+def test_block_scope_global_replicas(sgdb, dev, orc):
+    """A model too large for shared memory takes the global-replica path."""
+    S = sgdb
+    ds = S.fixtures.sparse_classification(800, 200000, 30.0, 10).rounded_f32()
+    plan = S.parse_plan("row-ch:block:0")
+    plan.workers, plan.group_size = 16, 1
+    r = S.hogwild.train(S.Task.LR, ds, _inc(S, S.Task.LR, 0.1, 2), plan, 0, device=dev)
+    om, ol, _ = orc.hogwild_serial(ds, 0, 0.1, 2, 0, 1, 0, 16, group_size=1)
+    assert rel_l2(r.model, om[-1]) <= MODEL_TOL
+
+
+def test_evals_per_epoch(sgdb, dev):
+    """test_async_engine.cpp:301-311 / acceptance 6: evals = n + T*k."""
+    S = sgdb
+    ds = S.fixtures.sparse_classification(64, 16, 3.0, 16)
+    for k in (0, 2, 5, 10):
+        plan = S.parse_plan(f"row-ch:kernel:{k}")
+        plan.workers = 4
+        r = S.hogwild.train(S.Task.LR, ds, _inc(S, S.Task.LR, 0.02, 3), plan, 0, device=dev)
+        assert r.evals_per_epoch == [64 + 4 * k] * 3
+
+
+def test_dual_equals_single(sgdb, dev):
+    """test_async_engine.cpp:273-299."""
+    S = sgdb
+    ds = S.fixtures.sparse_classification(40, 12, 3.0, 14)
+    plan = S.parse_plan("row-ch:kernel:0")
+    dual = S.hogwild.numa_dual_train(S.Task.LR, ds, _inc(S, S.Task.LR, 0.08, 4), plan, 0, device=dev)
+    single = S.hogwild.train(S.Task.LR, ds, _inc(S, S.Task.LR, 0.08, 4), plan, 0, device=dev)
+    np.testing.assert_array_equal(dual.model, single.model)
+    assert dual.trace.losses() == single.trace.losses()
+    assert dual.evals_per_epoch[0] == 2 * ds.n_examples
+    plan.merge_period_epochs = 0
+    dual = S.hogwild.numa_dual_train(S.Task.SVM, ds, _inc(S, S.Task.SVM, 0.05, 3), plan, 0, device=dev)
+    single = S.hogwild.train(S.Task.SVM, ds, _inc(S, S.Task.SVM, 0.05, 3), plan, 0, device=dev)
+    np.testing.assert_array_equal(dual.model, single.model)
+
+
+def test_invalid_plan_layout_rejected(sgdb, dev):
+    S = sgdb
+    csr = S.fixtures.sparse_classification(10, 5, 2.0, 19)
+    plan = S.parse_plan("col-rr:kernel:0")
+    with pytest.raises(ValueError):
+        S.hogwild.train(S.Task.LR, csr, _inc(S, S.Task.LR, 0.1, 1), plan, 0, device=dev)
+
+
+def test_example_scope_is_reported_unsupported(sgdb, dev):
+    S = sgdb
+    csr = S.fixtures.sparse_classification(10, 5, 2.0, 19)
+    plan = S.parse_plan("row-ch:example:0")
+    with pytest.raises(S.UnsupportedError):
+        S.hogwild.train(S.Task.LR, csr, _inc(S, S.Task.LR, 0.1, 1), plan, 0, device=dev)
+
+
+@pytest.mark.parametrize("plan_text,lanes", [("row-ch:kernel:0", 0), ("row-rr:kernel:0", 8),
+                                             ("row-ch:block:0", 0), ("row-ch:kernel:10", 0)])
+def test_many_workers_converge(sgdb, dev, plan_text, lanes):
+    """Acceptance 5 (acceptance.cpp:222-264): sparse 20000x10000 avg 50, SVM
+    alpha 0.5 decay 0.93, 60 epochs; thousands of racing lane groups must reach
+    1% of L* within 3x the epochs one worker needs."""
+    S = sgdb
+    ds = S.fixtures.sparse_classification(20000, 10000, 50.0, 20250810, 0.1)
+    dds = S.DeviceDataset(dev, ds)
+    l_star = np.inf
+    for alpha in (1e-4, 1e-3, 1e-2, 1e-1, 1.0):
+        hp = S.Hyperparams(alpha=alpha, batch_b=ds.n_examples, epochs=60, task=S.Task.SVM)
+        r = S.sync.train(S.Task.SVM, dds, hp, 0)
+        l_star = min([l_star] + [x for x in r.trace.losses() if np.isfinite(x)])
+    hp = _inc(S, S.Task.SVM, 0.5, 60, 0.93)
+
+    def epochs_to(losses):
+        for i, l in enumerate(losses):
+            if l <= 1.01 * l_star:
+                return i + 1
+        return None
+
+    p1 = S.parse_plan("row-ch:kernel:0")
+    e1 = epochs_to(S.hogwild.train(S.Task.SVM, dds, hp, p1, 0).trace.losses())
+    assert e1 is not None
+    plan = S.parse_plan(plan_text)
+    plan.workers = 4096
+    plan.lanes_per_worker = lanes
+    r = S.hogwild.train(S.Task.SVM, dds, hp, plan, 0)
+    en = epochs_to(r.trace.losses())
+    assert en is not None and en <= 3 * e1, (en, e1, r.trace.losses()[-5:], l_star)
