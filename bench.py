@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 GLM SGD engine.
+
+Workload (BASELINE.json configs[1]): SVM Hogwild async SGD, warp-group-per-
+example kernel, on sparse synthetic w8a-shaped data — 64,700 x 300 CSR,
+fixtures::sparse_classification(64700, 300, 11.65, 20250811),
+plan row-ch + kernel + no-rep with every resident lane group a worker.
+
+A step is one Hogwild epoch over the dataset. metric = examples/sec per epoch
+(N / t_epoch); the whole-job value at N GPUs is N*n / t_epoch
+(weak scaling: every rank trains its own w8a-shaped partition, seed + rank,
+and the replicas are averaged over NCCL after every epoch). The dataset
+(6.5 MB) is L2-resident, so L2 is flushed (256 MiB memset) before every timed
+epoch, outside the per-epoch CUDA-event window.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_EX, D, AVG, SEED = 64700, 300, 11.65, 20250811
+PLAN = "row-ch:kernel:0"
+TASK_SVM = 1
+METRIC = "examples/sec per epoch (SVM Hogwild, w8a-shaped 64,700x300 CSR)"
+UNIT = "examples/s"
+WORKLOAD = "C2 w8a-shaped SVM Hogwild (BASELINE.json configs[1])"
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _reference_time_epochs(ref, ds, plan, workers, epochs, alpha, handle=None):
+    _, losses, secs, _ = ref.hogwild_train(ds, TASK_SVM, alpha, epochs, plan, workers=workers,
+                                           handle=handle)
+    return losses, secs
+
+
+def _epochs_to(losses, l_star, tol=0.01):
+    for i, v in enumerate(losses):
+        if v <= (1 + tol) * l_star:
+            return i + 1
+    return None
+
+
+# --------------------------------------------------------------------------------------
+def run_reference(args):
+    """--impl reference: the reference's own CPU Hogwild (oracle/_ref, built from
+    /root/reference/proj/src) with every host thread, same workload/metric."""
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    import oracle
+    if not oracle.reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return 0
+    ref = oracle.reference()
+    ds = ref.fixture_sparse(N_EX, D, AVG, SEED)
+    threads = ref.hardware_threads()
+    h = ref.to_handle(ds)
+    try:
+        epochs = args.warmup + args.steps
+        _, secs = _reference_time_epochs(ref, ds, PLAN, threads, epochs, 0.01, handle=h)
+    finally:
+        ref.lib.ref_ds_free(h)
+    timed = list(secs[args.warmup:]) or list(secs)
+    mean = float(np.mean(timed))
+    value = N_EX / mean
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": len(timed), "warmup": args.warmup,
+        "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference fixtures)",
+        "config": {"workload": WORKLOAD, "plan": PLAN, "workers": threads,
+                   "n": N_EX, "d": D},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{len(timed)} timed epochs of hogwild::train (+{args.warmup} "
+                                   f"warm-up), EpochRecord.seconds mean"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+    return 0
+
+
+# --------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1802_08800_b200 as S
+    from paper_1802_08800_b200 import distributed as SD
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    torch.cuda.init()
+    stream = torch.cuda.current_stream()
+    dev = S.Device(local, stream=stream.cuda_stream)
+    SD.attach(dev)
+
+    host = S.fixtures.sparse_classification(N_EX, D, AVG, SEED + rank)
+    dds = S.DeviceDataset(dev, host)
+    model = S.DeviceModel(dev, D)
+    plan = S.parse_plan(PLAN)
+    plan.workers = dev.resident_workers(dds) if args.workers <= 0 else args.workers
+    alpha = args.alpha
+    task = S.Task.SVM
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        S.hogwild_epoch(dds, model, task, alpha, plan)
+        if world > 1:
+            SD.average_ranks(dev, model, world)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    barrier()
+    launches0 = dev.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        barrier()
+        t_wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush, outside the event window
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        barrier()
+        t_wall1 = time.perf_counter()
+    launches = dev.launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * N_EX / (ms / 1e3)
+
+    # Dominant-kernel roofline: per-launch CUDA-event time of hogwild_kernel.
+    dev.set_profiling(True)
+    for _ in range(args.steps):
+        flush.zero_()
+        step()
+    stats = dev.kernel_stats()
+    dev.set_profiling(False)
+    name = "hogwild_kernel"
+    launches_k, total_ms = stats.get(name, (0, 0.0))
+    kern_ms = total_ms / max(1, launches_k)
+    sweep = dds.sweep_bytes()
+    peak, peak_src = _peaks()
+    achieved = sweep / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else 0.0
+    share = total_ms / max(1e-9, sum(v[1] for v in stats.values()))
+
+    # End to end through the public API with host buffers: per step, pinned-host
+    # fp32 CSR arrays -> device (sgdb_dataset_refresh_f32), the epoch, and the
+    # trained model back to the host (sgdb_model_get).
+    vals = torch.from_numpy(host.values.astype(np.float32)).pin_memory()
+    labs = torch.from_numpy(host.labels.astype(np.float32)).pin_memory()
+    idx = torch.from_numpy(host.indices.astype(np.int32)).pin_memory()
+    rp = torch.from_numpy(host.row_offsets.astype(np.int32)).pin_memory()
+    h2d = vals.numel() * 4 + labs.numel() * 4 + idx.numel() * 4 + rp.numel() * 4
+    d2h = D * 8
+    e2e_steps = max(3, args.steps)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        dds.refresh_f32(vals, labs, idx, rp)
+        step()
+        model.get()
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * N_EX / e2e_s
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference fixtures, seed+rank)",
+        "config": {"workload": WORKLOAD, "plan": PLAN, "workers": plan.workers,
+                   "lanes_per_worker": "auto", "alpha": alpha, "n_per_gpu": N_EX, "d": D,
+                   "nnz_per_gpu": dds.nnz, "l2": "flushed before every step (256 MiB memset, "
+                                                  "outside the event window)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": name,
+                     "kernel_ms": kern_ms, "kernel_share_of_step": share,
+                     "algorithmic_bytes_per_launch": sweep, "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "wall_s_timed_region": t_wall1 - t_wall0,
+        "step_ms_median": float(np.median(step_ms)),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(host)
+    if rank == 0 and not args.no_convergence:
+        out["convergence"] = convergence(S, dev, dds, plan, alpha, ms, out.get("cpu_baseline"))
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline(host):
+    """The unmodified reference (oracle/_ref) timed on this box's host cores:
+    hogwild::train, same data and plan, 1 worker (sequential Alg. 3)."""
+    import oracle
+    if not oracle.reference_available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    ref = oracle.reference()
+    h = ref.to_handle(host)
+    try:
+        epochs = 400
+        t0 = time.perf_counter()
+        _, secs = _reference_time_epochs(ref, host, PLAN, 1, epochs, 0.01, handle=h)
+        wall = time.perf_counter() - t0
+        threads = ref.hardware_threads()
+        _, secs_mt = _reference_time_epochs(ref, host, PLAN, threads, 100, 0.01, handle=h)
+    finally:
+        ref.lib.ref_ds_free(h)
+    v1 = N_EX / float(np.mean(secs))
+    vmt = N_EX / float(np.mean(secs_mt))
+    return {"value": v1, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"{epochs} epochs of the reference hogwild::train, 1 worker, full w8a-shaped "
+                      f"data ({wall:.1f} s wall incl. loss)",
+            "multithread": {"value": vmt, "cores": threads, "sample": "100 epochs"}}
+
+
+def convergence(S, dev, dds, plan, alpha, ms_epoch, cpu):
+    """Time to 1% of L* (harness.cpp:44-50): L* = min loss over GPU batch-GD probes
+    (alpha grid, harness.cpp:275-289) and the runs below."""
+    task = S.Task.SVM
+    l_star = float("inf")
+    for a in (1e-5, 1e-4, 1e-3, 1e-2):
+        r = S.sync.train(task, dds, S.Hyperparams(alpha=a, batch_b=dds.n_global, epochs=300,
+                                                  task=task), 0)
+        l_star = min([l_star] + [v for v in r.trace.losses() if np.isfinite(v)])
+    hp = S.Hyperparams(alpha=alpha, batch_b=1, epochs=100, task=task)
+    gpu = S.hogwild.train(task, dds, hp, plan, 0)
+    l_star = min([l_star] + gpu.trace.losses())
+    out = {"l_star": l_star, "gpu_epochs_to_1pct": _epochs_to(gpu.trace.losses(), l_star)}
+    if out["gpu_epochs_to_1pct"]:
+        out["gpu_time_to_1pct_s"] = out["gpu_epochs_to_1pct"] * ms_epoch / 1e3
+    try:
+        import oracle
+        if oracle.reference_available():
+            ref = oracle.reference()
+            host = dds.host
+            _, losses, secs, _ = ref.hogwild_train(host, 1, alpha, 100, PLAN, workers=1)
+            e = _epochs_to(list(losses), l_star)
+            out["cpu_epochs_to_1pct"] = e
+            if e:
+                out["cpu_time_to_1pct_s"] = float(np.sum(secs[:e]))
+    except Exception as exc:  # reported, not fatal
+        out["cpu_error"] = str(exc)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workers", type=int, default=0, help="0 = every resident lane group")
+    ap.add_argument("--alpha", type=float, default=0.01)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-convergence", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

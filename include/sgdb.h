@@ -181,6 +181,13 @@ sgdb_status sgdb_ctx_synchronize(sgdb_ctx* ctx);
 /* Number of this library's kernels launched on the context so far. */
 sgdb_status sgdb_ctx_launch_count(sgdb_ctx* ctx, uint64_t* out);
 sgdb_status sgdb_ctx_set_allreduce(sgdb_ctx* ctx, sgdb_allreduce_fn fn, void* user);
+/* Per-launch CUDA-event timing of this library's kernels on the context
+ * stream (off by default; enabling clears earlier records). Entry i of the
+ * per-kernel aggregate: name, launches, total milliseconds; *n_entries is the
+ * number of distinct kernels. */
+sgdb_status sgdb_ctx_set_profiling(sgdb_ctx* ctx, int32_t enable);
+sgdb_status sgdb_ctx_kernel_stats(sgdb_ctx* ctx, uint64_t i, char* name, uint64_t cap,
+                                  uint64_t* launches, double* total_ms, uint64_t* n_entries);
 /* Worker geometry the Hogwild kernels resolve for `lanes` lanes per worker
  * (0 = auto for this dataset): the number of concurrently resident workers. */
 sgdb_status sgdb_ctx_resident_workers(sgdb_ctx* ctx, const sgdb_dataset* ds,
@@ -241,6 +248,11 @@ sgdb_status sgdb_hogwild_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, i
  * mean (weights NULL = unweighted); when refresh != 0 every input is set to it. */
 sgdb_status sgdb_models_average(sgdb_ctx* ctx, sgdb_model* const* models, uint64_t count,
                                 const double* weights, sgdb_model* out, int32_t refresh);
+
+/* Multi-GPU replica averaging (the numa_dual_train merge generalised to G
+ * ranks, async_engine.cpp:478-501): SUM all-reduce of the fp64 model through
+ * the context's hook, then scale by 1/world. */
+sgdb_status sgdb_model_average_ranks(sgdb_ctx* ctx, sgdb_model* m, uint64_t world);
 
 /* dataset_loss (glm.cpp:85-94): sum of point losses, fp64. With an allreduce
  * hook set the per-shard sum is reduced across ranks. */

@@ -73,6 +73,9 @@ PROTOTYPES = {
     "sgdb_ctx_launch_count": (_S, [vp, P(u64)]),
     "sgdb_ctx_set_allreduce": (_S, [vp, ALLREDUCE_FN, vp]),
     "sgdb_ctx_resident_workers": (_S, [vp, vp, i32, P(u64)]),
+    "sgdb_ctx_set_profiling": (_S, [vp, i32]),
+    "sgdb_ctx_kernel_stats": (_S, [vp, u64, C.c_char_p, u64, P(u64), P(dbl), P(u64)]),
+    "sgdb_model_average_ranks": (_S, [vp, vp, u64]),
     "sgdb_dataset_upload": (_S, [vp, P(DatasetView), u64, u64, P(vp)]),
     "sgdb_dataset_refresh_f32": (_S, [vp, vp, vp, vp, vp, vp]),
     "sgdb_dataset_free": (_S, [vp]),

@@ -359,6 +359,28 @@ class Device:
         check(_lib().sgdb_ctx_launch_count(self._h, C.byref(n)))
         return int(n.value)
 
+    def set_profiling(self, enable: bool) -> None:
+        """Per-launch CUDA-event timing of the library's kernels (clears records)."""
+        check(_lib().sgdb_ctx_set_profiling(self._h, int(enable)))
+
+    def kernel_stats(self) -> dict:
+        """{kernel name: (launches, total ms)} since profiling was enabled."""
+        out, n = {}, L.u64(0)
+        check(_lib().sgdb_ctx_kernel_stats(self._h, 0, None, 0, None, None, C.byref(n)))
+        for i in range(int(n.value)):
+            name = C.create_string_buffer(128)
+            cnt, ms = L.u64(0), L.dbl(0)
+            check(_lib().sgdb_ctx_kernel_stats(self._h, i, name, 128, C.byref(cnt), C.byref(ms),
+                                               None))
+            out[name.value.decode()] = (int(cnt.value), float(ms.value))
+        return out
+
+    def resident_workers(self, dds: "DeviceDataset", lanes: int = 0) -> int:
+        """Lane groups the Hogwild kernels keep resident for `lanes` lanes/worker."""
+        n = L.u64(0)
+        check(_lib().sgdb_ctx_resident_workers(self._h, dds.handle, lanes, C.byref(n)))
+        return int(n.value)
+
     def set_allreduce(self, fn: Optional[Callable[[int, int, int, int], None]]):
         """fn(device_ptr, count, dtype(0=f32,1=f64), stream) sum-reduces in place."""
         if fn is None:

@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -204,6 +206,57 @@ sgdb_status sgdb_ctx_set_allreduce(sgdb_ctx* ctx, sgdb_allreduce_fn fn, void* us
   return sgdb_guard([&] {
     ctx->allreduce = fn;
     ctx->allreduce_user = user;
+  });
+}
+
+sgdb_status sgdb_ctx_set_profiling(sgdb_ctx* ctx, int32_t enable) {
+  return sgdb_guard([&] {
+    check(cudaStreamSynchronize(ctx->stream), "profiling sync");
+    for (auto& r : ctx->recs) {
+      cudaEventDestroy(r.start);
+      cudaEventDestroy(r.stop);
+    }
+    ctx->recs.clear();
+    ctx->profiling = enable != 0;
+  });
+}
+
+sgdb_status sgdb_ctx_kernel_stats(sgdb_ctx* ctx, uint64_t i, char* name, uint64_t cap,
+                                  uint64_t* launches, double* total_ms, uint64_t* n_entries) {
+  return sgdb_guard([&] {
+    check(cudaStreamSynchronize(ctx->stream), "stats sync");
+    std::vector<std::string> names;
+    std::vector<std::pair<uint64_t, double>> agg;
+    for (auto& r : ctx->recs) {
+      float ms = 0.f;
+      check(cudaEventElapsedTime(&ms, r.start, r.stop), "cudaEventElapsedTime");
+      auto it = std::find(names.begin(), names.end(), std::string(r.name));
+      if (it == names.end()) {
+        names.emplace_back(r.name);
+        agg.push_back({1, ms});
+      } else {
+        auto& a = agg[static_cast<size_t>(it - names.begin())];
+        a.first += 1;
+        a.second += ms;
+      }
+    }
+    if (n_entries) *n_entries = names.size();
+    if (i < names.size()) {
+      if (name && cap) std::snprintf(name, cap, "%s", names[i].c_str());
+      if (launches) *launches = agg[i].first;
+      if (total_ms) *total_ms = agg[i].second;
+    }
+  });
+}
+
+sgdb_status sgdb_model_average_ranks(sgdb_ctx* ctx, sgdb_model* m, uint64_t world) {
+  return sgdb_guard([&] {
+    require(world >= 1, "world size must be >= 1");
+    if (world == 1) return;
+    if (!ctx->allreduce) throw std::invalid_argument("no allreduce hook set on the context");
+    call_allreduce(*ctx, m->w64.p, m->d, 1);
+    scale_model(*m, 1.0 / static_cast<double>(world));
+    check(cudaStreamSynchronize(ctx->stream), "average_ranks sync");
   });
 }
 
@@ -530,6 +583,10 @@ sgdb_status sgdb_hogwild_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, i
     require(a.lanes == 1 || a.lanes == 2 || a.lanes == 4 || a.lanes == 8 || a.lanes == 16 ||
                 a.lanes == 32,
             "lanes_per_worker must be 1, 2, 4, 8, 16 or 32");
+    if (const char* e = std::getenv("SGDB_HOGWILD_MODE")) a.model_mode = std::atoi(e);
+    if (const char* e = std::getenv("SGDB_HOGWILD_REFRESH"))
+      a.refresh = static_cast<uint32_t>(std::max(1, std::atoi(e)));
+    if (const char* e = std::getenv("SGDB_HOGWILD_SPREAD")) a.spread = std::atoi(e) != 0;
     hogwild_epoch(*ds, *m, a);
     check(cudaStreamSynchronize(ctx->stream), "hogwild sync");
     if (evals_out) {

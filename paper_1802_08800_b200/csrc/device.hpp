@@ -60,7 +60,29 @@ struct Ctx {
   DBuf<double> loss_partials;  // per-block loss sums
   DBuf<double> loss_out;       // [0] loss, [1] scratch
   DBuf<unsigned> tickets;      // [0] loss ticket
+  // Optional per-launch CUDA-event timing (sgdb_ctx_set_profiling).
+  bool profiling = false;
+  struct LaunchRec {
+    const char* name;
+    cudaEvent_t start, stop;
+  };
+  std::vector<LaunchRec> recs;
 };
+
+// Bracket every kernel launch: prof_begin before, launched after.
+inline void prof_begin(Ctx& c, const char* name) {
+  if (!c.profiling) return;
+  Ctx::LaunchRec r{name, nullptr, nullptr};
+  check(cudaEventCreate(&r.start), "cudaEventCreate");
+  check(cudaEventCreate(&r.stop), "cudaEventCreate");
+  check(cudaEventRecord(r.start, c.stream), "cudaEventRecord");
+  c.recs.push_back(r);
+}
+inline void launched(Ctx& c, const char* what) {
+  ++c.launches;
+  check(cudaGetLastError(), what);
+  if (c.profiling && !c.recs.empty()) check(cudaEventRecord(c.recs.back().stop, c.stream), "cudaEventRecord");
+}
 
 // Device storage kind chosen at upload.
 enum class Kind { Dense, Csr };
@@ -112,6 +134,7 @@ struct Model {
   DBuf<int> finite;      // [0] 1 while every gradient entry was finite
   DBuf<double> scal;     // [0] ||g||^2
   DBuf<float> replicas;  // Hogwild replicas, R x ld
+  DBuf<float> spread;    // kernel-scope Hogwild model, slice-spread layout
   uint64_t n_replicas = 0, replica_ld = 0;
 };
 
@@ -151,10 +174,16 @@ struct HogwildArgs {
   uint64_t k = 0, workers = 1, group_size = 32;
   bool offsets = true;
   int lanes = 0;         // resolved lanes per worker
+  int model_mode = 1;    // kernel scope: 0 plain ld/st, 1 red.add, 2 smem mirror + red.add
+  uint32_t refresh = 4;  // mirror: refresh a read from L2 on every refresh-th example id
+  bool spread = true;    // kernel scope: 256 B-strided model copy during the epoch
 };
 int hogwild_auto_lanes(const Dataset& ds, int access);
 uint64_t hogwild_resident_workers(const Ctx& c, int lanes);
 void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a);
+
+// w64 *= scale; w32 = w64 (rank averaging after a SUM all-reduce).
+void scale_model(Model& m, double scale);
 
 void build_csc(Dataset& ds);
 void build_col(Dataset& ds);

@@ -29,6 +29,7 @@ constexpr int kKindPaddedCol = 3; // slot-major padded (stride n, sentinel d)
 
 constexpr int kScopeShared = 0;   // one model in global memory (kernel scope)
 constexpr int kScopeGlobalRep = 1;// replicas in global memory, replica = worker / gs
+constexpr int kScopeSharedAtomic = 2;  // one model, red.global.add updates
 
 struct HogParams {
   const float* val;
@@ -46,6 +47,8 @@ struct HogParams {
   float* model;
   uint64_t ld;
   float alpha;
+  uint32_t refresh;  // mirror kernel: refresh reads from L2 every `refresh` examples
+  uint32_t ms;       // kernel scope: float stride between model coordinates in global
 };
 
 template <int G>
@@ -62,15 +65,50 @@ __device__ __forceinline__ float group_sum_m(float v, unsigned mask) {
   return v;
 }
 
-struct GlobalModel {
+// Model access policies. `add(j, delta)` is the reference's
+// m.store(j, m.load(j) - alpha*(c*x)) with delta = -(alpha*(c*x)), which is the
+// same IEEE result (a - b == a + (-b)).
+struct GlobalModel {  // plain load / store: lost updates allowed (Hogwild)
   float* m;
-  __device__ float load(uint64_t j) const { return ld_model(m + j); }
-  __device__ void store(uint64_t j, float v) const { st_model(m + j, v); }
+  uint32_t ms;
+  __device__ float load(uint64_t j) const { return ld_model(m + j * ms); }
+  __device__ void add(uint64_t j, float delta) const {
+    st_model(m + j * ms, ld_model(m + j * ms) + delta);
+  }
 };
-struct SmemModel {
+struct GlobalAtomicModel {  // red.global.add.f32: every update lands
+  float* m;
+  uint32_t ms;
+  __device__ float load(uint64_t j) const { return ld_model(m + j * ms); }
+  __device__ void add(uint64_t j, float delta) const { atomicAdd(m + j * ms, delta); }
+};
+struct SmemModel {  // block-scope replica in shared memory, plain RMW
   volatile float* m;
   __device__ float load(uint64_t j) const { return m[j]; }
-  __device__ void store(uint64_t j, float v) const { m[j] = v; }
+  __device__ void add(uint64_t j, float delta) const { m[j] = m[j] + delta; }
+};
+// Kernel scope with a per-CTA shared-memory mirror of the shared model:
+// updates go to the global model (red.add) AND the mirror (smem atomic), so
+// a CTA sees its own updates at once and other CTAs' updates whenever a read
+// refreshes the coordinate from L2 (one example in `refresh`). Staleness is
+// bounded; with one worker every read sees every update (sequential Alg. 3).
+struct MirrorModel {
+  float* g;
+  uint32_t ms;
+  float* sm;
+  bool refresh;
+  __device__ float load(uint64_t j) const {
+    if (refresh) {
+      const float v = ld_model(g + j * ms);
+      sm[j] = v;
+      return v;
+    }
+    return *(volatile float*)(sm + j);
+  }
+  __device__ void add(uint64_t j, float delta) const {
+    atomicAdd(g + j * ms, delta);
+    atomicAdd(sm + j, delta);
+  }
 };
 
 // One example (process_examples body). Slot s of example e: value / index.
@@ -102,6 +140,11 @@ __device__ __forceinline__ void process_example(const HogParams& p, const M& m, 
   };
   auto value = [&](uint64_t s) -> float { return __ldg(p.val + base + s * stride); };
 
+  // A worker is sequential (Alg. 3): the lanes of the group must see each
+  // other's stores of the previous example before reading the model again.
+  // Under independent thread scheduling a lane with fewer slots could
+  // otherwise run ahead into this dot product.
+  __syncwarp(mask);
   float z = 0.f;
   for (uint64_t s = lg; s < len; s += G) z = fmaf(value(s), m.load(index(s)), z);
   z = group_sum_m<G>(z, mask);
@@ -112,15 +155,11 @@ __device__ __forceinline__ void process_example(const HogParams& p, const M& m, 
     // Circular offsets (async_engine.cpp:188-193): start at wid mod len.
     uint64_t s = wid % len;
     for (uint64_t i = 0; i < len; ++i) {
-      const uint64_t j = index(s);
-      m.store(j, m.load(j) - ac * (c * value(s)));
+      m.add(index(s), -(ac * (c * value(s))));
       if (++s == len) s = 0;
     }
   } else {
-    for (uint64_t s = lg; s < len; s += G) {
-      const uint64_t j = index(s);
-      m.store(j, m.load(j) - ac * (c * value(s)));
-    }
+    for (uint64_t s = lg; s < len; s += G) m.add(index(s), -(ac * (c * value(s))));
   }
 }
 
@@ -159,10 +198,37 @@ __global__ void __launch_bounds__(256) hogwild_kernel(HogParams p) {
   const uint64_t hg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
   const uint64_t HG = ((uint64_t)gridDim.x * blockDim.x) / G;
   for (uint64_t w = hg; w < p.T; w += HG) {
-    GlobalModel m{SCOPE == kScopeShared ? p.model : p.model + (w / p.gs) * p.ld};
     const WorkerList l = worker_list(p, w);
-    for (uint64_t i = 0; i < l.total; ++i)
-      process_example<G, TASK, KIND>(p, m, list_at(p, l, i), w, lg, mask);
+    if (SCOPE == kScopeSharedAtomic) {
+      GlobalAtomicModel m{p.model, p.ms};
+      for (uint64_t i = 0; i < l.total; ++i)
+        process_example<G, TASK, KIND>(p, m, list_at(p, l, i), w, lg, mask);
+    } else {
+      GlobalModel m{SCOPE == kScopeShared ? p.model : p.model + (w / p.gs) * p.ld,
+                    SCOPE == kScopeShared ? p.ms : 1u};
+      for (uint64_t i = 0; i < l.total; ++i)
+        process_example<G, TASK, KIND>(p, m, list_at(p, l, i), w, lg, mask);
+    }
+  }
+}
+
+// K5 with a per-CTA shared-memory mirror of the shared model (see MirrorModel).
+template <int G, int TASK, int KIND>
+__global__ void __launch_bounds__(256) hogwild_mirror_kernel(HogParams p) {
+  extern __shared__ float mirror[];
+  for (uint64_t j = threadIdx.x; j <= p.d; j += blockDim.x) mirror[j] = ld_model(p.model + j * p.ms);
+  __syncthreads();
+  const int lg = threadIdx.x % G;
+  const unsigned mask = group_mask<G>();
+  const uint64_t hg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const uint64_t HG = ((uint64_t)gridDim.x * blockDim.x) / G;
+  for (uint64_t w = hg; w < p.T; w += HG) {
+    const WorkerList l = worker_list(p, w);
+    for (uint64_t i = 0; i < l.total; ++i) {
+      const uint64_t e = list_at(p, l, i);
+      MirrorModel m{p.model, p.ms, mirror, p.refresh <= 1 || (e % p.refresh) == 0};
+      process_example<G, TASK, KIND>(p, m, e, w, lg, mask);
+    }
   }
 }
 
@@ -190,6 +256,25 @@ __global__ void __launch_bounds__(1024) hogwild_smem_kernel(HogParams p, const f
     __syncthreads();
     for (uint64_t j = threadIdx.x; j < p.d; j += blockDim.x) p.model[r * p.ld + j] = rep[j];
     __syncthreads();
+  }
+}
+
+// Slice-spread copy of the shared model for kernel scope: coordinate j at
+// float offset j*ms (ms*4 = 256 B), so concurrent red.add updates to
+// different coordinates land in different L2 slices instead of serialising on
+// the few lines a small model occupies (B300_MICROARCH.md, "L2-atom
+// multi-CTA": distinct >=128 B-spaced addresses are ~63x faster).
+__global__ void spread_kernel(uint64_t d, uint32_t ms, const float* w32, float* ws) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= d;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    ws[j * ms] = j < d ? w32[j] : 0.f;
+}
+__global__ void gather_kernel(uint64_t d, uint32_t ms, const float* ws, float* w32, double* w64) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const float v = ws[j * ms];
+    w32[j] = v;
+    w64[j] = static_cast<double>(v);
   }
 }
 
@@ -231,6 +316,15 @@ __global__ void models_mean_kernel(const double* const* ws, const double* wts, u
   }
 }
 
+__global__ void scale_model_kernel(uint64_t d, double scale, double* w64, float* w32) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const double v = w64[j] * scale;
+    w64[j] = v;
+    w32[j] = static_cast<float>(v);
+  }
+}
+
 __global__ void copy_model_kernel(uint64_t d, const double* src64, double* dst64, float* dst32) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
        j += (uint64_t)gridDim.x * blockDim.x) {
@@ -253,11 +347,6 @@ __global__ void transpose_kernel(const float* __restrict__ in, float* __restrict
     const uint64_t c = bx + i, r = by + threadIdx.x;
     if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
   }
-}
-
-void after_launch(Ctx& c, const char* what) {
-  ++c.launches;
-  check(cudaGetLastError(), what);
 }
 
 template <class Fn>
@@ -347,18 +436,51 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
   };
 
   if (a.replication == SGDB_REPL_KERNEL) {
-    p.model = m.w32.p;
     p.gs = 1;
     p.ld = 0;
     const unsigned grid = grid_threads(a.workers);
+    // Slice-spread layout for models that stay L2-resident when spread.
+    const uint32_t ms = (a.spread && ds.d <= (uint64_t{1} << 17)) ? 64u : 1u;
+    const unsigned dgrid = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>((ds.d + 256) / 256, c.num_sms * 8ull)));
+    if (ms > 1) {
+      m.spread.alloc((ds.d + 1) * ms);
+      prof_begin(c, "spread_kernel");
+      spread_kernel<<<dgrid, 256, 0, c.stream>>>(ds.d, ms, m.w32.p, m.spread.p);
+      launched(c, "spread_kernel");
+      p.model = m.spread.p;
+    } else {
+      p.model = m.w32.p;
+    }
+    p.ms = ms;
+    const size_t mirror_bytes = (ds.d + 1) * sizeof(float);
+    int mode = a.model_mode;
+    if (mode == 2 && mirror_bytes > 48 * 1024) mode = 1;  // mirror needs d+1 floats per CTA
+    p.refresh = a.refresh;
     dispatch_lanes(G, [&]<int GL>() {
       dispatch_kind(kind, [&]<int KD>() {
-        if (a.task == kTaskLR) hogwild_kernel<GL, kTaskLR, KD, kScopeShared><<<grid, 256, 0, c.stream>>>(p);
-        else hogwild_kernel<GL, kTaskSVM, KD, kScopeShared><<<grid, 256, 0, c.stream>>>(p);
+        prof_begin(c, "hogwild_kernel");
+        if (mode == 2) {
+          auto kern = a.task == kTaskLR ? hogwild_mirror_kernel<GL, kTaskLR, KD>
+                                        : hogwild_mirror_kernel<GL, kTaskSVM, KD>;
+          kern<<<grid, 256, mirror_bytes, c.stream>>>(p);
+        } else if (mode == 1) {
+          if (a.task == kTaskLR) hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomic><<<grid, 256, 0, c.stream>>>(p);
+          else hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomic><<<grid, 256, 0, c.stream>>>(p);
+        } else {
+          if (a.task == kTaskLR) hogwild_kernel<GL, kTaskLR, KD, kScopeShared><<<grid, 256, 0, c.stream>>>(p);
+          else hogwild_kernel<GL, kTaskSVM, KD, kScopeShared><<<grid, 256, 0, c.stream>>>(p);
+        }
       });
     });
-    after_launch(c, "hogwild_kernel");
-    sync_w64_from_w32(m);
+    launched(c, "hogwild_kernel");
+    if (ms > 1) {
+      prof_begin(c, "gather_kernel");
+      gather_kernel<<<dgrid, 256, 0, c.stream>>>(ds.d, ms, m.spread.p, m.w32.p, m.w64.p);
+      launched(c, "gather_kernel");
+    } else {
+      sync_w64_from_w32(m);
+    }
     return;
   }
 
@@ -371,6 +493,7 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
   m.replica_ld = ld;
   p.gs = gs;
   p.ld = ld;
+  p.ms = 1;
   p.model = m.replicas.p;
   const size_t rep_bytes = (ds.d + 1) * sizeof(float);
   const bool smem_ok = a.replication == SGDB_REPL_BLOCK && rep_bytes + 1024 <= c.max_smem_optin;
@@ -389,28 +512,32 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
         check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(rep_bytes)),
               "cudaFuncSetAttribute(hogwild_smem)");
+        prof_begin(c, "hogwild_smem_kernel");
         kern<<<grid, static_cast<unsigned>(threads), rep_bytes, c.stream>>>(p, m.w32.p, R);
       });
     });
-    after_launch(c, "hogwild_smem_kernel");
+    launched(c, "hogwild_smem_kernel");
   } else {
     const unsigned fill_grid = static_cast<unsigned>(
         std::max<uint64_t>(1, std::min<uint64_t>((R * ld + 255) / 256, c.num_sms * 8ull)));
+    prof_begin(c, "replicas_fill_kernel");
     replicas_fill_kernel<<<fill_grid, 256, 0, c.stream>>>(m.replicas.p, R, ld, ds.d, m.w32.p);
-    after_launch(c, "replicas_fill_kernel");
+    launched(c, "replicas_fill_kernel");
     const unsigned grid = grid_threads(a.workers);
     dispatch_lanes(G, [&]<int GL>() {
       dispatch_kind(kind, [&]<int KD>() {
+        prof_begin(c, "hogwild_kernel(replicas)");
         if (a.task == kTaskLR) hogwild_kernel<GL, kTaskLR, KD, kScopeGlobalRep><<<grid, 256, 0, c.stream>>>(p);
         else hogwild_kernel<GL, kTaskSVM, KD, kScopeGlobalRep><<<grid, 256, 0, c.stream>>>(p);
       });
     });
-    after_launch(c, "hogwild_kernel(replicas)");
+    launched(c, "hogwild_kernel(replicas)");
   }
   const unsigned mgrid = static_cast<unsigned>(
       std::max<uint64_t>(1, std::min<uint64_t>((ds.d + 255) / 256, c.num_sms * 8ull)));
+  prof_begin(c, "replicas_merge_kernel");
   replicas_merge_kernel<<<mgrid, 256, 0, c.stream>>>(m.replicas.p, R, ld, ds.d, m.w64.p, m.w32.p);
-  after_launch(c, "replicas_merge_kernel");
+  launched(c, "replicas_merge_kernel");
 }
 
 void average_models(Ctx& c, Model* const* models, uint64_t count, const double* weights,
@@ -437,18 +564,29 @@ void average_models(Ctx& c, Model* const* models, uint64_t count, const double* 
   }
   const unsigned grid =
       static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((d + 255) / 256, c.num_sms * 8ull)));
+  prof_begin(c, "models_mean_kernel");
   models_mean_kernel<<<grid, 256, 0, c.stream>>>(dptrs.p, weights ? dw.p : nullptr, count, total, d,
                                                  out.w64.p, out.w32.p);
-  after_launch(c, "models_mean_kernel");
+  launched(c, "models_mean_kernel");
   if (refresh) {
     for (uint64_t i = 0; i < count; ++i) {
       if (models[i] == &out) continue;
+      prof_begin(c, "copy_model_kernel");
       copy_model_kernel<<<grid, 256, 0, c.stream>>>(d, out.w64.p, models[i]->w64.p, models[i]->w32.p);
-      after_launch(c, "copy_model_kernel");
+      launched(c, "copy_model_kernel");
     }
   }
   // dptrs / dw are freed on scope exit; make sure the kernels consumed them.
   check(cudaStreamSynchronize(c.stream), "average_models sync");
+}
+
+void scale_model(Model& m, double scale) {
+  Ctx& c = *m.ctx;
+  const unsigned grid =
+      static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((m.d + 255) / 256, c.num_sms * 8ull)));
+  prof_begin(c, "scale_model_kernel");
+  scale_model_kernel<<<grid, 256, 0, c.stream>>>(m.d, scale, m.w64.p, m.w32.p);
+  launched(c, "scale_model_kernel");
 }
 
 void build_col(Dataset& ds) {
@@ -459,8 +597,9 @@ void build_col(Dataset& ds) {
   } else if (ds.kind == Kind::Dense) {
     ds.xcol.alloc(ds.n * ds.d);
     dim3 grid(static_cast<unsigned>((ds.d + 31) / 32), static_cast<unsigned>((ds.n + 31) / 32));
+    prof_begin(c, "transpose_kernel");
     transpose_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(ds.x.p, ds.xcol.p, ds.n, ds.d);
-    after_launch(c, "transpose_kernel");
+    launched(c, "transpose_kernel");
   } else {
     throw std::invalid_argument("column access paths on sparse data require the padded dense layout");
   }

@@ -536,11 +536,6 @@ unsigned grid_for(const Ctx& c, uint64_t items_per_block_unit, uint64_t units, u
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min(want, cap)));
 }
 
-void after_launch(Ctx& c, const char* what) {
-  ++c.launches;
-  check(cudaGetLastError(), what);
-}
-
 template <int L, int F, int TASK>
 void launch_dense_full_LF(Dataset& ds, Model& m, const StepArgs& a) {
   Ctx& c = *ds.ctx;
@@ -572,8 +567,9 @@ void launch_dense_full_LF(Dataset& ds, Model& m, const StepArgs& a) {
   check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem)),
         "cudaFuncSetAttribute(dense_full)");
+  prof_begin(c, "dense_full_kernel");
   kern<<<grid, 32 * (WC + 1), smem, c.stream>>>(p);
-  after_launch(c, "dense_full_kernel");
+  launched(c, "dense_full_kernel");
 }
 
 template <int L, int F, int TASK>
@@ -594,8 +590,9 @@ void launch_dense_batch_LF(Dataset& ds, Model& m, const uint32_t* ids, uint64_t 
     check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)),
           "cudaFuncSetAttribute(dense_batch)");
+  prof_begin(c, "dense_batch_kernel");
   kern<<<grid, 32 * W, smem, c.stream>>>(p);
-  after_launch(c, "dense_batch_kernel");
+  launched(c, "dense_batch_kernel");
 }
 
 template <int L, int F>
@@ -604,10 +601,11 @@ void launch_dense_loss_LF(Dataset& ds, Model& m, int task) {
   constexpr int RS = 32 / L;
   const unsigned grid = grid_for(c, 8ull * RS * 4, ds.n, 8);
   c.loss_partials.alloc(grid);
+  prof_begin(c, "dense_loss_kernel");
   dense_loss_kernel<L, F><<<grid, 256, 0, c.stream>>>(
       ds.x.p, ds.labels.p, ds.n, static_cast<int>(ds.d), m.w64.p, task,
       LossTail{c.loss_partials.p, c.tickets.p, c.loss_out.p});
-  after_launch(c, "dense_loss_kernel");
+  launched(c, "dense_loss_kernel");
 }
 
 // (L, F) per d: L lanes per row, F features per lane, L*F >= d.
@@ -626,30 +624,33 @@ template <int G, int TASK>
 void launch_csr_coef_G(Dataset& ds, Model& m) {
   Ctx& c = *ds.ctx;
   const unsigned grid = grid_for(c, 8ull * (32 / G) * 4, ds.n, 8);
+  prof_begin(c, "csr_coef_kernel");
   csr_coef_kernel<G, TASK><<<grid, 256, 0, c.stream>>>(ds.val.p, ds.idx.p, ds.rowptr.p,
                                                        ds.labels.p, ds.n, m.w32.p, ds.coef.p);
-  after_launch(c, "csr_coef_kernel");
+  launched(c, "csr_coef_kernel");
 }
 
 template <int G>
 void launch_csc_grad_G(Dataset& ds, Model& m, const StepArgs& a) {
   Ctx& c = *ds.ctx;
   const unsigned grid = grid_for(c, 8ull * (32 / G) * 4, ds.d, 8);
+  prof_begin(c, "csc_grad_kernel");
   csc_grad_kernel<G><<<grid, 256, 0, c.stream>>>(ds.cval.p, ds.crow.p, ds.colptr.p, ds.d,
                                                  ds.coef.p, a.alpha, a.apply ? 1 : 0,
                                                  a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p,
                                                  m.finite.p, m.scal.p);
-  after_launch(c, "csc_grad_kernel");
+  launched(c, "csc_grad_kernel");
 }
 
 template <int G, int TASK>
 void launch_csr_batch_G(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, bool check) {
   Ctx& c = *ds.ctx;
   const unsigned grid = grid_for(c, 8ull * (32 / G) * 2, nb, 8);
+  prof_begin(c, "csr_batch_kernel");
   csr_batch_kernel<G, TASK><<<grid, 256, 0, c.stream>>>(
       ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p, ds.n, ds.row_base, ids, nb, m.w32.p,
       m.g64.p, m.finite.p, check ? 1 : 0);
-  after_launch(c, "csr_batch_kernel");
+  launched(c, "csr_batch_kernel");
 }
 
 template <int G>
@@ -657,10 +658,11 @@ void launch_csr_loss_G(Dataset& ds, Model& m, int task) {
   Ctx& c = *ds.ctx;
   const unsigned grid = grid_for(c, 8ull * (32 / G) * 4, ds.n, 8);
   c.loss_partials.alloc(grid);
+  prof_begin(c, "csr_loss_kernel");
   csr_loss_kernel<G><<<grid, 256, 0, c.stream>>>(
       ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p, ds.n, m.w64.p, task,
       LossTail{c.loss_partials.p, c.tickets.p, c.loss_out.p});
-  after_launch(c, "csr_loss_kernel");
+  launched(c, "csr_loss_kernel");
 }
 
 template <class Fn>
@@ -716,9 +718,10 @@ void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, con
 void apply_update(Model& m, double alpha, bool want_norm) {
   Ctx& c = *m.ctx;
   const unsigned grid = grid_for(c, 256ull * 4, m.d, 8);
+  prof_begin(c, "apply_kernel");
   apply_kernel<<<grid, 256, 0, c.stream>>>(m.d, alpha, m.w64.p, m.w32.p, m.g64.p, m.finite.p,
                                            m.scal.p, want_norm ? 1 : 0);
-  after_launch(c, "apply_kernel");
+  launched(c, "apply_kernel");
 }
 
 void loss_launch(Dataset& ds, Model& m, int task) {
@@ -738,8 +741,9 @@ void loss_launch(Dataset& ds, Model& m, int task) {
 void sync_w64_from_w32(Model& m) {
   Ctx& c = *m.ctx;
   const unsigned grid = grid_for(c, 256ull * 4, m.d, 8);
+  prof_begin(c, "w64_from_w32_kernel");
   w64_from_w32_kernel<<<grid, 256, 0, c.stream>>>(m.d, m.w32.p, m.w64.p);
-  after_launch(c, "w64_from_w32_kernel");
+  launched(c, "w64_from_w32_kernel");
 }
 
 }  // namespace sgdb::dev

@@ -1,0 +1,72 @@
+"""Multi-GPU plumbing: one process per GPU, torch.distributed (NCCL) as the
+collective provider behind the engine's allreduce hook (include/sgdb.h,
+sgdb_allreduce_fn).
+
+The reference has no multi-device path; its closest analogs are
+the worker-count-invariant reduction of the sync path
+(proj/include/sgdbench/linalg.hpp:14-18) and numa_dual_train's replica
+averaging (proj/src/async_engine.cpp:462-520). Here:
+
+* sync SGD: rows are sharded in contiguous chunks
+  (``shard_rows``, the chunk rule of assign(), dataset.cpp:484-490); every
+  rank walks the same global mini-batch schedule, computes the partial
+  gradient of its members, the engine SUM-all-reduces g (fp64) and applies
+  the identical update on every rank.
+* Hogwild: each rank runs the Hogwild kernels on its replica and the models
+  are averaged every ``merge_period`` epochs (``average_ranks``).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from .api import Device, DeviceModel
+
+
+def shard_rows(n: int, rank: int, world: int) -> tuple[int, int]:
+    """(row_base, n_local) of rank's contiguous chunk: ceil(n/world) rows each."""
+    chunk = (n + world - 1) // world
+    base = min(n, rank * chunk)
+    return base, min(n, base + chunk) - base
+
+
+class _CudaArray:
+    """Zero-copy view of a device buffer for torch.as_tensor."""
+
+    def __init__(self, ptr: int, count: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None,
+                                         "stream": None}
+
+
+def device_view(ptr: int, count: int, dtype: int) -> torch.Tensor:
+    """torch tensor aliasing an engine buffer (dtype 0 = float32, 1 = float64)."""
+    return torch.as_tensor(_CudaArray(ptr, count, "<f4" if dtype == 0 else "<f8"), device="cuda")
+
+
+def sum_in_place(t: torch.Tensor, group=None) -> torch.Tensor:
+    """The collective the engine asks for: SUM all-reduce, in place."""
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def attach(dev: Device, group=None) -> None:
+    """Installs torch.distributed as the engine's allreduce hook on dev.
+
+    The engine calls the hook on its own stream; torch's current stream must be
+    that stream (create the Device with stream=torch.cuda.current_stream().cuda_stream).
+    """
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        dev.set_allreduce(None)
+        return
+
+    def hook(ptr, count, dtype, stream):
+        sum_in_place(device_view(ptr, count, dtype), group)
+
+    dev.set_allreduce(hook)
+
+
+def average_ranks(dev: Device, model: DeviceModel, world: int) -> None:
+    """Replica averaging across ranks: SUM all-reduce of the fp64 model, / world."""
+    L.check(L.load().sgdb_model_average_ranks(dev.handle, model.handle, world))
