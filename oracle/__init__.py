@@ -280,6 +280,10 @@ class Reference(_Lib):
     def hardware_threads(self) -> int:
         return int(self.lib.ref_hardware_threads())
 
+    def assign(self, n, workers, round_robin, k):
+        # ref_assign takes the reference's Strategy enum (RoundRobin = 0, Chunk = 1).
+        return super().assign(n, workers, 0 if round_robin else 1, k)
+
     def convert_layout(self, ds: HostData, target) -> HostData:
         h = self.to_handle(ds)
         try:
