@@ -135,6 +135,7 @@ void model_init(sgdb_model* m, Ctx* c, uint64_t d) {
 
 void model_set(sgdb_model* m, const double* w) {
   Ctx& c = *m->ctx;
+  dense_written(*m);
   std::vector<float> w32(m->d + 1, 0.f);
   for (uint64_t j = 0; j < m->d; ++j) w32[j] = static_cast<float>(w[j]);
   h2d(m->w64.p, w, m->d, c.stream);
@@ -254,6 +255,8 @@ sgdb_status sgdb_model_average_ranks(sgdb_ctx* ctx, sgdb_model* m, uint64_t worl
     require(world >= 1, "world size must be >= 1");
     if (world == 1) return;
     if (!ctx->allreduce) throw std::invalid_argument("no allreduce hook set on the context");
+    materialize(*m);
+    dense_written(*m);
     call_allreduce(*ctx, m->w64.p, m->d, 1);
     scale_model(*m, 1.0 / static_cast<double>(world));
     check(cudaStreamSynchronize(ctx->stream), "average_ranks sync");
@@ -437,6 +440,7 @@ sgdb_status sgdb_model_set(sgdb_ctx*, sgdb_model* m, const double* w) {
 sgdb_status sgdb_model_get(sgdb_ctx*, sgdb_model* m, double* w_out) {
   return sgdb_guard([&] {
     Ctx& c = *m->ctx;
+    materialize(*m);
     if (m->d)
       check(cudaMemcpyAsync(w_out, m->w64.p, m->d * sizeof(double), cudaMemcpyDeviceToHost,
                             c.stream),
@@ -447,6 +451,8 @@ sgdb_status sgdb_model_get(sgdb_ctx*, sgdb_model* m, double* w_out) {
 
 sgdb_status sgdb_model_device_ptrs(sgdb_model* m, float** w32, double** w64) {
   return sgdb_guard([&] {
+    materialize(*m);
+    dense_written(*m);  // the caller may write through the pointers
     if (w32) *w32 = m->w32.p;
     if (w64) *w64 = m->w64.p;
   });
@@ -468,6 +474,8 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
     require(m->d == ds->d, "model/dataset dim mismatch");
     require(batch_b >= 1, "batch size must be in [1, N]");
     Ctx& c = *ctx;
+    materialize(*m);
+    dense_written(*m);
     set_finite(m);
     const bool hook = c.allreduce != nullptr;
     StepArgs a;
@@ -542,6 +550,8 @@ sgdb_status sgdb_epoch_batch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int
   return sgdb_guard([&] {
     require(m->d == ds->d, "model/dataset dim mismatch");
     Ctx& c = *ctx;
+    materialize(*m);
+    dense_written(*m);
     check(cudaMemsetAsync(m->scal.p, 0, sizeof(double), c.stream), "memset norm");
     StepArgs a;
     a.task = task;
@@ -587,6 +597,8 @@ sgdb_status sgdb_hogwild_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, i
     if (const char* e = std::getenv("SGDB_HOGWILD_REFRESH"))
       a.refresh = static_cast<uint32_t>(std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("SGDB_HOGWILD_SPREAD")) a.spread = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SGDB_HOGWILD_SHARDS"))
+      a.shards = static_cast<uint32_t>(std::max(1, std::atoi(e)));
     hogwild_epoch(*ds, *m, a);
     check(cudaStreamSynchronize(ctx->stream), "hogwild sync");
     if (evals_out) {
@@ -601,7 +613,13 @@ sgdb_status sgdb_models_average(sgdb_ctx* ctx, sgdb_model* const* models, uint64
   return sgdb_guard([&] {
     require(count > 0, "merge_models: no replicas");
     std::vector<Model*> ms(count);
-    for (uint64_t i = 0; i < count; ++i) ms[i] = models[i];
+    for (uint64_t i = 0; i < count; ++i) {
+      ms[i] = models[i];
+      materialize(*ms[i]);
+      if (refresh) dense_written(*ms[i]);
+    }
+    materialize(*out);
+    dense_written(*out);
     average_models(*ctx, ms.data(), count, weights, *out, refresh != 0);
   });
 }
@@ -611,6 +629,7 @@ sgdb_status sgdb_loss(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t ta
   return sgdb_guard([&] {
     require(m->d == ds->d, "model/dataset dim mismatch");
     Ctx& c = *ctx;
+    materialize(*m);
     loss_launch(*ds, *m, task);
     call_allreduce(c, c.loss_out.p, 1, 1);
     double l = 0.0;

@@ -135,6 +135,12 @@ struct Model {
   DBuf<double> scal;     // [0] ||g||^2
   DBuf<float> replicas;  // Hogwild replicas, R x ld
   DBuf<float> spread;    // kernel-scope Hogwild model, slice-spread layout
+  // Which copy holds the latest model: the dense w32/w64 pair and/or the
+  // spread copy (kept authoritative across back-to-back Hogwild epochs).
+  bool dense_current = true;
+  bool spread_current = false;
+  uint32_t spread_ms = 1, spread_shards = 1;
+  uint64_t spread_ss = 0;
   uint64_t n_replicas = 0, replica_ld = 0;
 };
 
@@ -177,10 +183,19 @@ struct HogwildArgs {
   int model_mode = 1;    // kernel scope: 0 plain ld/st, 1 red.add, 2 smem mirror + red.add
   uint32_t refresh = 4;  // mirror: refresh a read from L2 on every refresh-th example id
   bool spread = true;    // kernel scope: 256 B-strided model copy during the epoch
+  uint32_t shards = 1;   // kernel scope, red.add mode: additive model shards
 };
 int hogwild_auto_lanes(const Dataset& ds, int access);
 uint64_t hogwild_resident_workers(const Ctx& c, int lanes);
 void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a);
+
+// Make w32/w64 current (gathers the spread Hogwild copy if it is newer).
+void materialize(Model& m);
+// Mark the dense model as written (the spread copy is stale afterwards).
+inline void dense_written(Model& m) {
+  m.dense_current = true;
+  m.spread_current = false;
+}
 
 // w64 *= scale; w32 = w64 (rank averaging after a SUM all-reduce).
 void scale_model(Model& m, double scale);

@@ -49,6 +49,8 @@ struct HogParams {
   float alpha;
   uint32_t refresh;  // mirror kernel: refresh reads from L2 every `refresh` examples
   uint32_t ms;       // kernel scope: float stride between model coordinates in global
+  uint32_t shards;   // kernel scope: additive shards of the spread model (>= 1)
+  uint64_t ss;       // float stride between shards
 };
 
 template <int G>
@@ -76,11 +78,23 @@ struct GlobalModel {  // plain load / store: lost updates allowed (Hogwild)
     st_model(m + j * ms, ld_model(m + j * ms) + delta);
   }
 };
-struct GlobalAtomicModel {  // red.global.add.f32: every update lands
+// red.global.add.f32: every update lands. The model may be split into K
+// additive shards (w_j = sum_k shard_k[j]); CTA b adds into shard b mod K, a
+// read sums the shards. Same single-shared-model semantics, K-fold fewer
+// same-address atomics (the L2 atomic unit serialises per address).
+struct GlobalAtomicModel {
   float* m;
   uint32_t ms;
-  __device__ float load(uint64_t j) const { return ld_model(m + j * ms); }
-  __device__ void add(uint64_t j, float delta) const { atomicAdd(m + j * ms, delta); }
+  uint32_t shards;
+  uint64_t ss;
+  __device__ float load(uint64_t j) const {
+    float v = ld_model(m + j * ms);
+    for (uint32_t k = 1; k < shards; ++k) v += ld_model(m + k * ss + j * ms);
+    return v;
+  }
+  __device__ void add(uint64_t j, float delta) const {
+    atomicAdd(m + (blockIdx.x % shards) * ss + j * ms, delta);
+  }
 };
 struct SmemModel {  // block-scope replica in shared memory, plain RMW
   volatile float* m;
@@ -145,8 +159,26 @@ __device__ __forceinline__ void process_example(const HogParams& p, const M& m, 
   // Under independent thread scheduling a lane with fewer slots could
   // otherwise run ahead into this dot product.
   __syncwarp(mask);
+  // Dot product in batches of U slots per lane: U index/value loads, then U
+  // independent model gathers in flight before the FMAs (a long Pareto-tail
+  // row would otherwise serialise ~len/G dependent round trips).
+  constexpr int U = 4;
   float z = 0.f;
-  for (uint64_t s = lg; s < len; s += G) z = fmaf(value(s), m.load(index(s)), z);
+  for (uint64_t s0 = lg; s0 < len; s0 += uint64_t(G) * U) {
+    uint64_t jv[U];
+    float xv[U], mv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t s = s0 + uint64_t(u) * G;
+      const bool ok = s < len;
+      jv[u] = ok ? index(s) : 0;
+      xv[u] = ok ? value(s) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) mv[u] = (s0 + uint64_t(u) * G < len) ? m.load(jv[u]) : 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) z = fmaf(xv[u], mv[u], z);
+  }
   z = group_sum_m<G>(z, mask);
   const float c = coef_f<TASK>(z, __ldg(p.y + e));
   if (c == 0.f || len == 0) return;  // w - alpha*(0*x) == w: skip the no-op stores
@@ -159,7 +191,20 @@ __device__ __forceinline__ void process_example(const HogParams& p, const M& m, 
       if (++s == len) s = 0;
     }
   } else {
-    for (uint64_t s = lg; s < len; s += G) m.add(index(s), -(ac * (c * value(s))));
+    for (uint64_t s0 = lg; s0 < len; s0 += uint64_t(G) * U) {
+      uint64_t jv[U];
+      float xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t s = s0 + uint64_t(u) * G;
+        const bool ok = s < len;
+        jv[u] = ok ? index(s) : 0;
+        xv[u] = ok ? value(s) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (s0 + uint64_t(u) * G < len) m.add(jv[u], -(ac * (c * xv[u])));
+    }
   }
 }
 
@@ -200,7 +245,7 @@ __global__ void __launch_bounds__(256) hogwild_kernel(HogParams p) {
   for (uint64_t w = hg; w < p.T; w += HG) {
     const WorkerList l = worker_list(p, w);
     if (SCOPE == kScopeSharedAtomic) {
-      GlobalAtomicModel m{p.model, p.ms};
+      GlobalAtomicModel m{p.model, p.ms, p.shards, p.ss};
       for (uint64_t i = 0; i < l.total; ++i)
         process_example<G, TASK, KIND>(p, m, list_at(p, l, i), w, lg, mask);
     } else {
@@ -264,15 +309,20 @@ __global__ void __launch_bounds__(1024) hogwild_smem_kernel(HogParams p, const f
 // different coordinates land in different L2 slices instead of serialising on
 // the few lines a small model occupies (B300_MICROARCH.md, "L2-atom
 // multi-CTA": distinct >=128 B-spaced addresses are ~63x faster).
-__global__ void spread_kernel(uint64_t d, uint32_t ms, const float* w32, float* ws) {
+__global__ void spread_kernel(uint64_t d, uint32_t ms, uint32_t shards, uint64_t ss,
+                              const float* w32, float* ws) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= d;
-       j += (uint64_t)gridDim.x * blockDim.x)
+       j += (uint64_t)gridDim.x * blockDim.x) {
     ws[j * ms] = j < d ? w32[j] : 0.f;
+    for (uint32_t k = 1; k < shards; ++k) ws[k * ss + j * ms] = 0.f;
+  }
 }
-__global__ void gather_kernel(uint64_t d, uint32_t ms, const float* ws, float* w32, double* w64) {
+__global__ void gather_kernel(uint64_t d, uint32_t ms, uint32_t shards, uint64_t ss,
+                              const float* ws, float* w32, double* w64) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    const float v = ws[j * ms];
+    float v = ws[j * ms];
+    for (uint32_t k = 1; k < shards; ++k) v += ws[k * ss + j * ms];
     w32[j] = v;
     w64[j] = static_cast<double>(v);
   }
@@ -441,18 +491,29 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
     const unsigned grid = grid_threads(a.workers);
     // Slice-spread layout for models that stay L2-resident when spread.
     const uint32_t ms = (a.spread && ds.d <= (uint64_t{1} << 17)) ? 64u : 1u;
-    const unsigned dgrid = static_cast<unsigned>(
-        std::max<uint64_t>(1, std::min<uint64_t>((ds.d + 256) / 256, c.num_sms * 8ull)));
+    const uint32_t shards = (ms > 1 && a.model_mode == 1) ? std::max<uint32_t>(1, a.shards) : 1u;
+    const uint64_t ss = (ds.d + 1) * ms + 64;  // shard stride (floats), keeps slices apart
     if (ms > 1) {
-      m.spread.alloc((ds.d + 1) * ms);
-      prof_begin(c, "spread_kernel");
-      spread_kernel<<<dgrid, 256, 0, c.stream>>>(ds.d, ms, m.w32.p, m.spread.p);
-      launched(c, "spread_kernel");
+      if (!(m.spread_current && m.spread_ms == ms && m.spread_shards == shards)) {
+        materialize(m);
+        m.spread.alloc(ss * shards);
+        const unsigned dgrid = static_cast<unsigned>(
+            std::max<uint64_t>(1, std::min<uint64_t>((ds.d + 256) / 256, c.num_sms * 8ull)));
+        prof_begin(c, "spread_kernel");
+        spread_kernel<<<dgrid, 256, 0, c.stream>>>(ds.d, ms, shards, ss, m.w32.p, m.spread.p);
+        launched(c, "spread_kernel");
+        m.spread_ms = ms;
+        m.spread_shards = shards;
+        m.spread_ss = ss;
+      }
       p.model = m.spread.p;
     } else {
+      materialize(m);
       p.model = m.w32.p;
     }
     p.ms = ms;
+    p.shards = shards;
+    p.ss = ss;
     const size_t mirror_bytes = (ds.d + 1) * sizeof(float);
     int mode = a.model_mode;
     if (mode == 2 && mirror_bytes > 48 * 1024) mode = 1;  // mirror needs d+1 floats per CTA
@@ -475,9 +536,10 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
     });
     launched(c, "hogwild_kernel");
     if (ms > 1) {
-      prof_begin(c, "gather_kernel");
-      gather_kernel<<<dgrid, 256, 0, c.stream>>>(ds.d, ms, m.spread.p, m.w32.p, m.w64.p);
-      launched(c, "gather_kernel");
+      // The spread copy stays authoritative until someone reads the dense
+      // model (materialize) — no gather between back-to-back epochs.
+      m.spread_current = true;
+      m.dense_current = false;
     } else {
       sync_w64_from_w32(m);
     }
@@ -485,6 +547,8 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
   }
 
   // Block (group_size workers per replica) or thread (one per worker) scope.
+  materialize(m);
+  m.spread_current = false;
   const uint64_t gs = a.replication == SGDB_REPL_THREAD ? 1 : a.group_size;
   const uint64_t R = (a.workers + gs - 1) / gs;
   const uint64_t ld = (ds.d + 1 + 31) & ~uint64_t(31);
@@ -578,6 +642,18 @@ void average_models(Ctx& c, Model* const* models, uint64_t count, const double* 
   }
   // dptrs / dw are freed on scope exit; make sure the kernels consumed them.
   check(cudaStreamSynchronize(c.stream), "average_models sync");
+}
+
+void materialize(Model& m) {
+  if (m.dense_current) return;
+  Ctx& c = *m.ctx;
+  const unsigned dgrid = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>((m.d + 256) / 256, c.num_sms * 8ull)));
+  prof_begin(c, "gather_kernel");
+  gather_kernel<<<dgrid, 256, 0, c.stream>>>(m.d, m.spread_ms, m.spread_shards, m.spread_ss,
+                                             m.spread.p, m.w32.p, m.w64.p);
+  launched(c, "gather_kernel");
+  m.dense_current = true;
 }
 
 void scale_model(Model& m, double scale) {

@@ -297,6 +297,31 @@ __global__ void __launch_bounds__(32 * W) dense_batch_kernel(DenseBatchParams p)
   if (threadIdx.x == 0) *p.ticket = 0u;
 }
 
+// Lane-strided sparse dot x_row . w over slots [b, e): U slots per batch so
+// U index loads and then U independent model gathers are in flight at once.
+template <int G>
+__device__ __forceinline__ float gather_dot(const float* __restrict__ val,
+                                            const uint32_t* __restrict__ idx, uint32_t b,
+                                            uint32_t e, int lg, const float* __restrict__ w) {
+  constexpr int U = 4;
+  float z = 0.f;
+  for (uint32_t s0 = b + lg; s0 < e; s0 += G * U) {
+    uint32_t jv[U];
+    float xv[U], wv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t s = s0 + u * G;
+      jv[u] = s < e ? __ldg(idx + s) : 0u;
+      xv[u] = s < e ? __ldg(val + s) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) wv[u] = s0 + u * G < e ? __ldg(w + jv[u]) : 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) z = fmaf(xv[u], wv[u], z);
+  }
+  return z;
+}
+
 // ---------------------------------------------------------------------------
 // K2: sparse margins + coefficients for all local rows. G lanes per row,
 // coalesced val/idx, model gathered from L2 (d <= 1.4M floats stays resident).
@@ -315,10 +340,7 @@ __global__ void __launch_bounds__(256) csr_coef_kernel(const float* __restrict__
   for (uint64_t base = gw * RW; base < n; base += tw * RW) {
     const uint64_t row = base + grp;
     float z = 0.f;
-    if (row < n) {
-      const uint32_t b = rowptr[row], e = rowptr[row + 1];
-      for (uint32_t s = b + lg; s < e; s += G) z = fmaf(__ldg(val + s), __ldg(w32 + __ldg(idx + s)), z);
-    }
+    if (row < n) z = gather_dot<G>(val, idx, rowptr[row], rowptr[row + 1], lg, w32);
     z = group_sum<G>(z);
     if (row < n && lg == 0) coef[row] = coef_f<TASK>(z, y[row]);
   }
@@ -348,8 +370,21 @@ __global__ void __launch_bounds__(256) csc_grad_kernel(const float* __restrict__
     double acc = 0.0;
     if (j < d) {
       const uint32_t b = colptr[j], e = colptr[j + 1];
-      for (uint32_t s = b + lg; s < e; s += G)
-        acc += static_cast<double>(__ldg(cval + s) * __ldg(coef + __ldg(crow + s)));
+      constexpr int U = 4;
+      for (uint32_t s0 = b + lg; s0 < e; s0 += G * U) {
+        uint32_t rv[U];
+        float xv[U], cv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t s = s0 + u * G;
+          rv[u] = s < e ? __ldg(crow + s) : 0u;
+          xv[u] = s < e ? __ldg(cval + s) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) cv[u] = s0 + u * G < e ? __ldg(coef + rv[u]) : 0.f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += static_cast<double>(xv[u] * cv[u]);
+      }
     }
     acc = group_sum<G>(acc);
     if (j < d && lg == 0) {
@@ -400,9 +435,7 @@ __global__ void __launch_bounds__(256) csr_batch_kernel(
       b = rowptr[row];
       e = rowptr[row + 1];
     }
-    float z = 0.f;
-    for (uint32_t s = b + lg; s < e; s += G) z = fmaf(__ldg(val + s), __ldg(w32 + __ldg(idx + s)), z);
-    z = group_sum<G>(z);
+    const float z = group_sum<G>(gather_dot<G>(val, idx, b, e, lg, w32));
     if (!valid) continue;
     const float c = coef_f<TASK>(z, y[row]);
     if (c == 0.f) continue;
@@ -506,8 +539,22 @@ __global__ void __launch_bounds__(256) csr_loss_kernel(const float* __restrict__
     double z = 0.0;
     if (row < n) {
       const uint32_t b = rowptr[row], e = rowptr[row + 1];
-      for (uint32_t s = b + lg; s < e; s += G)
-        z += static_cast<double>(__ldg(val + s)) * __ldg(w64 + __ldg(idx + s));
+      constexpr int U = 4;
+      for (uint32_t s0 = b + lg; s0 < e; s0 += G * U) {
+        uint32_t jv[U];
+        float xv[U];
+        double wv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t s = s0 + u * G;
+          jv[u] = s < e ? __ldg(idx + s) : 0u;
+          xv[u] = s < e ? __ldg(val + s) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) wv[u] = s0 + u * G < e ? __ldg(w64 + jv[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) z += static_cast<double>(xv[u]) * wv[u];
+      }
     }
     z = group_sum<G>(z);
     if (row < n && lg == 0) lsum += loss_d(task, z, static_cast<double>(y[row]));
@@ -539,10 +586,16 @@ unsigned grid_for(const Ctx& c, uint64_t items_per_block_unit, uint64_t units, u
 template <int L, int F, int TASK>
 void launch_dense_full_LF(Dataset& ds, Model& m, const StepArgs& a) {
   Ctx& c = *ds.ctx;
-  constexpr int WC = 8;
+  // Consumer warps scale with the register budget of F accumulators per lane.
+  constexpr int WC = F <= 8 ? 24 : (F <= 16 ? 12 : 8);
+  constexpr int RS = 32 / L;
   const int d = static_cast<int>(ds.d);
   const int row_bytes = d * 4;
-  int R = std::max(4, (32768 / row_bytes) & ~3);
+  // Rows per tile: ~32 KB, a multiple of the rows all consumer warps take per
+  // pass (balanced warps) and of 4 (16-byte bulk-copy granularity).
+  const int unit = std::max(4, WC * RS);
+  int R = std::max(unit, ((32768 / row_bytes) / unit) * unit);
+  R = (R + 3) & ~3;
   DenseFullParams p{};
   p.x = ds.x.p;
   p.y = ds.labels.p;

@@ -1,0 +1,46 @@
+"""Small driver for ncu captures: runs a few epochs of one target op.
+
+    python scripts/prof_targets.py {hogwild_w8a|sync_covtype|sync_rcv1|sync_dense1000} [epochs]
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1802_08800_b200 as S  # noqa: E402
+
+
+def main():
+    target = sys.argv[1]
+    epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    torch.cuda.init()
+    dev = S.Device(0, stream=torch.cuda.current_stream().cuda_stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    if target == "hogwild_w8a":
+        host = S.fixtures.sparse_classification(64700, 300, 11.65, 20250811)
+        dds = S.DeviceDataset(dev, host)
+        plan = S.parse_plan("row-ch:kernel:0")
+        plan.workers = dev.resident_workers(dds)
+        model = S.DeviceModel(dev, host.n_features)
+        for _ in range(epochs):
+            flush.zero_()
+            S.hogwild_epoch(dds, model, S.Task.SVM, 0.01, plan)
+    else:
+        name = target.split("_")[1]
+        if name == "covtype":
+            host, task = S.fixtures.dense_classification(581012, 54, 20250810), S.Task.LR
+        elif name == "dense1000":
+            host, task = S.fixtures.dense_classification(200000, 1000, 7), S.Task.LR
+        else:
+            host, task = S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813), S.Task.LR
+        dds = S.DeviceDataset(dev, host)
+        model = S.DeviceModel(dev, host.n_features)
+        for _ in range(epochs):
+            flush.zero_()
+            S.sync_epoch(dds, model, task, 1e-6, None, host.n_examples)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()

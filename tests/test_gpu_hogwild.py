@@ -191,20 +191,20 @@ def test_acceptance5_eight_workers(sgdb, acceptance5, plan_text, lanes):
     assert en is not None and en <= 3 * e1, (en, e1)
 
 
-def test_block_scope_replicas_converge(sgdb, acceptance5):
-    """Block scope at GPU scale (2 replicas of 2048 racing workers, merged by
-    mean each epoch, async_engine.cpp:311-331): the loss decreases steadily and
-    ends within 5% of L* (replica averaging halves the per-epoch progress, so
-    the 1% target of the kernel-scope test is not the right yardstick)."""
+@pytest.mark.parametrize("workers,gs,lanes", [(4096, 2048, 0), (4096, 2048, 32), (64, 32, 0),
+                                              (8, 4, 0)])
+def test_block_scope_loss_curve_tracks_oracle(sgdb, dev, orc, workers, gs, lanes):
+    """Block scope with racing workers per replica (async_engine.cpp:293-331):
+    the per-epoch loss curve stays within 2% of the serialized-worker oracle
+    (one legal Hogwild interleaving) on acceptance 5's fixture."""
     S = sgdb
-    dds, l_star, _ = acceptance5
+    ds = S.fixtures.sparse_classification(20000, 10000, 50.0, 20250810).rounded_f32()
     plan = S.parse_plan("row-ch:block:0")
-    plan.workers, plan.group_size = 4096, 2048
-    r = S.hogwild.train(S.Task.SVM, dds, _inc(S, S.Task.SVM, 0.1, 60, 0.97), plan, 0)
-    losses = r.trace.losses()
-    assert not r.trace.diverged
-    assert losses[-1] <= 1.05 * l_star, (losses[-1], l_star)
-    assert losses[-1] < losses[0]
+    plan.workers, plan.group_size, plan.lanes_per_worker = workers, gs, lanes
+    r = S.hogwild.train(S.Task.SVM, ds, _inc(S, S.Task.SVM, 0.1, 5, 0.97), plan, 0, device=dev)
+    _, ol, _ = orc.hogwild_serial(ds, 1, 0.1, 5, 0, 1, 0, workers, group_size=gs, decay=0.97)
+    for e in range(5):
+        assert rel(r.trace.epochs[e].loss, ol[e]) <= 0.02, (e, r.trace.losses(), list(ol))
 
 
 @pytest.mark.parametrize("plan_text,workers,gs", [("row-ch:kernel:0", 4096, 32),
