@@ -227,7 +227,8 @@ sgdb_status sgdb_model_free(sgdb_model* m);
  * batch_b; per batch g = X_B^T c(X_B w) then w -= alpha*g. With
  * batch_b >= n_global the epoch is one full-batch step and `order` is not
  * read. *finite_out = 0 if any gradient entry was non-finite (the epoch stops
- * after that batch, as the reference does). */
+ * after that batch, as the reference does); passing finite_out == NULL makes
+ * the call fully asynchronous on the context stream. */
 sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
                             double alpha, const uint32_t* order, uint64_t batch_b,
                             int32_t* finite_out);
@@ -241,7 +242,9 @@ sgdb_status sgdb_epoch_batch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int
                              double alpha, double* grad_norm_out);
 
 /* One Hogwild epoch of `plan` (async_engine.cpp:244-254 + 372-396): replica
- * prepare, the workers' passes, replica merge. *evals_out = n + T_nonempty*k. */
+ * prepare, the workers' passes, replica merge. *evals_out = n + T_nonempty*k.
+ * Asynchronous on the context stream (like a kernel launch): synchronise, or
+ * read the model, before using results on the host. */
 sgdb_status sgdb_hogwild_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
                                double alpha, const sgdb_plan* plan, uint64_t* evals_out);
 /* merge_models (async_engine.cpp:133-156) over device models: out = weighted

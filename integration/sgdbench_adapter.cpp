@@ -1,0 +1,215 @@
+// Drop-in adapter: the reference's training entry points, implemented on the
+// B200 engine through the C-ABI of include/sgdb.h.
+//
+// Compiled against the reference's own headers (proj/include/sgdbench), it
+// defines exactly the symbols a maintainer replaces:
+//   sgdbench::sync::batch_gradient   proj/include/sgdbench/sync_engine.hpp:33-36
+//   sgdbench::sync::epoch_batch      proj/include/sgdbench/sync_engine.hpp:40-41
+//   sgdbench::sync::train            proj/include/sgdbench/sync_engine.hpp:51-52
+//   sgdbench::hogwild::train         proj/include/sgdbench/async_engine.hpp:96-97
+//   sgdbench::hogwild::numa_dual_train proj/include/sgdbench/async_engine.hpp:102-104
+// Everything else (dataset I/O, plan grammar, harness, warp simulator) stays
+// the reference's. See INTEGRATION.md for the two ways to link it (replace
+// sync_engine.cpp / the engine half of async_engine.cpp, or interpose the
+// shared library ahead of libsgdbench).
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "sgdb.h"
+#include "sgdbench/async_engine.hpp"
+#include "sgdbench/sync_engine.hpp"
+
+namespace {
+
+void throw_for(sgdb_status st) {
+  if (st == SGDB_OK) return;
+  const std::string msg = sgdb_last_error();
+  switch (st) {
+    case SGDB_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case SGDB_ERR_DOMAIN: throw std::domain_error(msg);
+    case SGDB_ERR_CAPACITY: throw sgdbench::CapacityError(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+sgdb_ctx* context() {
+  static sgdb_ctx* ctx = [] {
+    sgdb_ctx* c = nullptr;
+    throw_for(sgdb_ctx_create(0, nullptr, &c));
+    return c;
+  }();
+  return ctx;
+}
+
+// sgdbench::Dataset and sgdb_dataset_view carry the same fields.
+sgdb_dataset_view view_of(const sgdbench::Dataset& ds) {
+  static_assert(sizeof(std::size_t) == sizeof(std::uint64_t));
+  sgdb_dataset_view v{};
+  v.n_examples = ds.n_examples;
+  v.n_features = ds.n_features;
+  v.layout = static_cast<int32_t>(ds.layout);
+  v.labels = ds.labels.data();
+  v.values = ds.values.data();
+  v.n_values = ds.values.size();
+  v.indices = ds.indices.data();
+  v.n_indices = ds.indices.size();
+  v.row_offsets = reinterpret_cast<const std::uint64_t*>(ds.row_offsets.data());
+  v.n_row_offsets = ds.row_offsets.size();
+  v.padded_width = ds.padded_width;
+  return v;
+}
+
+struct Uploaded {
+  sgdb_dataset* ds = nullptr;
+  explicit Uploaded(const sgdbench::Dataset& d) {
+    const sgdb_dataset_view v = view_of(d);
+    throw_for(sgdb_dataset_upload(context(), &v, 0, 0, &ds));
+  }
+  ~Uploaded() { sgdb_dataset_free(ds); }
+};
+
+struct Model {
+  sgdb_model* m = nullptr;
+  Model(std::size_t d, const double* init) { throw_for(sgdb_model_create(context(), d, init, &m)); }
+  ~Model() { sgdb_model_free(m); }
+};
+
+sgdb_plan plan_of(const sgdbench::ExecutionPlan& p) {
+  sgdb_plan c{};
+  c.access_path = static_cast<int32_t>(p.access_path);
+  c.replication = static_cast<int32_t>(p.model_replication);
+  c.data_replication_k = p.data_replication_k;
+  c.workers = p.workers;
+  c.group_size = p.group_size;
+  c.circular_offsets = p.circular_offsets ? 1 : 0;
+  c.merge_period_epochs = p.merge_period_epochs;
+  c.lanes_per_worker = 0;
+  return c;
+}
+
+sgdb_hyperparams hyper_of(sgdbench::Task task, const sgdbench::Hyperparams& h) {
+  return sgdb_hyperparams{h.alpha, h.batch_b, h.epochs, static_cast<int32_t>(task), h.step_decay};
+}
+
+// Trampolines for the injectable Clock and epoch hook.
+struct Callbacks {
+  const sgdbench::Clock* clock;
+  const std::function<void(std::size_t, double)>* hook;
+};
+double clock_tramp(void* u) { return static_cast<Callbacks*>(u)->clock->now_seconds(); }
+void hook_tramp(void* u, uint64_t e, double l) { (*static_cast<Callbacks*>(u)->hook)(e, l); }
+
+sgdb_train_options options_of(Callbacks& cb, bool shuffle, double max_seconds,
+                              const std::vector<double>& init) {
+  sgdb_train_options o{};
+  o.workers = 1;
+  o.shuffle = shuffle ? 1 : 0;
+  o.max_seconds = max_seconds;
+  o.initial_model = init.empty() ? nullptr : init.data();
+  o.initial_model_len = init.size();
+  o.clock = clock_tramp;
+  o.clock_user = &cb;
+  if (*cb.hook) {
+    o.epoch_hook = hook_tramp;
+    o.hook_user = &cb;
+  }
+  return o;
+}
+
+sgdbench::LossTrace trace_of(const sgdb_trace& t, const std::vector<sgdb_epoch_record>& recs) {
+  sgdbench::LossTrace lt;
+  for (std::size_t i = 0; i < t.count; ++i) lt.epochs.push_back({recs[i].epoch, recs[i].loss, recs[i].seconds});
+  lt.diverged = t.diverged != 0;
+  lt.divergence_note = t.divergence_note;
+  return lt;
+}
+
+sgdbench::hogwild::Result run_hogwild(bool dual, sgdbench::Task task, const sgdbench::Dataset& ds,
+                                      const sgdbench::Hyperparams& hyper,
+                                      const sgdbench::ExecutionPlan& plan, std::uint64_t seed,
+                                      const sgdbench::hogwild::Options& options) {
+  sgdbench::validate_plan(plan, ds);
+  if (ds.n_examples == 0) throw std::invalid_argument("cannot train on an empty dataset");
+  hyper.validate(ds.n_examples);
+  Uploaded up(ds);
+  const sgdb_hyperparams h = hyper_of(task, hyper);
+  const sgdb_plan p = plan_of(plan);
+  Callbacks cb{&options.clock, &options.epoch_hook};
+  const sgdb_train_options o = options_of(cb, true, options.max_seconds, options.initial_model);
+  std::vector<sgdb_epoch_record> recs(hyper.epochs);
+  std::vector<uint64_t> evals(hyper.epochs);
+  sgdb_trace t{};
+  t.epochs = recs.data();
+  t.evals_per_epoch = evals.data();
+  t.capacity = hyper.epochs;
+  sgdbench::hogwild::Result r;
+  r.model.resize(ds.n_features);
+  throw_for(dual ? sgdb_numa_dual_train(context(), up.ds, &h, &p, seed, &o, r.model.data(), &t)
+                 : sgdb_hogwild_train(context(), up.ds, &h, &p, seed, &o, r.model.data(), &t));
+  r.trace = trace_of(t, recs);
+  r.evals_per_epoch.assign(evals.begin(), evals.begin() + static_cast<std::ptrdiff_t>(t.count));
+  return r;
+}
+
+}  // namespace
+
+namespace sgdbench {
+namespace sync {
+
+linalg::DenseVector batch_gradient(Task task, const Dataset& ds,
+                                   std::span<const std::uint32_t> rows,
+                                   std::span<const double> w, unsigned, const Dataset*) {
+  if (w.size() != ds.n_features) throw std::invalid_argument("matvec: dimension mismatch");
+  Uploaded up(ds);
+  linalg::DenseVector g(ds.n_features, 0.0);
+  throw_for(sgdb_batch_gradient(context(), up.ds, static_cast<int32_t>(task), rows.data(),
+                                rows.size(), w.data(), g.data()));
+  return g;
+}
+
+double epoch_batch(Task task, const Dataset& ds, std::vector<double>& w, double alpha, unsigned) {
+  Uploaded up(ds);
+  Model m(ds.n_features, w.data());
+  double norm = 0.0;
+  throw_for(sgdb_epoch_batch(context(), up.ds, m.m, static_cast<int32_t>(task), alpha, &norm));
+  throw_for(sgdb_model_get(context(), m.m, w.data()));
+  return norm;
+}
+
+TrainResult train(Task task, const Dataset& ds, const Hyperparams& hyper, std::uint64_t seed,
+                  const TrainOptions& options) {
+  hyper.validate(ds.n_examples);
+  if (ds.n_examples == 0) throw std::invalid_argument("cannot train on an empty dataset");
+  Uploaded up(ds);
+  const sgdb_hyperparams h = hyper_of(task, hyper);
+  Callbacks cb{&options.clock, &options.epoch_hook};
+  const sgdb_train_options o = options_of(cb, options.shuffle, options.max_seconds,
+                                          options.initial_model);
+  std::vector<sgdb_epoch_record> recs(hyper.epochs);
+  sgdb_trace t{};
+  t.epochs = recs.data();
+  t.capacity = hyper.epochs;
+  TrainResult r;
+  r.model.resize(ds.n_features);
+  throw_for(sgdb_sync_train(context(), up.ds, &h, seed, &o, r.model.data(), &t));
+  r.trace = trace_of(t, recs);
+  return r;
+}
+
+}  // namespace sync
+
+namespace hogwild {
+
+Result train(Task task, const Dataset& ds, const Hyperparams& hyper, const ExecutionPlan& plan,
+             std::uint64_t seed, const Options& options) {
+  return run_hogwild(false, task, ds, hyper, plan, seed, options);
+}
+
+Result numa_dual_train(Task task, const Dataset& ds, const Hyperparams& hyper,
+                       const ExecutionPlan& plan, std::uint64_t seed, const Options& options) {
+  return run_hogwild(true, task, ds, hyper, plan, seed, options);
+}
+
+}  // namespace hogwild
+}  // namespace sgdbench

@@ -326,9 +326,12 @@ class Schedule:
         return out
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib().sgdb_schedule_free(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib().sgdb_schedule_free(self._h)
+                self._h = None
+        except Exception:  # interpreter teardown
+            pass
 
 
 # ---- device objects ---------------------------------------------------------------
@@ -336,7 +339,13 @@ class Device:
     """A device context: CUDA device + the stream all ops are queued on."""
 
     def __init__(self, ordinal: int = 0, stream: Optional[int] = None):
+        """stream: a CUDA stream handle to queue every op on (e.g.
+        torch.cuda.current_stream().cuda_stream); handle 0 — torch's default
+        stream — means the legacy default stream (cudaStreamLegacy), not
+        "create one". None: the context creates its own stream."""
         self._h = L.vp()
+        if stream is not None and int(stream) == 0:
+            stream = 1  # cudaStreamLegacy
         check(_lib().sgdb_ctx_create(ordinal, stream, C.byref(self._h)))
         self._allreduce_cb = None
         self.ordinal = ordinal
@@ -406,7 +415,10 @@ class Device:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter teardown
+            pass
 
 
 class DeviceDataset:
@@ -450,7 +462,10 @@ class DeviceDataset:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter teardown
+            pass
 
 
 class DeviceModel:
@@ -487,7 +502,10 @@ class DeviceModel:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter teardown
+            pass
 
 
 # ---- device ops (layer 1) -------------------------------------------------------------

@@ -509,8 +509,8 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
         }
       }
     }
-    const int f = read_finite(m);
-    if (finite_out) *finite_out = f;
+    // finite_out == NULL: fully asynchronous on the context stream.
+    if (finite_out) *finite_out = read_finite(m);
   });
 }
 
@@ -597,10 +597,7 @@ sgdb_status sgdb_hogwild_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, i
     if (const char* e = std::getenv("SGDB_HOGWILD_REFRESH"))
       a.refresh = static_cast<uint32_t>(std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("SGDB_HOGWILD_SPREAD")) a.spread = std::atoi(e) != 0;
-    if (const char* e = std::getenv("SGDB_HOGWILD_SHARDS"))
-      a.shards = static_cast<uint32_t>(std::max(1, std::atoi(e)));
     hogwild_epoch(*ds, *m, a);
-    check(cudaStreamSynchronize(ctx->stream), "hogwild sync");
     if (evals_out) {
       const bool rr = plan->access_path == SGDB_ACCESS_ROW_RR || plan->access_path == SGDB_ACCESS_COL_RR;
       *evals_out = ds->n + nonempty_workers(ds->n, plan->workers, rr) * plan->data_replication_k;

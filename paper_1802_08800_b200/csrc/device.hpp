@@ -139,8 +139,7 @@ struct Model {
   // spread copy (kept authoritative across back-to-back Hogwild epochs).
   bool dense_current = true;
   bool spread_current = false;
-  uint32_t spread_ms = 1, spread_shards = 1;
-  uint64_t spread_ss = 0;
+  uint32_t spread_ms = 1;
   uint64_t n_replicas = 0, replica_ld = 0;
 };
 
@@ -183,7 +182,6 @@ struct HogwildArgs {
   int model_mode = 1;    // kernel scope: 0 plain ld/st, 1 red.add, 2 smem mirror + red.add
   uint32_t refresh = 4;  // mirror: refresh a read from L2 on every refresh-th example id
   bool spread = true;    // kernel scope: 256 B-strided model copy during the epoch
-  uint32_t shards = 1;   // kernel scope, red.add mode: additive model shards
 };
 int hogwild_auto_lanes(const Dataset& ds, int access);
 uint64_t hogwild_resident_workers(const Ctx& c, int lanes);

@@ -151,6 +151,7 @@ LoopResult hogwild_loop(sgdb_ctx* ctx, sgdb_dataset* ds, Task task, const Hyperp
       throw_status(sgdb_models_average(ctx, pair, 2, nullptr, merged->m, merge_due ? 1 : 0));
       view = merged->m;
     }
+    throw_status(sgdb_ctx_synchronize(ctx));  // epoch work is stream-asynchronous
     const double t1 = o.now();
     r.evals.push_back(static_cast<std::size_t>(ea + eb));
     const double loss = device_loss(ctx, ds, view, task);

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "device.hpp"
@@ -29,7 +30,9 @@ constexpr int kKindPaddedCol = 3; // slot-major padded (stride n, sentinel d)
 
 constexpr int kScopeShared = 0;   // one model in global memory (kernel scope)
 constexpr int kScopeGlobalRep = 1;// replicas in global memory, replica = worker / gs
-constexpr int kScopeSharedAtomic = 2;  // one model, red.global.add updates
+constexpr int kScopeSharedAtomic = 2;      // one model, red.global.add, slice-spread layout
+constexpr int kScopeSharedAtomicFlat = 3;  // one model, red.global.add, contiguous layout
+constexpr uint32_t kSpread = 64;           // floats between coordinates (256 B)
 
 struct HogParams {
   const float* val;
@@ -49,8 +52,7 @@ struct HogParams {
   float alpha;
   uint32_t refresh;  // mirror kernel: refresh reads from L2 every `refresh` examples
   uint32_t ms;       // kernel scope: float stride between model coordinates in global
-  uint32_t shards;   // kernel scope: additive shards of the spread model (>= 1)
-  uint64_t ss;       // float stride between shards
+  uint32_t variant;  // diagnostic knob (SGDB_HOGWILD_VARIANT)
 };
 
 template <int G>
@@ -73,31 +75,31 @@ __device__ __forceinline__ float group_sum_m(float v, unsigned mask) {
 struct GlobalModel {  // plain load / store: lost updates allowed (Hogwild)
   float* m;
   uint32_t ms;
-  __device__ float load(uint64_t j) const { return ld_model(m + j * ms); }
-  __device__ void add(uint64_t j, float delta) const {
-    st_model(m + j * ms, ld_model(m + j * ms) + delta);
+  __device__ GlobalModel at(uint64_t) const { return *this; }
+  __device__ float load(uint32_t j) const { return ld_model(m + uint64_t(j) * ms); }
+  __device__ void add(uint32_t j, float delta) const {
+    st_model(m + uint64_t(j) * ms, ld_model(m + uint64_t(j) * ms) + delta);
   }
 };
-// red.global.add.f32: every update lands. The model may be split into K
-// additive shards (w_j = sum_k shard_k[j]); CTA b adds into shard b mod K, a
-// read sums the shards. Same single-shared-model semantics, K-fold fewer
-// same-address atomics (the L2 atomic unit serialises per address).
+// red.global.add.f32: every update lands (no lost updates). MS = float stride
+// between coordinates (64 = the slice-spread layout, a compile-time constant
+// so the gather address is a shift).
+template <uint32_t MS>
 struct GlobalAtomicModel {
   float* m;
-  uint32_t ms;
-  uint32_t shards;
-  uint64_t ss;
-  __device__ float load(uint64_t j) const {
-    float v = ld_model(m + j * ms);
-    for (uint32_t k = 1; k < shards; ++k) v += ld_model(m + k * ss + j * ms);
-    return v;
+  uint32_t variant;  // diagnostic: 1 = non-coherent reads, 2 = no updates
+  __device__ GlobalAtomicModel at(uint64_t) const { return *this; }
+  __device__ float load(uint32_t j) const {
+    if (variant == 1) return __ldg(m + uint64_t(j) * MS);
+    return ld_model(m + uint64_t(j) * MS);
   }
-  __device__ void add(uint64_t j, float delta) const {
-    atomicAdd(m + (blockIdx.x % shards) * ss + j * ms, delta);
+  __device__ void add(uint32_t j, float delta) const {
+    if (variant != 2) atomicAdd(m + uint64_t(j) * MS, delta);
   }
 };
 struct SmemModel {  // block-scope replica in shared memory, plain RMW
   volatile float* m;
+  __device__ SmemModel at(uint64_t) const { return *this; }
   __device__ float load(uint64_t j) const { return m[j]; }
   __device__ void add(uint64_t j, float delta) const { m[j] = m[j] + delta; }
 };
@@ -110,7 +112,11 @@ struct MirrorModel {
   float* g;
   uint32_t ms;
   float* sm;
+  uint32_t period;
   bool refresh;
+  __device__ MirrorModel at(uint64_t e) const {
+    return MirrorModel{g, ms, sm, period, period <= 1 || (e % period) == 0};
+  }
   __device__ float load(uint64_t j) const {
     if (refresh) {
       const float v = ld_model(g + j * ms);
@@ -125,113 +131,170 @@ struct MirrorModel {
   }
 };
 
-// One example (process_examples body). Slot s of example e: value / index.
-template <int G, int TASK, int KIND, class M>
-__device__ __forceinline__ void process_example(const HogParams& p, const M& m, uint64_t e,
-                                                uint64_t wid, int lg, unsigned mask) {
-  uint64_t base, len, stride;
-  if (KIND == kKindCsr) {
-    base = p.rowptr[e];
-    len = p.rowptr[e + 1] - base;
-    stride = 1;
-  } else if (KIND == kKindDenseRow) {
-    base = e * p.d;
-    len = p.d;
-    stride = 1;
-  } else if (KIND == kKindDenseCol) {
-    base = e;
-    len = p.d;
-    stride = p.n;
-  } else {
-    base = e;
-    len = p.pw;
-    stride = p.n;
-  }
-  auto index = [&](uint64_t s) -> uint64_t {
-    if (KIND == kKindCsr) return __ldg(p.idx + base + s);
-    if (KIND == kKindPaddedCol) return __ldg(p.idx + base + s * stride);
-    return s;
-  };
-  auto value = [&](uint64_t s) -> float { return __ldg(p.val + base + s * stride); };
+// ---- one worker: its assign() list, a 2-stage prefetch pipeline, and the
+// per-example body of process_examples (async_engine.cpp:178-195) ----------
 
+constexpr int kU = 4;  // slots per lane per batch (U loads / gathers in flight)
+
+// Worker w's assign() list (dataset.cpp:470-503), generated on the fly:
+// base ids then k wrapped extras after the last base id.
+// (Example ids fit 32 bits: n_global <= 2^32 is enforced at upload.)
+struct WorkerList {
+  uint32_t first, step, cnt, total, last;
+};
+__device__ __forceinline__ WorkerList worker_list(const HogParams& p, uint64_t w) {
+  WorkerList l;
+  const uint64_t n = p.n;
+  if (p.rr) {
+    l.cnt = w < n ? static_cast<uint32_t>((n - 1 - w) / p.T + 1) : 0u;
+    l.first = static_cast<uint32_t>(w);
+    l.step = static_cast<uint32_t>(p.T);
+  } else {
+    const uint64_t chunk = (n + p.T - 1) / p.T;
+    const uint64_t b = w * chunk, e = min(n, b + chunk);
+    l.cnt = e > b ? static_cast<uint32_t>(e - b) : 0u;
+    l.first = static_cast<uint32_t>(min(b, n));
+    l.step = 1;
+  }
+  l.total = l.cnt ? l.cnt + static_cast<uint32_t>(p.k) : 0u;
+  l.last = l.cnt ? l.first + (l.cnt - 1) * l.step : 0u;
+  return l;
+}
+__device__ __forceinline__ uint32_t list_at(const HogParams& p, const WorkerList& l, uint32_t i) {
+  return i < l.cnt ? l.first + i * l.step
+                   : static_cast<uint32_t>((uint64_t(l.last) + 1 + (i - l.cnt)) % p.n);
+}
+
+// Example e's slots. Contiguous kinds (CSR, dense row): slots [b, bend).
+// Strided kinds (dense col, padded col): base b = e, bend = slot count.
+struct Row {
+  uint32_t e;
+  uint32_t b, bend;  // CSR offsets (< 2^32, enforced at upload) or strided base/count
+  float y;           // label, prefetched with the extent
+};
+template <int KIND>
+__device__ __forceinline__ Row make_row(const HogParams& p, uint32_t e) {
+  const float y = __ldg(p.y + e);  // loads issued here are consumed iterations later
+  if (KIND == kKindCsr) return {e, p.rowptr[e], p.rowptr[e + 1], y};
+  if (KIND == kKindDenseRow) return {e, 0u, static_cast<uint32_t>(p.d), y};  // base = e*d
+  if (KIND == kKindDenseCol) return {e, e, static_cast<uint32_t>(p.d), y};
+  return {e, e, static_cast<uint32_t>(p.pw), y};
+}
+template <int KIND>
+__device__ __forceinline__ uint32_t row_len(const Row& r) {
+  return KIND == kKindCsr ? r.bend - r.b : r.bend;
+}
+template <int KIND>
+__device__ __forceinline__ uint64_t row_base(const HogParams& p, const Row& r) {
+  return KIND == kKindDenseRow ? uint64_t(r.e) * p.d : uint64_t(r.b);
+}
+template <int KIND>
+__device__ __forceinline__ uint32_t slot_index(const HogParams& p, const Row& r, uint32_t s) {
+  if (KIND == kKindCsr) return __ldg(p.idx + r.b + s);
+  if (KIND == kKindPaddedCol) return __ldg(p.idx + r.b + uint64_t(s) * p.n);
+  return s;
+}
+template <int KIND>
+__device__ __forceinline__ float slot_value(const HogParams& p, const Row& r, uint32_t s) {
+  if (KIND == kKindCsr) return __ldg(p.val + r.b + s);
+  if (KIND == kKindDenseRow) return __ldg(p.val + row_base<KIND>(p, r) + s);
+  return __ldg(p.val + r.b + uint64_t(s) * p.n);
+}
+
+struct Batch {
+  uint32_t j[kU];
+  float x[kU];
+};
+// Lane lg's U slots s0, s0+G, ... of row r (zeros past the end).
+template <int G, int KIND>
+__device__ __forceinline__ Batch load_batch(const HogParams& p, const Row& r, uint32_t s0,
+                                            uint32_t len) {
+  Batch bt;
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const uint32_t s = s0 + u * G;
+    const bool ok = s < len;
+    bt.j[u] = ok ? slot_index<KIND>(p, r, s) : 0u;
+    bt.x[u] = ok ? slot_value<KIND>(p, r, s) : 0.f;
+  }
+  return bt;
+}
+
+// One example: margin over every slot (padded sentinels read the guard slot
+// w[d] == 0), coefficient (glm.cpp:30-34), lock-free update. `first` holds
+// this lane's first batch, prefetched by the worker loop.
+template <int G, int TASK, int KIND, class M>
+__device__ __forceinline__ void process_example(const HogParams& p, const M& m, const Row& r,
+                                                const Batch& first, uint64_t wid, int lg,
+                                                unsigned mask) {
+  const uint32_t len = row_len<KIND>(r);
   // A worker is sequential (Alg. 3): the lanes of the group must see each
-  // other's stores of the previous example before reading the model again.
-  // Under independent thread scheduling a lane with fewer slots could
+  // other's updates of the previous example before reading the model again;
+  // under independent thread scheduling a lane with fewer slots could
   // otherwise run ahead into this dot product.
   __syncwarp(mask);
-  // Dot product in batches of U slots per lane: U index/value loads, then U
-  // independent model gathers in flight before the FMAs (a long Pareto-tail
-  // row would otherwise serialise ~len/G dependent round trips).
-  constexpr int U = 4;
   float z = 0.f;
-  for (uint64_t s0 = lg; s0 < len; s0 += uint64_t(G) * U) {
-    uint64_t jv[U];
-    float xv[U], mv[U];
+  {
+    float mv[kU];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t s = s0 + uint64_t(u) * G;
-      const bool ok = s < len;
-      jv[u] = ok ? index(s) : 0;
-      xv[u] = ok ? value(s) : 0.f;
-    }
+    for (int u = 0; u < kU; ++u) mv[u] = (lg + u * G < len) ? m.load(first.j[u]) : 0.f;
 #pragma unroll
-    for (int u = 0; u < U; ++u) mv[u] = (s0 + uint64_t(u) * G < len) ? m.load(jv[u]) : 0.f;
+    for (int u = 0; u < kU; ++u) z = fmaf(first.x[u], mv[u], z);
+  }
+  for (uint32_t s0 = lg + G * kU; s0 < len; s0 += G * kU) {
+    const Batch bt = load_batch<G, KIND>(p, r, s0, len);
+    float mv[kU];
 #pragma unroll
-    for (int u = 0; u < U; ++u) z = fmaf(xv[u], mv[u], z);
+    for (int u = 0; u < kU; ++u) mv[u] = (s0 + u * G < len) ? m.load(bt.j[u]) : 0.f;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) z = fmaf(bt.x[u], mv[u], z);
   }
   z = group_sum_m<G>(z, mask);
-  const float c = coef_f<TASK>(z, __ldg(p.y + e));
+  const float c = coef_f<TASK>(z, r.y);
   if (c == 0.f || len == 0) return;  // w - alpha*(0*x) == w: skip the no-op stores
   const float ac = p.alpha;
   if (G == 1 && p.offsets) {
     // Circular offsets (async_engine.cpp:188-193): start at wid mod len.
-    uint64_t s = wid % len;
-    for (uint64_t i = 0; i < len; ++i) {
-      m.add(index(s), -(ac * (c * value(s))));
+    uint32_t s = static_cast<uint32_t>(wid % len);
+    for (uint32_t i = 0; i < len; ++i) {
+      m.add(slot_index<KIND>(p, r, s), -(ac * (c * slot_value<KIND>(p, r, s))));
       if (++s == len) s = 0;
     }
-  } else {
-    for (uint64_t s0 = lg; s0 < len; s0 += uint64_t(G) * U) {
-      uint64_t jv[U];
-      float xv[U];
+    return;
+  }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t s = s0 + uint64_t(u) * G;
-        const bool ok = s < len;
-        jv[u] = ok ? index(s) : 0;
-        xv[u] = ok ? value(s) : 0.f;
-      }
+  for (int u = 0; u < kU; ++u)
+    if (lg + u * G < len) m.add(first.j[u], -(ac * (c * first.x[u])));
+  for (uint32_t s0 = lg + G * kU; s0 < len; s0 += G * kU) {
+    const Batch bt = load_batch<G, KIND>(p, r, s0, len);
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (s0 + uint64_t(u) * G < len) m.add(jv[u], -(ac * (c * xv[u])));
-    }
+    for (int u = 0; u < kU; ++u)
+      if (s0 + u * G < len) m.add(bt.j[u], -(ac * (c * bt.x[u])));
   }
 }
 
-// Worker w's assign() list (dataset.cpp:470-503), generated on the fly:
-// base ids then k wrapped extras after the last base id.
-struct WorkerList {
-  uint64_t first, step, cnt, total, last;
-};
-__device__ __forceinline__ WorkerList worker_list(const HogParams& p, uint64_t w) {
-  WorkerList l;
-  if (p.rr) {
-    l.cnt = w < p.n ? (p.n - 1 - w) / p.T + 1 : 0;
-    l.first = w;
-    l.step = p.T;
-  } else {
-    const uint64_t chunk = (p.n + p.T - 1) / p.T;
-    const uint64_t b = w * chunk, e = min(p.n, b + chunk);
-    l.cnt = e > b ? e - b : 0;
-    l.first = b;
-    l.step = 1;
+// Worker w walks its list with a 2-stage software pipeline: while example i
+// runs, the row extent of example i+2 and the first slot batch of example
+// i+1 are already in flight (data only — the model is always read fresh, so
+// the single-worker schedule is exactly sequential Alg. 3).
+template <int G, int TASK, int KIND, class M>
+__device__ __forceinline__ void run_worker(const HogParams& p, const M& m, uint64_t w, int lg,
+                                           unsigned mask) {
+  const WorkerList l = worker_list(p, w);
+  if (l.total == 0) return;
+  Row cur = make_row<KIND>(p, list_at(p, l, 0));
+  Row nxt = l.total > 1 ? make_row<KIND>(p, list_at(p, l, 1)) : cur;
+  Batch bcur = load_batch<G, KIND>(p, cur, lg, row_len<KIND>(cur));
+  for (uint32_t i = 0; i < l.total; ++i) {
+    Batch bnxt = bcur;
+    Row after = nxt;
+    if (i + 1 < l.total) bnxt = load_batch<G, KIND>(p, nxt, lg, row_len<KIND>(nxt));
+    if (i + 2 < l.total) after = make_row<KIND>(p, list_at(p, l, i + 2));
+    process_example<G, TASK, KIND>(p, m.at(cur.e), cur, bcur, w, lg, mask);
+    cur = nxt;
+    bcur = bnxt;
+    nxt = after;
   }
-  l.total = l.cnt ? l.cnt + p.k : 0;
-  l.last = l.cnt ? l.first + (l.cnt - 1) * l.step : 0;
-  return l;
-}
-__device__ __forceinline__ uint64_t list_at(const HogParams& p, const WorkerList& l, uint64_t i) {
-  return i < l.cnt ? l.first + i * l.step : (l.last + 1 + (i - l.cnt)) % p.n;
 }
 
 // K5 (kernel scope, shared model) and the global-replica variant (block scope
@@ -243,16 +306,16 @@ __global__ void __launch_bounds__(256) hogwild_kernel(HogParams p) {
   const uint64_t hg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
   const uint64_t HG = ((uint64_t)gridDim.x * blockDim.x) / G;
   for (uint64_t w = hg; w < p.T; w += HG) {
-    const WorkerList l = worker_list(p, w);
     if (SCOPE == kScopeSharedAtomic) {
-      GlobalAtomicModel m{p.model, p.ms, p.shards, p.ss};
-      for (uint64_t i = 0; i < l.total; ++i)
-        process_example<G, TASK, KIND>(p, m, list_at(p, l, i), w, lg, mask);
+      run_worker<G, TASK, KIND>(p, GlobalAtomicModel<kSpread>{p.model, p.variant}, w, lg, mask);
+    } else if (SCOPE == kScopeSharedAtomicFlat) {
+      run_worker<G, TASK, KIND>(p, GlobalAtomicModel<1>{p.model, p.variant}, w, lg, mask);
     } else {
-      GlobalModel m{SCOPE == kScopeShared ? p.model : p.model + (w / p.gs) * p.ld,
-                    SCOPE == kScopeShared ? p.ms : 1u};
-      for (uint64_t i = 0; i < l.total; ++i)
-        process_example<G, TASK, KIND>(p, m, list_at(p, l, i), w, lg, mask);
+      run_worker<G, TASK, KIND>(
+          p,
+          GlobalModel{SCOPE == kScopeShared ? p.model : p.model + (w / p.gs) * p.ld,
+                      SCOPE == kScopeShared ? p.ms : 1u},
+          w, lg, mask);
     }
   }
 }
@@ -267,14 +330,8 @@ __global__ void __launch_bounds__(256) hogwild_mirror_kernel(HogParams p) {
   const unsigned mask = group_mask<G>();
   const uint64_t hg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
   const uint64_t HG = ((uint64_t)gridDim.x * blockDim.x) / G;
-  for (uint64_t w = hg; w < p.T; w += HG) {
-    const WorkerList l = worker_list(p, w);
-    for (uint64_t i = 0; i < l.total; ++i) {
-      const uint64_t e = list_at(p, l, i);
-      MirrorModel m{p.model, p.ms, mirror, p.refresh <= 1 || (e % p.refresh) == 0};
-      process_example<G, TASK, KIND>(p, m, e, w, lg, mask);
-    }
-  }
+  for (uint64_t w = hg; w < p.T; w += HG)
+    run_worker<G, TASK, KIND>(p, MirrorModel{p.model, p.ms, mirror, p.refresh, false}, w, lg, mask);
 }
 
 // K6 (block scope): CTA r owns replica r in shared memory, loaded from the
@@ -290,13 +347,10 @@ __global__ void __launch_bounds__(1024) hogwild_smem_kernel(HogParams p, const f
   for (uint64_t r = blockIdx.x; r < R; r += gridDim.x) {
     for (uint64_t j = threadIdx.x; j <= p.d; j += blockDim.x) rep[j] = j < p.d ? w32[j] : 0.f;
     __syncthreads();
-    SmemModel m{rep};
     for (uint64_t t = gi; t < p.gs; t += NG) {
       const uint64_t w = r * p.gs + t;
       if (w >= p.T) break;
-      const WorkerList l = worker_list(p, w);
-      for (uint64_t i = 0; i < l.total; ++i)
-        process_example<G, TASK, KIND>(p, m, list_at(p, l, i), w, lg, mask);
+      run_worker<G, TASK, KIND>(p, SmemModel{rep}, w, lg, mask);
     }
     __syncthreads();
     for (uint64_t j = threadIdx.x; j < p.d; j += blockDim.x) p.model[r * p.ld + j] = rep[j];
@@ -309,20 +363,15 @@ __global__ void __launch_bounds__(1024) hogwild_smem_kernel(HogParams p, const f
 // different coordinates land in different L2 slices instead of serialising on
 // the few lines a small model occupies (B300_MICROARCH.md, "L2-atom
 // multi-CTA": distinct >=128 B-spaced addresses are ~63x faster).
-__global__ void spread_kernel(uint64_t d, uint32_t ms, uint32_t shards, uint64_t ss,
-                              const float* w32, float* ws) {
+__global__ void spread_kernel(uint64_t d, uint32_t ms, const float* w32, float* ws) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= d;
-       j += (uint64_t)gridDim.x * blockDim.x) {
+       j += (uint64_t)gridDim.x * blockDim.x)
     ws[j * ms] = j < d ? w32[j] : 0.f;
-    for (uint32_t k = 1; k < shards; ++k) ws[k * ss + j * ms] = 0.f;
-  }
 }
-__global__ void gather_kernel(uint64_t d, uint32_t ms, uint32_t shards, uint64_t ss,
-                              const float* ws, float* w32, double* w64) {
+__global__ void gather_kernel(uint64_t d, uint32_t ms, const float* ws, float* w32, double* w64) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    float v = ws[j * ms];
-    for (uint32_t k = 1; k < shards; ++k) v += ws[k * ss + j * ms];
+    const float v = ws[j * ms];
     w32[j] = v;
     w64[j] = static_cast<double>(v);
   }
@@ -425,17 +474,34 @@ void dispatch_kind(int kind, Fn&& fn) {
 
 int hogwild_auto_lanes(const Dataset& ds, int access) {
   if (access == SGDB_ACCESS_COL_RR || access == SGDB_ACCESS_COL_CH) return 1;
+  // Row paths: one warp per example (the paper's GPU kernel). Narrower lane
+  // groups pack more workers per warp but lose on Pareto-tail rows; measured
+  // on w8a (avg 11.7 nnz) G=32 was fastest (scripts/hogwild_lanes.py).
   const double avg = ds.kind == Kind::Dense
                          ? static_cast<double>(ds.d)
                          : (ds.n ? static_cast<double>(ds.nnz) / static_cast<double>(ds.n) : 1.0);
-  if (avg <= 6.0) return 4;
-  if (avg <= 12.0) return 8;
-  if (avg <= 24.0) return 16;
-  return 32;
+  return avg <= 2.0 ? 8 : 32;
+}
+
+// One resident wave: CTAs/SM from the occupancy calculator for this kernel
+// instance, capped by the CTAs the workers need.
+template <class K>
+unsigned wave_grid(const Ctx& c, K kern, size_t smem, uint64_t workers, int lanes) {
+  int per_sm = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem), "occupancy");
+  const uint64_t cap = static_cast<uint64_t>(std::max(1, per_sm)) * c.num_sms;
+  const uint64_t need = (workers * static_cast<uint64_t>(lanes) + 255) / 256;
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min(need, cap)));
 }
 
 uint64_t hogwild_resident_workers(const Ctx& c, int lanes) {
-  return static_cast<uint64_t>(c.num_sms) * c.max_threads_per_sm / std::max(1, lanes);
+  uint64_t out = 0;
+  dispatch_lanes(lanes, [&]<int GL>() {
+    const unsigned grid = wave_grid(c, hogwild_kernel<GL, kTaskSVM, kKindCsr, kScopeSharedAtomic>, 0,
+                                    ~uint64_t(0) / 64, GL);
+    out = static_cast<uint64_t>(grid) * 256 / GL;
+  });
+  return out;
 }
 
 void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
@@ -479,32 +545,22 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
   p.alpha = a.alpha;
   const int G = a.lanes;
 
-  const uint64_t resident_threads = static_cast<uint64_t>(c.num_sms) * c.max_threads_per_sm;
-  auto grid_threads = [&](uint64_t workers) {
-    const uint64_t threads = std::min<uint64_t>(workers * G, resident_threads);
-    return static_cast<unsigned>(std::max<uint64_t>(1, (threads + 255) / 256));
-  };
 
   if (a.replication == SGDB_REPL_KERNEL) {
     p.gs = 1;
     p.ld = 0;
-    const unsigned grid = grid_threads(a.workers);
     // Slice-spread layout for models that stay L2-resident when spread.
-    const uint32_t ms = (a.spread && ds.d <= (uint64_t{1} << 17)) ? 64u : 1u;
-    const uint32_t shards = (ms > 1 && a.model_mode == 1) ? std::max<uint32_t>(1, a.shards) : 1u;
-    const uint64_t ss = (ds.d + 1) * ms + 64;  // shard stride (floats), keeps slices apart
+    const uint32_t ms = (a.spread && ds.d <= (uint64_t{1} << 17)) ? kSpread : 1u;
     if (ms > 1) {
-      if (!(m.spread_current && m.spread_ms == ms && m.spread_shards == shards)) {
+      if (!(m.spread_current && m.spread_ms == ms)) {
         materialize(m);
-        m.spread.alloc(ss * shards);
+        m.spread.alloc((ds.d + 1) * ms);
         const unsigned dgrid = static_cast<unsigned>(
             std::max<uint64_t>(1, std::min<uint64_t>((ds.d + 256) / 256, c.num_sms * 8ull)));
         prof_begin(c, "spread_kernel");
-        spread_kernel<<<dgrid, 256, 0, c.stream>>>(ds.d, ms, shards, ss, m.w32.p, m.spread.p);
+        spread_kernel<<<dgrid, 256, 0, c.stream>>>(ds.d, ms, m.w32.p, m.spread.p);
         launched(c, "spread_kernel");
         m.spread_ms = ms;
-        m.spread_shards = shards;
-        m.spread_ss = ss;
       }
       p.model = m.spread.p;
     } else {
@@ -512,26 +568,32 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
       p.model = m.w32.p;
     }
     p.ms = ms;
-    p.shards = shards;
-    p.ss = ss;
+    if (const char* v = std::getenv("SGDB_HOGWILD_VARIANT")) p.variant = static_cast<uint32_t>(std::atoi(v));
     const size_t mirror_bytes = (ds.d + 1) * sizeof(float);
     int mode = a.model_mode;
     if (mode == 2 && mirror_bytes > 48 * 1024) mode = 1;  // mirror needs d+1 floats per CTA
     p.refresh = a.refresh;
     dispatch_lanes(G, [&]<int GL>() {
       dispatch_kind(kind, [&]<int KD>() {
-        prof_begin(c, "hogwild_kernel");
+        void (*kern)(HogParams);
+        size_t smem = 0;
         if (mode == 2) {
-          auto kern = a.task == kTaskLR ? hogwild_mirror_kernel<GL, kTaskLR, KD>
-                                        : hogwild_mirror_kernel<GL, kTaskSVM, KD>;
-          kern<<<grid, 256, mirror_bytes, c.stream>>>(p);
+          kern = a.task == kTaskLR ? hogwild_mirror_kernel<GL, kTaskLR, KD>
+                                   : hogwild_mirror_kernel<GL, kTaskSVM, KD>;
+          smem = mirror_bytes;
+        } else if (mode == 1 && ms > 1) {
+          kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomic>
+                                   : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomic>;
         } else if (mode == 1) {
-          if (a.task == kTaskLR) hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomic><<<grid, 256, 0, c.stream>>>(p);
-          else hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomic><<<grid, 256, 0, c.stream>>>(p);
+          kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomicFlat>
+                                   : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomicFlat>;
         } else {
-          if (a.task == kTaskLR) hogwild_kernel<GL, kTaskLR, KD, kScopeShared><<<grid, 256, 0, c.stream>>>(p);
-          else hogwild_kernel<GL, kTaskSVM, KD, kScopeShared><<<grid, 256, 0, c.stream>>>(p);
+          kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeShared>
+                                   : hogwild_kernel<GL, kTaskSVM, KD, kScopeShared>;
         }
+        const unsigned grid = wave_grid(c, kern, smem, a.workers, GL);
+        prof_begin(c, "hogwild_kernel");
+        kern<<<grid, 256, smem, c.stream>>>(p);
       });
     });
     launched(c, "hogwild_kernel");
@@ -587,12 +649,13 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
     prof_begin(c, "replicas_fill_kernel");
     replicas_fill_kernel<<<fill_grid, 256, 0, c.stream>>>(m.replicas.p, R, ld, ds.d, m.w32.p);
     launched(c, "replicas_fill_kernel");
-    const unsigned grid = grid_threads(a.workers);
     dispatch_lanes(G, [&]<int GL>() {
       dispatch_kind(kind, [&]<int KD>() {
+        auto kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeGlobalRep>
+                                      : hogwild_kernel<GL, kTaskSVM, KD, kScopeGlobalRep>;
+        const unsigned grid = wave_grid(c, kern, 0, a.workers, GL);
         prof_begin(c, "hogwild_kernel(replicas)");
-        if (a.task == kTaskLR) hogwild_kernel<GL, kTaskLR, KD, kScopeGlobalRep><<<grid, 256, 0, c.stream>>>(p);
-        else hogwild_kernel<GL, kTaskSVM, KD, kScopeGlobalRep><<<grid, 256, 0, c.stream>>>(p);
+        kern<<<grid, 256, 0, c.stream>>>(p);
       });
     });
     launched(c, "hogwild_kernel(replicas)");
@@ -650,8 +713,7 @@ void materialize(Model& m) {
   const unsigned dgrid = static_cast<unsigned>(
       std::max<uint64_t>(1, std::min<uint64_t>((m.d + 256) / 256, c.num_sms * 8ull)));
   prof_begin(c, "gather_kernel");
-  gather_kernel<<<dgrid, 256, 0, c.stream>>>(m.d, m.spread_ms, m.spread_shards, m.spread_ss,
-                                             m.spread.p, m.w32.p, m.w64.p);
+  gather_kernel<<<dgrid, 256, 0, c.stream>>>(m.d, m.spread_ms, m.spread.p, m.w32.p, m.w64.p);
   launched(c, "gather_kernel");
   m.dense_current = true;
 }
