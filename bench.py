@@ -290,6 +290,12 @@ def run_ours(args):
         "wall_s_timed_region": t_wall1 - t_wall0,
         "step_ms_median": float(np.median(step_ms)),
     }
+    if not args.no_extra:
+        extra = {}
+        extra["c5_sync_lr_dense1000"] = extra_c5(S, dev, world, rank, args.c5_rows, barrier)
+        if world == 1:
+            extra["sync_full_batch"] = extra_sync_shapes(S, dev)
+        out["extra"] = extra
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(host)
     if rank == 0 and not args.no_convergence:
@@ -300,6 +306,86 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def _time_epochs(S, dds, model, task, alpha, epochs, warmup, flush=None):
+    import torch
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        S.sync_epoch(dds, model, task, alpha, None, dds.n_global)
+    times = []
+    for _ in range(epochs):
+        if flush is not None:
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        S.sync_epoch(dds, model, task, alpha, None, dds.n_global)
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    return float(np.mean(times))
+
+
+def extra_c5(S, dev, world, rank, rows_per_gpu, barrier):
+    """BASELINE.json configs[4]: row-sharded synchronous LR on
+    dense 1,000-d data, rows_per_gpu rows per GPU generated on the device (K9),
+    full-batch epochs, fp64 gradient all-reduced over NCCL when N > 1."""
+    import torch
+    import torch.distributed as dist
+    d = 1000
+    n_global = rows_per_gpu * world
+    dds = S.DeviceDataset.generate_dense(dev, rows_per_gpu, d, 20250815, row_base=rank * rows_per_gpu,
+                                         n_global=n_global)
+    model = S.DeviceModel(dev, d)
+    barrier()
+    dev.set_profiling(True)
+    ms = _time_epochs(S, dds, model, S.Task.LR, 1e-9, 5, 2)
+    stats = dev.kernel_stats()
+    dev.set_profiling(False)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    k = stats.get("dense_full_kernel", (1, 0.0))
+    kern_ms = k[1] / max(1, k[0])
+    sweep = dds.sweep_bytes()
+    peak, _ = _peaks()
+    loss = S.device_loss(dds, model, S.Task.LR)
+    out = {"rows_per_gpu": rows_per_gpu, "n_global": n_global, "d": d, "batch": "N",
+           "epoch_ms": ms, "value": n_global / (ms / 1e3), "unit": UNIT,
+           "kernel": "dense_full_kernel", "kernel_ms": kern_ms,
+           "hbm_GBps": sweep / (kern_ms / 1e3) / 1e9 if kern_ms else None,
+           "frac": sweep / (kern_ms / 1e3) / 1e9 / peak if kern_ms else None,
+           "loss_after": loss, "scaling": "weak",
+           "note": "epoch = dense_full_kernel + NCCL all-reduce of g (d fp64) + apply when N > 1"}
+    del dds
+    torch.cuda.empty_cache()
+    return out
+
+
+def extra_sync_shapes(S, dev):
+    """Full-batch synchronous epochs on the other BASELINE shapes."""
+    import torch
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    shapes = {
+        "C1_covtype_lr": (lambda: S.fixtures.dense_classification(581012, 54, 20250810), S.Task.LR, 1e-6),
+        "C3_rcv1_lr": (lambda: S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813), S.Task.LR, 1e-6),
+        "C4a_news20_svm": (lambda: S.fixtures.sparse_classification(19996, 1355191, 455.0, 20250814), S.Task.SVM, 1e-5),
+        "C4b_realsim_svm": (lambda: S.fixtures.sparse_classification(72309, 20958, 51.3, 20250812), S.Task.SVM, 1e-5),
+    }
+    peak, _ = _peaks()
+    out = {}
+    for name, (make, task, alpha) in shapes.items():
+        host = make()
+        dds = S.DeviceDataset(dev, host)
+        model = S.DeviceModel(dev, host.n_features)
+        ms = _time_epochs(S, dds, model, task, alpha, 5, 2, flush)
+        sweep = dds.sweep_bytes()
+        out[name] = {"n": host.n_examples, "d": host.n_features, "epoch_ms": ms,
+                     "value": host.n_examples / (ms / 1e3), "unit": UNIT,
+                     "alg_GBps": sweep / (ms / 1e3) / 1e9, "frac": sweep / (ms / 1e3) / 1e9 / peak}
+        del dds, model, host
+    return out
 
 
 def cpu_baseline(host):
@@ -368,6 +454,9 @@ def main():
     ap.add_argument("--alpha", type=float, default=0.01)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-convergence", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--c5-rows", type=int, default=25_000_000,
+                    help="rows per GPU of the 200M x 1000 configuration (25M = 8 GPUs x 25M)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

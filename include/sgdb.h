@@ -208,6 +208,20 @@ sgdb_status sgdb_dataset_refresh_f32(sgdb_ctx* ctx, sgdb_dataset* ds, const floa
                                      const float* labels, const uint32_t* indices,
                                      const uint32_t* row_offsets32);
 sgdb_status sgdb_dataset_free(sgdb_dataset* ds);
+/* K9: generate a dense synthetic classification shard on the device (rows
+ * [row_base, row_base + n_local) of an n_global x d dataset) — the
+ * distribution of fixtures::dense_classification (fixtures.cpp:30-52) with a
+ * counter-based Philox-4x32-10 stream, so the 200M x 1000 configuration can
+ * be produced where it is trained and any slice re-created on the CPU
+ * (oracle/glm_oracle.cpp orc_philox_dense). 1 <= d <= 1024. */
+sgdb_status sgdb_dataset_generate_dense(sgdb_ctx* ctx, uint64_t n_local, uint64_t d,
+                                        uint64_t row_base, uint64_t n_global, uint64_t seed,
+                                        double label_noise, sgdb_dataset** out);
+/* Copy rows [row0, row0+nrows) of a dense device dataset back (fp32). */
+sgdb_status sgdb_dataset_read_dense(sgdb_ctx* ctx, const sgdb_dataset* ds, uint64_t row0,
+                                    uint64_t nrows, float* values_out, float* labels_out);
+/* The generator's hidden model w_true (Box-Muller over Philox; host). */
+sgdb_status sgdb_generate_hidden_model(uint64_t seed, uint64_t d, double* out);
 /* Algorithmic bytes of one sweep: CSR nnz*8 + (N+1)*4 + N*4;
  * dense N*d*4 + N*4. */
 sgdb_status sgdb_dataset_sweep_bytes(const sgdb_dataset* ds, uint64_t* out);

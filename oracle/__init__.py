@@ -174,6 +174,8 @@ class Oracle(_Lib):
         L.orc_hogwild_serial.argtypes = [_vp, _int, _dbl, _u64, _dbl, _int, _int, _u64, _u64,
                                          _u64, _int, _P(_dbl), _P(_dbl), _P(_dbl), _P(_u64)]
         L.orc_merge_models.argtypes = [_P(_dbl), _u64, _u64, _P(_dbl), _P(_dbl)]
+        L.orc_philox_hidden_model.argtypes = [_u64, _u64, _P(_dbl)]
+        L.orc_philox_dense.argtypes = [_u64, _u64, _u64, _u64, _dbl, _P(_dbl), _P(_dbl)]
 
     def round_f32(self, ds: HostData) -> HostData:
         out = HostData(**ds.__dict__)
@@ -238,6 +240,18 @@ class Oracle(_Lib):
             return models[:ran], losses[:ran], evals[:ran]
         finally:
             self.lib.orc_ds_free(h)
+
+    def philox_hidden_model(self, seed, d) -> np.ndarray:
+        w = np.zeros(d, np.float64)
+        self.lib.orc_philox_hidden_model(seed, d, _ptr(w, _dbl))
+        return w
+
+    def philox_dense(self, n, d, seed, row_base=0, noise=0.1) -> HostData:
+        """Rows [row_base, row_base+n) of the device generator's dataset (K9 restatement)."""
+        values = np.zeros(n * d, np.float64)
+        labels = np.zeros(n, np.float64)
+        self.lib.orc_philox_dense(n, d, row_base, seed, noise, _ptr(values, _dbl), _ptr(labels, _dbl))
+        return HostData(n, d, DENSE_ROW, labels, values)
 
     def merge_models(self, replicas: np.ndarray, weights=None) -> np.ndarray:
         reps = np.ascontiguousarray(replicas, np.float64)

@@ -623,3 +623,86 @@ int orc_parse_libsvm(const char* text, uint64_t len, int64_t declared_d, void** 
 }
 
 }  // extern "C"
+
+// --- K9 restatement: the Philox dense generator (paper_1802_08800_b200/csrc/
+// kernels_gen.cu, philox.hpp), written independently here. Distribution of
+// fixtures::dense_classification (src/fixtures.cpp:30-52); exact bit-level
+// definition: Philox-4x32-10, value = 2*(r>>8)*2^-24 - 1, hidden model by
+// Box-Muller, label = sign of the fp64 dot product accumulated lane-strided
+// over feature quads (lane l takes quads l, l+32, ...) and combined by an xor
+// butterfly (16, 8, 4, 2, 1), flipped when the Philox flip draw < noise. ----
+
+namespace {
+struct P4 {
+  uint32_t v[4];
+};
+P4 philox10(P4 c, uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    uint64_t p0 = static_cast<uint64_t>(0xD2511F53u) * c.v[0];
+    uint64_t p1 = static_cast<uint64_t>(0xCD9E8D57u) * c.v[2];
+    P4 n{{static_cast<uint32_t>(p1 >> 32) ^ c.v[1] ^ k0, static_cast<uint32_t>(p1),
+          static_cast<uint32_t>(p0 >> 32) ^ c.v[3] ^ k1, static_cast<uint32_t>(p0)}};
+    c = n;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+float unit_val(uint32_t r) { return static_cast<float>(r >> 8) * (1.0f / 16777216.0f) * 2.0f - 1.0f; }
+}  // namespace
+
+extern "C" {
+
+void orc_philox_hidden_model(uint64_t seed, uint64_t d, double* w) {
+  const uint32_t k0 = static_cast<uint32_t>(seed) ^ 0x9E3779B9u;
+  const uint32_t k1 = static_cast<uint32_t>(seed >> 32) ^ 0x7F4A7C15u;
+  for (uint64_t i = 0; 2 * i < d; ++i) {
+    P4 r = philox10(P4{{static_cast<uint32_t>(i), 0u, 0u, 0x5EED0003u}}, k0, k1);
+    uint64_t a = (static_cast<uint64_t>(r.v[0]) << 20) | (r.v[1] >> 12);
+    uint64_t b = (static_cast<uint64_t>(r.v[2]) << 20) | (r.v[3] >> 12);
+    double u1 = static_cast<double>(a + 1) * 0x1p-52, u2 = static_cast<double>(b) * 0x1p-52;
+    double rad = std::sqrt(-2.0 * std::log(u1)), th = 6.283185307179586 * u2;
+    w[2 * i] = rad * std::cos(th);
+    if (2 * i + 1 < d) w[2 * i + 1] = rad * std::sin(th);
+  }
+}
+
+// Rows [row_base, row_base + n) of the generated dataset: values (row-major,
+// n*d doubles holding the fp32 values) and labels.
+void orc_philox_dense(uint64_t n, uint64_t d, uint64_t row_base, uint64_t seed, double noise,
+                      double* values, double* labels) {
+  std::vector<double> w(d);
+  orc_philox_hidden_model(seed, d, w.data());
+  const uint64_t nq = (d + 3) / 4;
+  for (uint64_t r = 0; r < n; ++r) {
+    const uint64_t e = row_base + r;
+    double part[32] = {0.0};
+    for (uint64_t q = 0; q < nq; ++q) {
+      P4 u = philox10(P4{{static_cast<uint32_t>(e), static_cast<uint32_t>(e >> 32),
+                          static_cast<uint32_t>(q), 0x5EED0001u}},
+                      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+      for (int t = 0; t < 4; ++t) {
+        const uint64_t j = 4 * q + t;
+        if (j >= d) continue;
+        const float v = unit_val(u.v[t]);
+        values[r * d + j] = static_cast<double>(v);
+        part[q % 32] = part[q % 32] + static_cast<double>(v) * w[j];
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      double nx[32];
+      for (int l = 0; l < 32; ++l) nx[l] = part[l] + part[l ^ off];
+      for (int l = 0; l < 32; ++l) part[l] = nx[l];
+    }
+    double y = part[0] >= 0.0 ? 1.0 : -1.0;
+    if (noise > 0.0) {
+      P4 f = philox10(P4{{static_cast<uint32_t>(e), static_cast<uint32_t>(e >> 32), 0u, 0x5EED0002u}},
+                      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+      const float u = static_cast<float>(f.v[0] >> 8) * (1.0f / 16777216.0f);
+      if (static_cast<double>(u) < noise) y = -y;
+    }
+    labels[r] = y;
+  }
+}
+
+}  // extern "C"

@@ -79,6 +79,9 @@ PROTOTYPES = {
     "sgdb_dataset_upload": (_S, [vp, P(DatasetView), u64, u64, P(vp)]),
     "sgdb_dataset_refresh_f32": (_S, [vp, vp, vp, vp, vp, vp]),
     "sgdb_dataset_free": (_S, [vp]),
+    "sgdb_dataset_generate_dense": (_S, [vp, u64, u64, u64, u64, u64, dbl, P(vp)]),
+    "sgdb_generate_hidden_model": (_S, [u64, u64, P(dbl)]),
+    "sgdb_dataset_read_dense": (_S, [vp, vp, u64, u64, vp, vp]),
     "sgdb_dataset_sweep_bytes": (_S, [vp, P(u64)]),
     "sgdb_dataset_shape": (_S, [vp, P(u64), P(u64), P(u64), P(u64), P(u64)]),
     "sgdb_model_create": (_S, [vp, u64, P(dbl), P(vp)]),

@@ -424,23 +424,45 @@ class Device:
 class DeviceDataset:
     """Device-resident dataset (fp32 storage), optionally a row shard."""
 
-    def __init__(self, dev: Device, ds: Dataset, row_base: int = 0, n_global: int = 0):
+    def __init__(self, dev: Device, ds: Optional[Dataset], row_base: int = 0, n_global: int = 0,
+                 _handle=None):
         self.dev = dev
         self.host = ds
-        self._h = L.vp()
-        v = ds.view()
-        check(_lib().sgdb_dataset_upload(dev.handle, C.byref(v), row_base, n_global,
-                                         C.byref(self._h)))
+        if _handle is not None:
+            self._h = _handle
+        else:
+            self._h = L.vp()
+            v = ds.view()
+            check(_lib().sgdb_dataset_upload(dev.handle, C.byref(v), row_base, n_global,
+                                             C.byref(self._h)))
         n, d, nnz, rb, ng = (L.u64() for _ in range(5))
         check(_lib().sgdb_dataset_shape(self._h, C.byref(n), C.byref(d), C.byref(nnz),
                                         C.byref(rb), C.byref(ng)))
         self.n_local, self.n_features, self.nnz = int(n.value), int(d.value), int(nnz.value)
         self.row_base, self.n_global = int(rb.value), int(ng.value)
-        self.layout = ds.layout
+        self.layout = ds.layout if ds is not None else Layout.DenseRowMajor
+
+    @classmethod
+    def generate_dense(cls, dev: Device, n_local: int, d: int, seed: int, row_base: int = 0,
+                       n_global: int = 0, label_noise: float = 0.1) -> "DeviceDataset":
+        """K9: rows [row_base, row_base+n_local) of the Philox dense classification
+        dataset generated on the device (sgdb_dataset_generate_dense)."""
+        h = L.vp()
+        check(_lib().sgdb_dataset_generate_dense(dev.handle, n_local, d, row_base, n_global, seed,
+                                                 label_noise, C.byref(h)))
+        return cls(dev, None, _handle=h)
 
     @property
     def handle(self):
         return self._h
+
+    def read_dense(self, row0: int, nrows: int):
+        """(values[nrows, d] float32, labels[nrows] float32) of a dense device dataset."""
+        vals = np.zeros((nrows, self.n_features), np.float32)
+        labs = np.zeros(nrows, np.float32)
+        check(_lib().sgdb_dataset_read_dense(self.dev.handle, self._h, row0, nrows,
+                                             vals.ctypes.data, labs.ctypes.data))
+        return vals, labs
 
     def sweep_bytes(self) -> int:
         b = L.u64(0)
@@ -539,6 +561,13 @@ def models_average(dev: Device, models: Sequence[DeviceModel], out: DeviceModel,
     w = None if weights is None else np.ascontiguousarray(weights, np.float64)
     check(_lib().sgdb_models_average(dev.handle, arr, len(models), _dptr(w), out.handle,
                                      int(refresh)))
+
+
+def generate_hidden_model(seed: int, d: int) -> np.ndarray:
+    """w_true of the device generator (sgdb_generate_hidden_model)."""
+    out = np.zeros(d, np.float64)
+    check(_lib().sgdb_generate_hidden_model(seed, d, _dptr(out)))
+    return out
 
 
 _DEFAULT_DEVICE: Optional[Device] = None
