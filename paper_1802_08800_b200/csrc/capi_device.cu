@@ -40,24 +40,41 @@ void h2d(T* dst, const T* src, uint64_t count, cudaStream_t s) {
   if (count) check(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
 }
 
-// CSC of a CSR matrix by counting sort; rows stay ascending inside a column.
-void csc_from_csr(uint64_t n, uint64_t d, const std::vector<uint32_t>& rowptr,
-                  const std::vector<uint32_t>& idx, const std::vector<float>& val,
-                  std::vector<uint32_t>& colptr, std::vector<uint32_t>& crow,
-                  std::vector<float>& cval) {
+// Row-blocked CSC of a CSR matrix (counting sort per row block; rows stay
+// ascending inside a column). Block count: enough blocks to feed every SM,
+// few enough that the per-block column pointers stay small next to the data.
+void csc_blocked_from_csr(uint64_t n, uint64_t d, const std::vector<uint32_t>& rowptr,
+                          const std::vector<uint32_t>& idx, const std::vector<float>& val,
+                          uint32_t& rb, uint32_t& nblk, std::vector<uint32_t>& colptr,
+                          std::vector<uint16_t>& crow, std::vector<float>& cval) {
   const uint64_t nnz = idx.size();
-  colptr.assign(d + 1, 0);
-  for (uint64_t s = 0; s < nnz; ++s) ++colptr[idx[s] + 1];
-  for (uint64_t j = 0; j < d; ++j) colptr[j + 1] += colptr[j];
-  std::vector<uint32_t> next(colptr.begin(), colptr.end() - 1);
+  uint64_t want = std::clamp<uint64_t>((nnz * 2) / ((d + 1) * 4), 1, 16);
+  want = std::max<uint64_t>(want, (n + 49151) / 49152);  // slice <= 192 KB of SMEM
+  rb = static_cast<uint32_t>(std::max<uint64_t>(1, (n + want - 1) / want));
+  nblk = static_cast<uint32_t>(std::max<uint64_t>(1, (n + rb - 1) / rb));
+  colptr.assign(static_cast<uint64_t>(nblk) * (d + 1), 0);
   crow.resize(nnz);
   cval.resize(nnz);
-  for (uint64_t r = 0; r < n; ++r)
-    for (uint32_t s = rowptr[r]; s < rowptr[r + 1]; ++s) {
-      const uint32_t pos = next[idx[s]]++;
-      crow[pos] = static_cast<uint32_t>(r);
-      cval[pos] = val[s];
+  std::vector<uint32_t> next(d);
+  uint32_t pos = 0;
+  for (uint32_t bk = 0; bk < nblk; ++bk) {
+    const uint64_t r0 = static_cast<uint64_t>(bk) * rb, r1 = std::min<uint64_t>(n, r0 + rb);
+    uint32_t* cp = colptr.data() + static_cast<uint64_t>(bk) * (d + 1);
+    std::fill(next.begin(), next.end(), 0u);
+    for (uint32_t s = rowptr[r0]; s < rowptr[r1]; ++s) ++next[idx[s]];
+    cp[0] = pos;
+    for (uint64_t j = 0; j < d; ++j) {
+      cp[j + 1] = cp[j] + next[j];
+      next[j] = cp[j];
     }
+    for (uint64_t r = r0; r < r1; ++r)
+      for (uint32_t s = rowptr[r]; s < rowptr[r + 1]; ++s) {
+        const uint32_t q = next[idx[s]]++;
+        crow[q] = static_cast<uint16_t>(r - r0);
+        cval[q] = val[s];
+      }
+    pos = cp[d];
+  }
 }
 
 void upload_csr(sgdb_dataset* ds, std::vector<uint32_t>& rowptr, std::vector<uint32_t>& idx,
@@ -71,15 +88,16 @@ void upload_csr(sgdb_dataset* ds, std::vector<uint32_t>& rowptr, std::vector<uin
   h2d(ds->val.p, val.data(), ds->nnz, s);
   h2d(ds->idx.p, idx.data(), ds->nnz, s);
   h2d(ds->rowptr.p, rowptr.data(), ds->n + 1, s);
-  std::vector<uint32_t> colptr, crow;
+  std::vector<uint32_t> colptr;
+  std::vector<uint16_t> crow;
   std::vector<float> cval;
-  csc_from_csr(ds->n, ds->d, rowptr, idx, val, colptr, crow, cval);
+  csc_blocked_from_csr(ds->n, ds->d, rowptr, idx, val, ds->csc_rb, ds->csc_nblk, colptr, crow, cval);
   ds->cval.alloc(std::max<uint64_t>(1, ds->nnz));
   ds->crow.alloc(std::max<uint64_t>(1, ds->nnz));
-  ds->colptr.alloc(ds->d + 1);
+  ds->colptr.alloc(colptr.size());
   h2d(ds->cval.p, cval.data(), ds->nnz, s);
   h2d(ds->crow.p, crow.data(), ds->nnz, s);
-  h2d(ds->colptr.p, colptr.data(), ds->d + 1, s);
+  h2d(ds->colptr.p, colptr.data(), colptr.size(), s);
   ds->csc_built = true;
   ds->coef.alloc(std::max<uint64_t>(1, ds->n));
   check(cudaStreamSynchronize(s), "upload sync");  // host vectors die with the caller
@@ -91,18 +109,20 @@ uint64_t nonempty_workers(uint64_t n, uint64_t T, bool rr) {
   return (n + chunk - 1) / chunk;
 }
 
+// The finite flag is any nonzero value while every gradient entry was
+// finite; kernels write 0. Reset with a device memset (no host staging) and
+// read back through pinned memory.
 void set_finite(sgdb_model* m) {
-  static const int one = 1;
-  check(cudaMemcpyAsync(m->finite.p, &one, sizeof(int), cudaMemcpyHostToDevice, m->ctx->stream),
-        "set finite");
+  check(cudaMemsetAsync(m->finite.p, 0x01, sizeof(int), m->ctx->stream), "set finite");
 }
 
 int read_finite(sgdb_model* m) {
-  int f = 0;
-  check(cudaMemcpyAsync(&f, m->finite.p, sizeof(int), cudaMemcpyDeviceToHost, m->ctx->stream),
+  Ctx& c = *m->ctx;
+  if (!c.pinned_flag) check(cudaMallocHost(&c.pinned_flag, sizeof(int)), "cudaMallocHost");
+  check(cudaMemcpyAsync(c.pinned_flag, m->finite.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream),
         "read finite");
-  check(cudaStreamSynchronize(m->ctx->stream), "sync");
-  return f;
+  check(cudaStreamSynchronize(c.stream), "sync");
+  return *c.pinned_flag != 0 ? 1 : 0;
 }
 
 void call_allreduce(Ctx& c, void* ptr, uint64_t count, int dtype) {
@@ -187,6 +207,7 @@ sgdb_status sgdb_ctx_destroy(sgdb_ctx* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->pinned_flag) cudaFreeHost(ctx->pinned_flag);
     delete ctx;
   });
 }

@@ -60,6 +60,7 @@ struct Ctx {
   DBuf<double> loss_partials;  // per-block loss sums
   DBuf<double> loss_out;       // [0] loss, [1] scratch
   DBuf<unsigned> tickets;      // [0] loss ticket
+  int* pinned_flag = nullptr;  // pinned host word for flag read-back
   // Optional per-launch CUDA-event timing (sgdb_ctx_set_profiling).
   bool profiling = false;
   struct LaunchRec {
@@ -102,10 +103,14 @@ struct Dataset {
   DBuf<float> val;
   DBuf<uint32_t> idx;
   DBuf<uint32_t> rowptr;
-  // CSC of the local rows (built lazily for full-batch sparse gradients).
+  // Row-blocked CSC of the local rows (full-batch sparse gradients): rows are
+  // split into csc_nblk blocks of csc_rb (< 2^16) rows; block b holds its
+  // columns back to back, colptr[b*(d+1) + j] are global offsets, row ids
+  // are 16-bit block-local.
   bool csc_built = false;
+  uint32_t csc_rb = 0, csc_nblk = 0;
   DBuf<float> cval;
-  DBuf<uint32_t> crow;
+  DBuf<uint16_t> crow;
   DBuf<uint32_t> colptr;
   // Column-major copies for the col-* access paths (built lazily).
   bool col_built = false;

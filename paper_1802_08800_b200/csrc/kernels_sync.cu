@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "device.hpp"
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(32 * W) dense_batch_kernel(DenseBatchParams p)
 
 // Lane-strided sparse dot x_row . w over slots [b, e): U slots per batch so
 // U index loads and then U independent model gathers are in flight at once.
-template <int G>
+template <int G, bool SMEM = false>
 __device__ __forceinline__ float gather_dot(const float* __restrict__ val,
                                             const uint32_t* __restrict__ idx, uint32_t b,
                                             uint32_t e, int lg, const float* __restrict__ w) {
@@ -315,7 +316,7 @@ __device__ __forceinline__ float gather_dot(const float* __restrict__ val,
       xv[u] = s < e ? __ldg(val + s) : 0.f;
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) wv[u] = s0 + u * G < e ? __ldg(w + jv[u]) : 0.f;
+    for (int u = 0; u < U; ++u) wv[u] = s0 + u * G < e ? (SMEM ? w[jv[u]] : __ldg(w + jv[u])) : 0.f;
 #pragma unroll
     for (int u = 0; u < U; ++u) z = fmaf(xv[u], wv[u], z);
   }
@@ -347,62 +348,207 @@ __global__ void __launch_bounds__(256) csr_coef_kernel(const float* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// K3: g_j = sum over column j of the CSC copy of c[row] * x_ij (fp64
-// accumulation), fused with w_j -= alpha*g_j (one writer per coordinate, so
-// the result is deterministic) and the finite flag.
+// K2p: K2 with a 2-stage software pipeline across the rows a warp walks:
+// while row i reduces, the extent (and label) of row i+2 and the first slot
+// batch of row i+1 are in flight, so a warp is never idle on a dependent
+// rowptr -> idx -> gather chain. SMEM = stage the fp32 model in shared memory
+// (d <= 48K floats) and gather from it.
 // ---------------------------------------------------------------------------
+struct SegBatch {
+  uint32_t j[4];
+  float x[4];
+};
+
 template <int G>
-__global__ void __launch_bounds__(256) csc_grad_kernel(const float* __restrict__ cval,
-                                                       const uint32_t* __restrict__ crow,
-                                                       const uint32_t* __restrict__ colptr,
-                                                       uint64_t d, const float* __restrict__ coef,
-                                                       double alpha, int apply, int want_norm,
-                                                       double* w64, float* w32, double* g64,
-                                                       int* finite, double* norm2) {
-  constexpr int CW = 32 / G;
+__device__ __forceinline__ SegBatch seg_batch(const float* __restrict__ val,
+                                              const uint32_t* __restrict__ idx, uint32_t s0,
+                                              uint32_t e) {
+  SegBatch bt;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t s = s0 + u * G;
+    bt.j[u] = s < e ? __ldg(idx + s) : 0u;
+    bt.x[u] = s < e ? __ldg(val + s) : 0.f;
+  }
+  return bt;
+}
+
+template <int G, bool SMEM>
+__device__ __forceinline__ float seg_dot(const float* __restrict__ val,
+                                         const uint32_t* __restrict__ idx, uint32_t b, uint32_t e,
+                                         int lg, const SegBatch& first, const float* __restrict__ w) {
+  float z = 0.f;
+  {
+    float wv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) wv[u] = b + lg + u * G < e ? (SMEM ? w[first.j[u]] : __ldg(w + first.j[u])) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) z = fmaf(first.x[u], wv[u], z);
+  }
+  for (uint32_t s0 = b + lg + G * 4; s0 < e; s0 += G * 4) {
+    const SegBatch bt = seg_batch<G>(val, idx, s0, e);
+    float wv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) wv[u] = s0 + u * G < e ? (SMEM ? w[bt.j[u]] : __ldg(w + bt.j[u])) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) z = fmaf(bt.x[u], wv[u], z);
+  }
+  return z;
+}
+
+template <int G, int TASK, bool SMEM>
+__global__ void __launch_bounds__(SMEM ? 1024 : 256) csr_coef_pipe_kernel(
+    const float* __restrict__ val, const uint32_t* __restrict__ idx,
+    const uint32_t* __restrict__ rowptr, const float* __restrict__ y, uint64_t n,
+    const float* __restrict__ w32, uint32_t d, float* __restrict__ coef) {
+  extern __shared__ float ws[];
+  const float* w = w32;
+  if (SMEM) {
+    for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) ws[j] = w32[j];
+    __syncthreads();
+    w = ws;
+  }
+  constexpr int RW = 32 / G;
   const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  double nrm = 0.0;
-  int bad = 0;
-  for (uint64_t base = gw * CW; base < d; base += tw * CW) {
-    const uint64_t j = base + grp;
+  const uint64_t step = (((uint64_t)gridDim.x * blockDim.x) >> 5) * RW;
+  uint64_t base = gw * RW;
+  auto extent = [&](uint64_t bs, uint32_t& b, uint32_t& e, float& yy) {
+    const uint64_t r = bs + grp;
+    if (r < n) {
+      b = rowptr[r];
+      e = rowptr[r + 1];
+      yy = y[r];
+    } else {
+      b = e = 0u;
+      yy = 0.f;
+    }
+  };
+  uint32_t cb, ce, nb, ne;
+  float cy, ny;
+  extent(base, cb, ce, cy);
+  extent(base + step, nb, ne, ny);
+  SegBatch cur = seg_batch<G>(val, idx, cb + lg, ce);
+  for (; base < n; base += step) {
+    const SegBatch nxt = seg_batch<G>(val, idx, nb + lg, ne);
+    uint32_t ab, ae;
+    float ay;
+    extent(base + 2 * step, ab, ae, ay);
+    float z = seg_dot<G, SMEM>(val, idx, cb, ce, lg, cur, w);
+    z = group_sum<G>(z);
+    const uint64_t row = base + grp;
+    if (row < n && lg == 0) coef[row] = coef_f<TASK>(z, cy);
+    cur = nxt;
+    cb = nb, ce = ne, cy = ny;
+    nb = ab, ne = ae, ny = ay;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: g = X^T c over the row-blocked CSC. CTA (block b, column range k)
+// stages c[rows of b] in SMEM, then G lanes per column reduce
+// cval * c_smem[crow] in fp64 into partials[b][j]; K3f sums the partials over
+// b in fixed order, so the gradient is deterministic.
+// ---------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(1024) csc_block_kernel(
+    const float* __restrict__ cval, const uint16_t* __restrict__ crow,
+    const uint32_t* __restrict__ colptr, const float* __restrict__ coef, uint64_t n, uint32_t d,
+    uint32_t rb, uint32_t nblk, uint32_t cpb, double* __restrict__ partials) {
+  extern __shared__ float cs[];
+  const uint32_t b = blockIdx.x / cpb, k = blockIdx.x % cpb;
+  if (b >= nblk) return;
+  const uint64_t r0 = static_cast<uint64_t>(b) * rb;
+  const uint32_t rows = static_cast<uint32_t>(min(static_cast<uint64_t>(rb), n - r0));
+  for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) cs[i] = coef[r0 + i];
+  __syncthreads();
+  const uint32_t j0 = static_cast<uint32_t>(static_cast<uint64_t>(d) * k / cpb);
+  const uint32_t j1 = static_cast<uint32_t>(static_cast<uint64_t>(d) * (k + 1) / cpb);
+  const uint32_t* cp = colptr + static_cast<uint64_t>(b) * (d + 1);
+  constexpr int CW = 32 / G;
+  constexpr int U = 4;
+  const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
+  const uint32_t warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // 2-stage pipeline over the columns this warp walks (as in K2p).
+  const uint32_t step = nw * CW;
+  uint32_t base = j0 + warp * CW;
+  auto extent = [&](uint32_t bs, uint32_t& sb, uint32_t& se) {
+    const uint32_t j = bs + grp;
+    if (j < j1) {
+      sb = cp[j];
+      se = cp[j + 1];
+    } else {
+      sb = se = 0u;
+    }
+  };
+  auto batch = [&](uint32_t s0, uint32_t se, float* xv, uint32_t* rv) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t s = s0 + u * G;
+      xv[u] = s < se ? __ldg(cval + s) : 0.f;
+      rv[u] = s < se ? __ldg(crow + s) : 0u;
+    }
+  };
+  uint32_t cb, ce, nb, ne;
+  extent(base, cb, ce);
+  extent(base + step, nb, ne);
+  float cx[U];
+  uint32_t cr[U];
+  batch(cb + lg, ce, cx, cr);
+  for (; base < j1; base += step) {
+    float nx[U];
+    uint32_t nr[U];
+    batch(nb + lg, ne, nx, nr);
+    uint32_t ab, ae;
+    extent(base + 2 * step, ab, ae);
     double acc = 0.0;
-    if (j < d) {
-      const uint32_t b = colptr[j], e = colptr[j + 1];
-      constexpr int U = 4;
-      for (uint32_t s0 = b + lg; s0 < e; s0 += G * U) {
-        uint32_t rv[U];
-        float xv[U], cv[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t s = s0 + u * G;
-          rv[u] = s < e ? __ldg(crow + s) : 0u;
-          xv[u] = s < e ? __ldg(cval + s) : 0.f;
-        }
+    for (int u = 0; u < U; ++u) acc += static_cast<double>(cx[u] * cs[cr[u]]);
+    for (uint32_t s0 = cb + lg + G * U; s0 < ce; s0 += G * U) {
+      float xv[U];
+      uint32_t rv[U];
+      batch(s0, ce, xv, rv);
 #pragma unroll
-        for (int u = 0; u < U; ++u) cv[u] = s0 + u * G < e ? __ldg(coef + rv[u]) : 0.f;
-#pragma unroll
-        for (int u = 0; u < U; ++u) acc += static_cast<double>(xv[u] * cv[u]);
-      }
+      for (int u = 0; u < U; ++u) acc += static_cast<double>(xv[u] * cs[rv[u]]);
     }
     acc = group_sum<G>(acc);
-    if (j < d && lg == 0) {
-      if (!isfinite(acc)) bad = 1;
-      if (apply) {
-        const double w = w64[j] - alpha * acc;
-        w64[j] = w;
-        w32[j] = static_cast<float>(w);
-      } else {
-        g64[j] = acc;
-      }
-      nrm += acc * acc;
+    const uint32_t j = base + grp;
+    if (j < j1 && lg == 0) partials[static_cast<uint64_t>(b) * d + j] = acc;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      cx[u] = nx[u];
+      cr[u] = nr[u];
     }
+    cb = nb, ce = ne;
+    nb = ab, ne = ae;
+  }
+}
+
+// K3f: g_j = sum_b partials[b][j] (fixed order), fused w -= alpha*g_j (one
+// writer per coordinate), finite flag, ||g||^2.
+__global__ void apply_partials_kernel(uint64_t d, uint32_t nblk, const double* __restrict__ partials,
+                                      double alpha, int apply, int want_norm, double* w64,
+                                      float* w32, double* g64, int* finite, double* norm2) {
+  double nrm = 0.0;
+  int bad = 0;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    double g = 0.0;
+    for (uint32_t b = 0; b < nblk; ++b) g += partials[static_cast<uint64_t>(b) * d + j];
+    if (!isfinite(g)) bad = 1;
+    if (apply) {
+      const double w = w64[j] - alpha * g;
+      w64[j] = w;
+      w32[j] = static_cast<float>(w);
+    } else {
+      g64[j] = g;
+    }
+    nrm += g * g;
   }
   if (bad) *finite = 0;
   if (want_norm) {
     nrm = warp_sum_d(nrm);
-    if (lane == 0 && nrm != 0.0) atomicAdd(norm2, nrm);
+    if ((threadIdx.x & 31) == 0 && nrm != 0.0) atomicAdd(norm2, nrm);
   }
 }
 
@@ -577,6 +723,11 @@ int lanes_for(double avg) {
   return 32;
 }
 
+int env_lanes(const char* name, int fallback) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : fallback;
+}
+
 unsigned grid_for(const Ctx& c, uint64_t items_per_block_unit, uint64_t units, unsigned per_sm) {
   uint64_t want = (units + items_per_block_unit - 1) / items_per_block_unit;
   uint64_t cap = static_cast<uint64_t>(c.num_sms) * per_sm;
@@ -683,16 +834,54 @@ void launch_csr_coef_G(Dataset& ds, Model& m) {
   launched(c, "csr_coef_kernel");
 }
 
-template <int G>
-void launch_csc_grad_G(Dataset& ds, Model& m, const StepArgs& a) {
+template <int G, int TASK, bool SMEM>
+void launch_csr_coef_pipe_G(Dataset& ds, Model& m) {
   Ctx& c = *ds.ctx;
-  const unsigned grid = grid_for(c, 8ull * (32 / G) * 4, ds.d, 8);
+  const size_t smem = SMEM ? ds.d * sizeof(float) : 0;
+  const int threads = SMEM ? 1024 : 256;
+  auto kern = csr_coef_pipe_kernel<G, TASK, SMEM>;
+  if (smem > 48 * 1024)
+    check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+          "cudaFuncSetAttribute(csr_coef_pipe)");
+  int per_sm = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem), "occupancy");
+  const uint64_t want = (ds.n * G + threads - 1) / threads;
+  const unsigned grid = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(std::max(1, per_sm)) * c.num_sms)));
+  prof_begin(c, "csr_coef_kernel");
+  kern<<<grid, threads, smem, c.stream>>>(ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p, ds.n, m.w32.p,
+                                          static_cast<uint32_t>(ds.d), ds.coef.p);
+  launched(c, "csr_coef_kernel");
+}
+
+template <int G>
+void launch_csc_block_G(Dataset& ds, Model& m) {
+  Ctx& c = *ds.ctx;
+  const size_t smem = static_cast<size_t>(ds.csc_rb) * sizeof(float);
+  auto kern = csc_block_kernel<G>;
+  if (smem > 48 * 1024)
+    check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+          "cudaFuncSetAttribute(csc_block)");
+  int per_sm = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, smem), "occupancy");
+  const uint32_t slots = static_cast<uint32_t>(std::max(1, per_sm) * c.num_sms);
+  const uint32_t cpb = std::max<uint32_t>(1, slots / ds.csc_nblk);
+  m.partials.alloc(static_cast<uint64_t>(ds.csc_nblk) * ds.d);
   prof_begin(c, "csc_grad_kernel");
-  csc_grad_kernel<G><<<grid, 256, 0, c.stream>>>(ds.cval.p, ds.crow.p, ds.colptr.p, ds.d,
-                                                 ds.coef.p, a.alpha, a.apply ? 1 : 0,
-                                                 a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p,
-                                                 m.finite.p, m.scal.p);
+  kern<<<cpb * ds.csc_nblk, 1024, smem, c.stream>>>(ds.cval.p, ds.crow.p, ds.colptr.p, ds.coef.p, ds.n,
+                                                    static_cast<uint32_t>(ds.d), ds.csc_rb,
+                                                    ds.csc_nblk, cpb, m.partials.p);
   launched(c, "csc_grad_kernel");
+}
+
+void launch_apply_partials(Dataset& ds, Model& m, const StepArgs& a) {
+  Ctx& c = *ds.ctx;
+  const unsigned grid = grid_for(c, 256ull * 4, ds.d, 8);
+  prof_begin(c, "apply_partials_kernel");
+  apply_partials_kernel<<<grid, 256, 0, c.stream>>>(ds.d, ds.csc_nblk, m.partials.p, a.alpha,
+                                                    a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p,
+                                                    m.w32.p, m.g64.p, m.finite.p, m.scal.p);
+  launched(c, "apply_partials_kernel");
 }
 
 template <int G, int TASK>
@@ -749,14 +938,31 @@ void dense_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb,
 void csr_full_step(Dataset& ds, Model& m, const StepArgs& a) {
   build_csc(ds);
   if (ds.n > 0) {
-    const int g = lanes_for(static_cast<double>(ds.nnz) / static_cast<double>(ds.n));
+    const int g = env_lanes("SGDB_ROW_LANES", lanes_for(static_cast<double>(ds.nnz) / static_cast<double>(ds.n)));
+    // SMEM staging of the model: opt-in (SGDB_COEF_SMEM=1); measured slower on
+    // rcv1 because one 189 KB CTA per SM halves the resident warps.
+    static const bool smem_pref = [] {
+      const char* e = std::getenv("SGDB_COEF_SMEM");
+      return e && std::atoi(e) != 0;
+    }();
+    const bool smem_model = smem_pref && ds.d * sizeof(float) <= 192 * 1024;
     dispatch_G(g, [&]<int G>() {
-      if (a.task == kTaskLR) launch_csr_coef_G<G, kTaskLR>(ds, m);
-      else launch_csr_coef_G<G, kTaskSVM>(ds, m);
+      if (smem_model) {
+        if (a.task == kTaskLR) launch_csr_coef_pipe_G<G, kTaskLR, true>(ds, m);
+        else launch_csr_coef_pipe_G<G, kTaskSVM, true>(ds, m);
+      } else {
+        if (a.task == kTaskLR) launch_csr_coef_pipe_G<G, kTaskLR, false>(ds, m);
+        else launch_csr_coef_pipe_G<G, kTaskSVM, false>(ds, m);
+      }
     });
   }
-  const int gc = lanes_for(static_cast<double>(ds.nnz) / static_cast<double>(std::max<uint64_t>(1, ds.d)));
-  dispatch_G(gc, [&]<int G>() { launch_csc_grad_G<G>(ds, m, a); });
+  const double per_col = static_cast<double>(ds.nnz) /
+                         static_cast<double>(std::max<uint64_t>(1, ds.d) * std::max(1u, ds.csc_nblk));
+  // Column segments: narrow groups amortise the per-column reduction over
+  // more columns per warp (measured: rcv1 8 lanes, news20/real-sim 4).
+  const int gc = per_col <= 16.0 ? 4 : (per_col <= 128.0 ? 8 : 16);
+  dispatch_G(env_lanes("SGDB_COL_LANES", gc), [&]<int G>() { launch_csc_block_G<G>(ds, m); });
+  launch_apply_partials(ds, m, a);
 }
 
 void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, const StepArgs& a) {
