@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -195,6 +196,7 @@ sgdb_status sgdb_ctx_create(int32_t device, void* cuda_stream, sgdb_ctx** out) {
       check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
       c->own_stream = true;
     }
+    check(cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->loss_out.alloc(2);
     c->tickets.alloc(4);
     c->tickets.zero(c->stream);
@@ -208,6 +210,7 @@ sgdb_status sgdb_ctx_destroy(sgdb_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->pinned_flag) cudaFreeHost(ctx->pinned_flag);
+    if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
     delete ctx;
   });
 }
@@ -304,6 +307,7 @@ sgdb_status sgdb_dataset_upload(sgdb_ctx* ctx, const sgdb_dataset_view* v, uint6
     auto* ds = new sgdb_dataset();
     std::unique_ptr<sgdb_dataset> guard(ds);
     ds->ctx = ctx;
+    ds->uid = next_dataset_uid();
     ds->n = n;
     ds->d = d;
     ds->row_base = row_base;
@@ -519,15 +523,64 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
         h2d(ds->order.p, iota.data(), ng, c.stream);
         check(cudaStreamSynchronize(c.stream), "order sync");
       }
-      for (uint64_t lo = 0; lo < ng; lo += batch_b) {
-        const uint64_t nb = std::min(batch_b, ng - lo);
-        const uint32_t* ids = ds->order.p + lo;
-        if (ds->kind == Kind::Dense) dense_batch_step(*ds, *m, ids, nb, a);
-        else csr_batch_step(*ds, *m, ids, nb, a);
-        if (hook) {
-          call_allreduce(c, m->g64.p, m->d, 1);
-          apply_update(*m, alpha, false);
+      auto run_steps = [&](const StepArgs& sa) {
+        for (uint64_t lo = 0; lo < ng; lo += batch_b) {
+          const uint64_t nb = std::min(batch_b, ng - lo);
+          const uint32_t* ids = ds->order.p + lo;
+          if (ds->kind == Kind::Dense) dense_batch_step(*ds, *m, ids, nb, sa);
+          else csr_batch_step(*ds, *m, ids, nb, sa);
+          if (hook) {
+            call_allreduce(c, m->g64.p, m->d, 1);
+            apply_update(*m, alpha, false);
+          }
         }
+      };
+      if (hook || ng / batch_b < 4) {
+        run_steps(a);
+      } else {
+        // Launch-bound many-step epoch: replay a captured CUDA graph of the
+        // whole step sequence (captured once per dataset / batch size / task;
+        // the step size is read from device memory).
+        if (!(m->epoch_graph && m->graph_ds == ds->uid && m->graph_b == batch_b &&
+              m->graph_task == task)) {
+          if (m->epoch_graph) cudaGraphExecDestroy(m->epoch_graph);
+          m->epoch_graph = nullptr;
+          m->alpha_dev.alloc(1);
+          StepArgs ga = a;
+          ga.alpha_dev = m->alpha_dev.p;
+          const cudaStream_t saved = c.stream;
+          const bool prof = c.profiling;
+          const uint64_t l0 = c.launches;
+          c.stream = c.capture_stream;
+          c.profiling = false;
+          cudaGraph_t graph = nullptr;
+          check(cudaStreamBeginCapture(c.capture_stream, cudaStreamCaptureModeThreadLocal),
+                "cudaStreamBeginCapture");
+          try {
+            run_steps(ga);
+          } catch (...) {
+            cudaStreamEndCapture(c.capture_stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            c.stream = saved;
+            c.profiling = prof;
+            throw;
+          }
+          check(cudaStreamEndCapture(c.capture_stream, &graph), "cudaStreamEndCapture");
+          c.stream = saved;
+          c.profiling = prof;
+          m->graph_nodes = c.launches - l0;
+          c.launches = l0;
+          check(cudaGraphInstantiate(&m->epoch_graph, graph, 0), "cudaGraphInstantiate");
+          cudaGraphDestroy(graph);
+          m->graph_ds = ds->uid;
+          m->graph_b = batch_b;
+          m->graph_task = task;
+        }
+        h2d(m->alpha_dev.p, &alpha, 1, c.stream);  // pageable source: staged before return
+        prof_begin(c, "sync_epoch_graph");
+        check(cudaGraphLaunch(m->epoch_graph, c.stream), "cudaGraphLaunch");
+        launched(c, "sync_epoch_graph");
+        c.launches += m->graph_nodes - 1;
       }
     }
     // finite_out == NULL: fully asynchronous on the context stream.
@@ -661,6 +714,11 @@ sgdb_status sgdb_loss(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t ta
 }  // extern "C"
 
 namespace sgdb::dev {
+uint64_t next_dataset_uid() {
+  static std::atomic<uint64_t> counter{1};
+  return counter.fetch_add(1);
+}
+
 void build_csc(Dataset& ds) {
   if (!ds.csc_built) throw Unsupported("CSC copy missing (dataset was not uploaded as CSR)");
 }

@@ -61,6 +61,7 @@ struct Ctx {
   DBuf<double> loss_out;       // [0] loss, [1] scratch
   DBuf<unsigned> tickets;      // [0] loss ticket
   int* pinned_flag = nullptr;  // pinned host word for flag read-back
+  cudaStream_t capture_stream = nullptr;  // private stream for CUDA-graph capture
   // Optional per-launch CUDA-event timing (sgdb_ctx_set_profiling).
   bool profiling = false;
   struct LaunchRec {
@@ -90,6 +91,7 @@ enum class Kind { Dense, Csr };
 
 struct Dataset {
   Ctx* ctx = nullptr;
+  uint64_t uid = 0;  // unique per upload (keys cached epoch graphs)
   uint64_t n = 0;  // local rows
   uint64_t d = 0;
   uint64_t row_base = 0, n_global = 0;
@@ -146,6 +148,18 @@ struct Model {
   bool spread_current = false;
   uint32_t spread_ms = 1;
   uint64_t n_replicas = 0, replica_ld = 0;
+  // Captured mini-batch epoch (one kernel sequence per step), replayed each
+  // epoch; key = (dataset uid, batch size, task).
+  cudaGraphExec_t epoch_graph = nullptr;
+  uint64_t graph_ds = 0, graph_b = 0, graph_nodes = 0;
+  int graph_task = -1;
+  DBuf<double> alpha_dev;
+  Model() = default;
+  Model(const Model&) = delete;
+  Model& operator=(const Model&) = delete;
+  ~Model() {
+    if (epoch_graph) cudaGraphExecDestroy(epoch_graph);
+  }
 };
 
 // ---- launchers (kernels_*.cu) -------------------------------------------------
@@ -153,6 +167,7 @@ struct Model {
 struct StepArgs {
   int task = 0;
   double alpha = 0.0;
+  const double* alpha_dev = nullptr;  // device step size (graph-captured epochs)
   bool apply = true;      // fuse w -= alpha*g (else g64 holds the gradient)
   bool want_norm = false; // accumulate ||g||^2 into model.scal[0]
 };
@@ -166,8 +181,8 @@ void dense_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb,
 void csr_full_step(Dataset& ds, Model& m, const StepArgs& a);
 // Sparse mini-batch: scatter with fp64 atomics, then apply.
 void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, const StepArgs& a);
-// w -= alpha*g64; w32 = w64; finite; g64 = 0.
-void apply_update(Model& m, double alpha, bool want_norm);
+// w -= alpha*g64; w32 = w64; finite; g64 = 0. alpha_dev (if set) overrides alpha.
+void apply_update(Model& m, double alpha, bool want_norm, const double* alpha_dev = nullptr);
 // fp64 loss over all local rows; result left in ctx.loss_out[0] (device).
 void loss_launch(Dataset& ds, Model& m, int task);
 // w64 = (double) w32[0..d)
@@ -203,6 +218,7 @@ inline void dense_written(Model& m) {
 // w64 *= scale; w32 = w64 (rank averaging after a SUM all-reduce).
 void scale_model(Model& m, double scale);
 
+uint64_t next_dataset_uid();
 void build_csc(Dataset& ds);
 void build_col(Dataset& ds);
 

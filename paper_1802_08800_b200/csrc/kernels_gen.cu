@@ -124,6 +124,7 @@ sgdb_status sgdb_dataset_generate_dense(sgdb_ctx* ctx, uint64_t n_local, uint64_
     auto* ds = new sgdb_dataset();
     std::unique_ptr<sgdb_dataset> guard(ds);
     ds->ctx = ctx;
+    ds->uid = next_dataset_uid();
     ds->n = n_local;
     ds->d = d;
     ds->row_base = row_base;

@@ -52,7 +52,6 @@ struct HogParams {
   float alpha;
   uint32_t refresh;  // mirror kernel: refresh reads from L2 every `refresh` examples
   uint32_t ms;       // kernel scope: float stride between model coordinates in global
-  uint32_t variant;  // diagnostic knob (SGDB_HOGWILD_VARIANT)
 };
 
 template <int G>
@@ -87,15 +86,9 @@ struct GlobalModel {  // plain load / store: lost updates allowed (Hogwild)
 template <uint32_t MS>
 struct GlobalAtomicModel {
   float* m;
-  uint32_t variant;  // diagnostic: 1 = non-coherent reads, 2 = no updates
   __device__ GlobalAtomicModel at(uint64_t) const { return *this; }
-  __device__ float load(uint32_t j) const {
-    if (variant == 1) return __ldg(m + uint64_t(j) * MS);
-    return ld_model(m + uint64_t(j) * MS);
-  }
-  __device__ void add(uint32_t j, float delta) const {
-    if (variant != 2) atomicAdd(m + uint64_t(j) * MS, delta);
-  }
+  __device__ float load(uint32_t j) const { return ld_model(m + uint64_t(j) * MS); }
+  __device__ void add(uint32_t j, float delta) const { atomicAdd(m + uint64_t(j) * MS, delta); }
 };
 struct SmemModel {  // block-scope replica in shared memory, plain RMW
   volatile float* m;
@@ -307,9 +300,9 @@ __global__ void __launch_bounds__(256) hogwild_kernel(HogParams p) {
   const uint64_t HG = ((uint64_t)gridDim.x * blockDim.x) / G;
   for (uint64_t w = hg; w < p.T; w += HG) {
     if (SCOPE == kScopeSharedAtomic) {
-      run_worker<G, TASK, KIND>(p, GlobalAtomicModel<kSpread>{p.model, p.variant}, w, lg, mask);
+      run_worker<G, TASK, KIND>(p, GlobalAtomicModel<kSpread>{p.model}, w, lg, mask);
     } else if (SCOPE == kScopeSharedAtomicFlat) {
-      run_worker<G, TASK, KIND>(p, GlobalAtomicModel<1>{p.model, p.variant}, w, lg, mask);
+      run_worker<G, TASK, KIND>(p, GlobalAtomicModel<1>{p.model}, w, lg, mask);
     } else {
       run_worker<G, TASK, KIND>(
           p,
@@ -568,7 +561,6 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
       p.model = m.w32.p;
     }
     p.ms = ms;
-    if (const char* v = std::getenv("SGDB_HOGWILD_VARIANT")) p.variant = static_cast<uint32_t>(std::atoi(v));
     const size_t mirror_bytes = (ds.d + 1) * sizeof(float);
     int mode = a.model_mode;
     if (mode == 2 && mirror_bytes > 48 * 1024) mode = 1;  // mirror needs d+1 floats per CTA

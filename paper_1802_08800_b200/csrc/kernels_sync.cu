@@ -216,6 +216,7 @@ struct DenseBatchParams {
   double alpha;
   int apply;
   int want_norm;
+  const double* alpha_dev;
 };
 
 template <int L, int F, int TASK, int W>
@@ -279,12 +280,13 @@ __global__ void __launch_bounds__(32 * W) dense_batch_kernel(DenseBatchParams p)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  const double alpha = p.alpha_dev ? *p.alpha_dev : p.alpha;
   double nrm = 0.0;
   int bad = 0;
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     const double g = __ldcg(&p.g64[j]);
     if (!isfinite(g)) bad = 1;
-    const double w = p.w64[j] - p.alpha * g;
+    const double w = p.w64[j] - alpha * g;
     p.w64[j] = w;
     p.w32_out[j] = static_cast<float>(w);
     p.g64[j] = 0.0;
@@ -590,8 +592,9 @@ __global__ void __launch_bounds__(256) csr_batch_kernel(
   }
 }
 
-__global__ void apply_kernel(uint64_t d, double alpha, double* w64, float* w32, double* g64,
-                             int* finite, double* norm2, int want_norm) {
+__global__ void apply_kernel(uint64_t d, double alpha_in, const double* alpha_dev, double* w64,
+                             float* w32, double* g64, int* finite, double* norm2, int want_norm) {
+  const double alpha = alpha_dev ? *alpha_dev : alpha_in;
   double nrm = 0.0;
   int bad = 0;
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
@@ -786,7 +789,7 @@ void launch_dense_batch_LF(Dataset& ds, Model& m, const uint32_t* ids, uint64_t 
   DenseBatchParams p{ds.x.p,  ds.labels.p, ds.n,     ds.row_base, d,
                      ids,     nb,          m.w32.p,  m.g64.p,     m.ticket.p,
                      m.finite.p, m.w64.p,  m.w32.p,  m.scal.p,    a.alpha,
-                     a.apply ? 1 : 0, a.want_norm ? 1 : 0};
+                     a.apply ? 1 : 0, a.want_norm ? 1 : 0, a.alpha_dev};
   const unsigned grid = grid_for(c, static_cast<uint64_t>(W) * RS * 2, nb, 8);
   const size_t smem = static_cast<size_t>(W) * d * 4;
   auto kern = dense_batch_kernel<L, F, TASK, W>;
@@ -971,14 +974,14 @@ void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, con
     if (a.task == kTaskLR) launch_csr_batch_G<G, kTaskLR>(ds, m, ids, nb, a.apply);
     else launch_csr_batch_G<G, kTaskSVM>(ds, m, ids, nb, a.apply);
   });
-  if (a.apply) apply_update(m, a.alpha, a.want_norm);
+  if (a.apply) apply_update(m, a.alpha, a.want_norm, a.alpha_dev);
 }
 
-void apply_update(Model& m, double alpha, bool want_norm) {
+void apply_update(Model& m, double alpha, bool want_norm, const double* alpha_dev) {
   Ctx& c = *m.ctx;
   const unsigned grid = grid_for(c, 256ull * 4, m.d, 8);
   prof_begin(c, "apply_kernel");
-  apply_kernel<<<grid, 256, 0, c.stream>>>(m.d, alpha, m.w64.p, m.w32.p, m.g64.p, m.finite.p,
+  apply_kernel<<<grid, 256, 0, c.stream>>>(m.d, alpha, alpha_dev, m.w64.p, m.w32.p, m.g64.p, m.finite.p,
                                            m.scal.p, want_norm ? 1 : 0);
   launched(c, "apply_kernel");
 }
