@@ -83,8 +83,11 @@ void upload_csr(sgdb_dataset* ds, std::vector<uint32_t>& rowptr, std::vector<uin
   cudaStream_t s = ds->ctx->stream;
   ds->kind = Kind::Csr;
   ds->nnz = idx.size();
-  ds->val.alloc(std::max<uint64_t>(1, ds->nnz));
-  ds->idx.alloc(std::max<uint64_t>(1, ds->nnz));
+  // +8 slack: vectorised kernels read whole aligned 16-byte groups around a row.
+  ds->val.alloc(ds->nnz + 8);
+  ds->idx.alloc(ds->nnz + 8);
+  ds->val.zero(s);
+  ds->idx.zero(s);
   ds->rowptr.alloc(ds->n + 1);
   h2d(ds->val.p, val.data(), ds->nnz, s);
   h2d(ds->idx.p, idx.data(), ds->nnz, s);

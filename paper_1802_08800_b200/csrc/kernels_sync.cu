@@ -447,6 +447,82 @@ __global__ void __launch_bounds__(SMEM ? 1024 : 256) csr_coef_pipe_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// K2v: warp-per-row margin pass with 16-byte vector loads. Lane l of the
+// warp loads the aligned group 4l of the window [b & ~3, e) — a float4 of
+// values and a uint4 of indices — and gathers only its in-row slots, so a
+// row costs ~2 vector loads + 4 gathers per lane instead of 8 scalar loads.
+// Same 2-stage row pipeline as K2p (extent two rows ahead, first vector
+// group one row ahead). The CSR arrays carry 8 elements of zero slack.
+// ---------------------------------------------------------------------------
+struct VecGroup {
+  float4 v;
+  uint4 j;
+};
+
+__device__ __forceinline__ VecGroup vec_group(const float* __restrict__ val,
+                                              const uint32_t* __restrict__ idx, uint32_t a) {
+  return VecGroup{__ldg(reinterpret_cast<const float4*>(val + a)),
+                  __ldg(reinterpret_cast<const uint4*>(idx + a))};
+}
+
+__device__ __forceinline__ float vec_dot(const VecGroup& g, uint32_t a, uint32_t b, uint32_t e,
+                                         const float* __restrict__ w) {
+  float z = 0.f;
+  if (a >= b && a + 3 < e) {  // whole group inside the row (the common case)
+    z = fmaf(g.v.x, __ldg(w + g.j.x), z);
+    z = fmaf(g.v.y, __ldg(w + g.j.y), z);
+    z = fmaf(g.v.z, __ldg(w + g.j.z), z);
+    z = fmaf(g.v.w, __ldg(w + g.j.w), z);
+  } else {
+    if (a + 0 >= b && a + 0 < e) z = fmaf(g.v.x, __ldg(w + g.j.x), z);
+    if (a + 1 >= b && a + 1 < e) z = fmaf(g.v.y, __ldg(w + g.j.y), z);
+    if (a + 2 >= b && a + 2 < e) z = fmaf(g.v.z, __ldg(w + g.j.z), z);
+    if (a + 3 >= b && a + 3 < e) z = fmaf(g.v.w, __ldg(w + g.j.w), z);
+  }
+  return z;
+}
+
+template <int TASK>
+__global__ void __launch_bounds__(256) csr_coef_vec_kernel(
+    const float* __restrict__ val, const uint32_t* __restrict__ idx,
+    const uint32_t* __restrict__ rowptr, const float* __restrict__ y, uint64_t n,
+    const float* __restrict__ w, float* __restrict__ coef) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t step = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  uint64_t row = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  auto extent = [&](uint64_t r, uint32_t& b, uint32_t& e, float& yy) {
+    if (r < n) {
+      b = rowptr[r];
+      e = rowptr[r + 1];
+      yy = y[r];
+    } else {
+      b = e = 0u;
+      yy = 0.f;
+    }
+  };
+  uint32_t cb, ce, nb, ne;
+  float cy, ny;
+  extent(row, cb, ce, cy);
+  extent(row + step, nb, ne, ny);
+  uint32_t ca = (cb & ~3u) + 4u * lane;
+  VecGroup cur = vec_group(val, idx, ca < ce ? ca : 0u);
+  for (; row < n; row += step) {
+    const uint32_t na = (nb & ~3u) + 4u * lane;
+    const VecGroup nxt = vec_group(val, idx, na < ne ? na : 0u);
+    uint32_t ab, ae;
+    float ay;
+    extent(row + 2 * step, ab, ae, ay);
+    float z = ca < ce ? vec_dot(cur, ca, cb, ce, w) : 0.f;
+    for (uint32_t a = ca + 128; a < ce; a += 128) z += vec_dot(vec_group(val, idx, a), a, cb, ce, w);
+    z = group_sum<32>(z);
+    if (lane == 0) coef[row] = coef_f<TASK>(z, cy);
+    cur = nxt;
+    ca = na, cb = nb, ce = ne, cy = ny;
+    nb = ab, ne = ae, ny = ay;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K3: g = X^T c over the row-blocked CSC. CTA (block b, column range k)
 // stages c[rows of b] in SMEM, then G lanes per column reduce
 // cval * c_smem[crow] in fp64 into partials[b][j]; K3f sums the partials over
@@ -857,6 +933,20 @@ void launch_csr_coef_pipe_G(Dataset& ds, Model& m) {
   launched(c, "csr_coef_kernel");
 }
 
+template <int TASK>
+void launch_csr_coef_vec(Dataset& ds, Model& m) {
+  Ctx& c = *ds.ctx;
+  auto kern = csr_coef_vec_kernel<TASK>;
+  int per_sm = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0), "occupancy");
+  const uint64_t want = (ds.n * 32 + 255) / 256;
+  const unsigned grid = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(std::max(1, per_sm)) * c.num_sms)));
+  prof_begin(c, "csr_coef_kernel");
+  kern<<<grid, 256, 0, c.stream>>>(ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p, ds.n, m.w32.p, ds.coef.p);
+  launched(c, "csr_coef_kernel");
+}
+
 template <int G>
 void launch_csc_block_G(Dataset& ds, Model& m) {
   Ctx& c = *ds.ctx;
@@ -949,7 +1039,14 @@ void csr_full_step(Dataset& ds, Model& m, const StepArgs& a) {
       return e && std::atoi(e) != 0;
     }();
     const bool smem_model = smem_pref && ds.d * sizeof(float) <= 192 * 1024;
-    dispatch_G(g, [&]<int G>() {
+    static const bool vec_pref = [] {
+      const char* e = std::getenv("SGDB_ROW_VEC");
+      return !e || std::atoi(e) != 0;
+    }();
+    if (g == 32 && vec_pref && !smem_model) {
+      if (a.task == kTaskLR) launch_csr_coef_vec<kTaskLR>(ds, m);
+      else launch_csr_coef_vec<kTaskSVM>(ds, m);
+    } else dispatch_G(g, [&]<int G>() {
       if (smem_model) {
         if (a.task == kTaskLR) launch_csr_coef_pipe_G<G, kTaskLR, true>(ds, m);
         else launch_csr_coef_pipe_G<G, kTaskSVM, true>(ds, m);
