@@ -75,6 +75,15 @@ typedef enum {                                                             /* as
   SGDB_REPL_THREAD = 2,
   SGDB_REPL_EXAMPLE = 3
 } sgdb_replication;
+typedef enum {                                                             /* linalg.hpp:40 */
+  SGDB_EW_MUL = 0,
+  SGDB_EW_DIV = 1,
+  SGDB_EW_EXP = 2,
+  SGDB_EW_NEG = 3,
+  SGDB_EW_ADD_SCALAR = 4,
+  SGDB_EW_SIGMOID = 5,          /* ew_sigmoid (linalg.hpp:47), not in the reference enum */
+  SGDB_EW_HINGE_INDICATOR = 6   /* ew_hinge_indicator (linalg.hpp:50) */
+} sgdb_elementwise_op;
 
 /* ---- plain structs ------------------------------------------------------- */
 
@@ -275,6 +284,26 @@ sgdb_status sgdb_model_average_ranks(sgdb_ctx* ctx, sgdb_model* m, uint64_t worl
  * hook set the per-shard sum is reduced across ranks. */
 sgdb_status sgdb_loss(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
                       double* loss_out);
+
+/* ---- the §4 operator API (linalg.hpp:23-58) ------------------------------
+ * Stand-alone device primitives with host vectors in and out (the training
+ * path uses the fused kernels instead). fp64 arithmetic on the uploaded fp32
+ * matrix, with the reference's summation order: matvec sums each row in slot
+ * order; matvec_transposed is one sequential dot per column for a
+ * DenseColMajor upload and 256-row block partials + the fixed pairwise tree
+ * otherwise (linalg.cpp:46-109), so results equal the reference on the same
+ * (f32-valued) matrix. rows NULL / n_rows 0 = all examples (ascending). */
+sgdb_status sgdb_matvec(sgdb_ctx* ctx, sgdb_dataset* ds, const uint32_t* rows, uint64_t n_rows,
+                        const double* v, uint64_t v_len, double* out /* n_rows or n */);
+sgdb_status sgdb_matvec_transposed(sgdb_ctx* ctx, sgdb_dataset* ds, const uint32_t* rows,
+                                   uint64_t n_rows, const double* a_by_position, uint64_t a_len,
+                                   double* out /* d */);
+/* ew_* / elementwise (linalg.hpp:35-55); b is read by MUL and DIV only, scalar
+ * by ADD_SCALAR. DIV with a zero divisor -> SGDB_ERR_DOMAIN. */
+sgdb_status sgdb_elementwise(sgdb_ctx* ctx, int32_t op, const double* a, const double* b,
+                             uint64_t n, double scalar, double* out);
+/* axpy (linalg.hpp:58): w <- w - alpha * g, in place on the host array. */
+sgdb_status sgdb_axpy(sgdb_ctx* ctx, double* w, double alpha, const double* g, uint64_t n);
 
 /* ======================================================================== */
 /* 2. whole runs (host C++ epoch loops over layer 1)                        */

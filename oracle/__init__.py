@@ -290,6 +290,14 @@ class Reference(_Lib):
         L.ref_hardware_threads.restype = C.c_uint
         L.ref_write_libsvm.restype = _u64
         L.ref_write_libsvm.argtypes = [_vp, C.c_char_p, _u64]
+        L.ref_matvec.restype = _int
+        L.ref_matvec.argtypes = [_vp, _P(C.c_uint32), _u64, _P(_dbl), C.c_uint, _P(_dbl)]
+        L.ref_matvec_transposed.restype = _int
+        L.ref_matvec_transposed.argtypes = [_vp, _P(C.c_uint32), _u64, _P(_dbl), _u64, C.c_uint,
+                                            _P(_dbl)]
+        L.ref_elementwise.restype = _int
+        L.ref_elementwise.argtypes = [_int, _P(_dbl), _P(_dbl), _u64, _dbl, C.c_uint, _P(_dbl)]
+        L.ref_axpy.argtypes = [_P(_dbl), _dbl, _P(_dbl), _u64, C.c_uint]
 
     def hardware_threads(self) -> int:
         return int(self.lib.ref_hardware_threads())
@@ -317,6 +325,50 @@ class Reference(_Lib):
             return buf.raw[:size].decode()
         finally:
             self.lib.ref_ds_free(h)
+
+    def matvec(self, ds: HostData, v, rows=None, workers=1) -> np.ndarray:
+        """linalg::matvec (linalg.cpp:30-44)."""
+        h = self.to_handle(ds)
+        try:
+            rows = np.ascontiguousarray(rows if rows is not None else [], np.uint32)
+            v = np.ascontiguousarray(v, np.float64)
+            out = np.zeros(len(rows) if len(rows) else ds.n_examples, np.float64)
+            if self.lib.ref_matvec(h, _ptr(rows, C.c_uint32), len(rows), _ptr(v, _dbl), workers,
+                                   _ptr(out, _dbl)) != 0:
+                raise RuntimeError(self.err())
+            return out
+        finally:
+            self.lib.ref_ds_free(h)
+
+    def matvec_transposed(self, ds: HostData, a, rows=None, workers=1) -> np.ndarray:
+        """linalg::matvec_transposed (linalg.cpp:46-109)."""
+        h = self.to_handle(ds)
+        try:
+            rows = np.ascontiguousarray(rows if rows is not None else [], np.uint32)
+            a = np.ascontiguousarray(a, np.float64)
+            out = np.zeros(ds.n_features, np.float64)
+            if self.lib.ref_matvec_transposed(h, _ptr(rows, C.c_uint32), len(rows), _ptr(a, _dbl),
+                                              len(a), workers, _ptr(out, _dbl)) != 0:
+                raise RuntimeError(self.err())
+            return out
+        finally:
+            self.lib.ref_ds_free(h)
+
+    def elementwise(self, op, a, b=None, scalar=0.0, workers=1) -> np.ndarray:
+        """linalg::elementwise / ew_sigmoid (op 5) / ew_hinge_indicator (op 6)."""
+        a = np.ascontiguousarray(a, np.float64)
+        b = None if b is None else np.ascontiguousarray(b, np.float64)
+        out = np.zeros(len(a), np.float64)
+        if self.lib.ref_elementwise(int(op), _ptr(a, _dbl), None if b is None else _ptr(b, _dbl),
+                                    len(a), scalar, workers, _ptr(out, _dbl)) != 0:
+            raise RuntimeError(self.err())
+        return out
+
+    def axpy(self, w, alpha, g, workers=1) -> np.ndarray:
+        w = np.array(w, np.float64)
+        g = np.ascontiguousarray(g, np.float64)
+        self.lib.ref_axpy(_ptr(w, _dbl), alpha, _ptr(g, _dbl), len(w), workers)
+        return w
 
     def batch_gradient(self, ds: HostData, task, rows, w, workers=1) -> np.ndarray:
         h = self.to_handle(ds)

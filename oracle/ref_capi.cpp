@@ -343,4 +343,54 @@ double ref_point_loss_from_margin(int task, double z, double y) {
 
 unsigned ref_hardware_threads() { return std::thread::hardware_concurrency(); }
 
+// linalg:: primitives (proj/src/linalg.cpp:26-183), verbatim calls.
+int ref_matvec(void* h, const uint32_t* rows, uint64_t n_rows, const double* v, unsigned workers,
+               double* out) {
+  try {
+    Dataset* ds = D(h);
+    auto r = linalg::matvec(*ds, std::span<const std::uint32_t>(rows, n_rows),
+                            std::span<const double>(v, ds->n_features), workers);
+    std::copy(r.begin(), r.end(), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_matvec_transposed(void* h, const uint32_t* rows, uint64_t n_rows, const double* a,
+                          uint64_t a_len, unsigned workers, double* out) {
+  try {
+    Dataset* ds = D(h);
+    auto r = linalg::matvec_transposed(*ds, std::span<const std::uint32_t>(rows, n_rows),
+                                       std::span<const double>(a, a_len), workers);
+    std::copy(r.begin(), r.end(), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// op 0..4 = linalg::ElementwiseOp, 5 = ew_sigmoid, 6 = ew_hinge_indicator.
+int ref_elementwise(int op, const double* a, const double* b, uint64_t n, double scalar,
+                    unsigned workers, double* out) {
+  try {
+    std::span<const double> sa(a, n), sb(b, b ? n : 0);
+    linalg::DenseVector r;
+    if (op == 5)
+      r = linalg::ew_sigmoid(sa, workers);
+    else if (op == 6)
+      r = linalg::ew_hinge_indicator(sa, workers);
+    else
+      r = linalg::elementwise(static_cast<linalg::ElementwiseOp>(op), sa, sb, scalar, workers);
+    std::copy(r.begin(), r.end(), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+void ref_axpy(double* w, double alpha, const double* g, uint64_t n, unsigned workers) {
+  linalg::axpy(std::span<double>(w, n), alpha, std::span<const double>(g, n), workers);
+}
+
 }  // extern "C"

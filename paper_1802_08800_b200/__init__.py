@@ -7,10 +7,11 @@ Importing requires the in-tree libsgdb_b200.so (no CPU fallback).
 """
 from . import _lib
 from .api import (  # noqa: F401
-    AccessPath, Dataset, Device, DeviceDataset, DeviceModel, EpochRecord, ExecutionPlan,
+    AccessPath, Dataset, Device, DeviceDataset, DeviceModel, ElementwiseOp, EpochRecord,
+    ExecutionPlan,
     Hyperparams, Layout, LossTrace, ModelReplication, Options, Result, Schedule, Strategy, Task,
     TrainOptions, TrainResult, assign, convert_layout, dataset_loss, default_device,
-    device_loss, fixtures, generate_hidden_model, hogwild, hogwild_epoch, load_binary, models_average, parse_libsvm,
+    device_loss, fixtures, generate_hidden_model, hogwild, hogwild_epoch, linalg, load_binary, models_average, parse_libsvm,
     parse_plan, plan_to_string, save_binary, sync, sync_epoch, validate_plan, write_libsvm,
 )
 from ._lib import CapacityError, CudaError, ParseError, SgdbError, UnsupportedError  # noqa: F401

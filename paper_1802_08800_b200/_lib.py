@@ -95,6 +95,10 @@ PROTOTYPES = {
     "sgdb_hogwild_epoch": (_S, [vp, vp, vp, i32, dbl, P(Plan), P(u64)]),
     "sgdb_models_average": (_S, [vp, P(vp), u64, P(dbl), vp, i32]),
     "sgdb_loss": (_S, [vp, vp, vp, i32, P(dbl)]),
+    "sgdb_matvec": (_S, [vp, vp, P(u32), u64, P(dbl), u64, P(dbl)]),
+    "sgdb_matvec_transposed": (_S, [vp, vp, P(u32), u64, P(dbl), u64, P(dbl)]),
+    "sgdb_elementwise": (_S, [vp, i32, P(dbl), P(dbl), u64, dbl, P(dbl)]),
+    "sgdb_axpy": (_S, [vp, P(dbl), dbl, P(dbl), u64]),
     "sgdb_sync_train": (_S, [vp, vp, P(Hyper), u64, P(TrainOptions), P(dbl), P(Trace)]),
     "sgdb_hogwild_train": (_S, [vp, vp, P(Hyper), P(Plan), u64, P(TrainOptions), P(dbl),
                                 P(Trace)]),

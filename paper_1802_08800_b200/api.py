@@ -700,6 +700,106 @@ class sync:  # noqa: N801 — namespace mirror of sgdbench::sync
         return float(norm.value)
 
 
+# ---- linalg.hpp ---------------------------------------------------------------------------
+class ElementwiseOp(IntEnum):  # linalg.hpp:40 (+ the two fused ops)
+    Mul = 0
+    Div = 1
+    Exp = 2
+    Neg = 3
+    AddScalar = 4
+    Sigmoid = 5
+    HingeIndicator = 6
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, np.float64)
+
+
+class linalg:  # noqa: N801 — namespace mirror of sgdbench::linalg (linalg.hpp:23-58)
+    """The §4 operator API on the device. `workers` is accepted for signature
+    parity and ignored (the device decides its own parallelism); results follow
+    the reference's summation order (see include/sgdb.h)."""
+
+    @staticmethod
+    def matvec(ds, v, rows=None, workers: int = 1, device: Optional[Device] = None) -> np.ndarray:
+        """out_p = x_{rows[p]} . v (linalg.cpp:30-44)."""
+        dds = _as_device_dataset(ds, device)
+        v = _f64(v)
+        r = np.ascontiguousarray(rows if rows is not None else [], np.uint32)
+        out = np.zeros(r.size if r.size else dds.n_global, np.float64)
+        check(_lib().sgdb_matvec(dds.dev.handle, dds.handle, _u32ptr(r), r.size, _dptr(v), v.size,
+                                 _dptr(out)))
+        return out
+
+    @staticmethod
+    def matvec_transposed(ds, a, rows=None, workers: int = 1,
+                          device: Optional[Device] = None) -> np.ndarray:
+        """X^T a over the rows, `a` indexed by position (linalg.cpp:46-109)."""
+        dds = _as_device_dataset(ds, device)
+        a = _f64(a)
+        r = np.ascontiguousarray(rows if rows is not None else [], np.uint32)
+        out = np.zeros(dds.n_features, np.float64)
+        check(_lib().sgdb_matvec_transposed(dds.dev.handle, dds.handle, _u32ptr(r), r.size,
+                                            _dptr(a), a.size, _dptr(out)))
+        return out
+
+    @staticmethod
+    def elementwise(op: ElementwiseOp, a, b=None, scalar: float = 0.0, workers: int = 1,
+                    device: Optional[Device] = None) -> np.ndarray:
+        """elementwise (linalg.cpp:167-177); binary ops require equal lengths."""
+        dev = device or default_device()
+        a = _f64(a)
+        binary = op in (ElementwiseOp.Mul, ElementwiseOp.Div)
+        if binary:
+            b = _f64(b)
+            if b.size != a.size:
+                name = "ew_mul" if op == ElementwiseOp.Mul else "ew_div"
+                raise ValueError(f"{name}: length mismatch")
+        out = np.zeros(a.size, np.float64)
+        check(_lib().sgdb_elementwise(dev.handle, int(op), _dptr(a), _dptr(b) if binary else None,
+                                      a.size, float(scalar), _dptr(out)))
+        return out
+
+    @staticmethod
+    def ew_mul(a, b, workers: int = 1, device=None):
+        return linalg.elementwise(ElementwiseOp.Mul, a, b, device=device)
+
+    @staticmethod
+    def ew_div(a, b, workers: int = 1, device=None):
+        return linalg.elementwise(ElementwiseOp.Div, a, b, device=device)
+
+    @staticmethod
+    def ew_exp(a, workers: int = 1, device=None):
+        return linalg.elementwise(ElementwiseOp.Exp, a, device=device)
+
+    @staticmethod
+    def ew_neg(a, workers: int = 1, device=None):
+        return linalg.elementwise(ElementwiseOp.Neg, a, device=device)
+
+    @staticmethod
+    def ew_add_scalar(s: float, a, workers: int = 1, device=None):
+        return linalg.elementwise(ElementwiseOp.AddScalar, a, scalar=s, device=device)
+
+    @staticmethod
+    def ew_sigmoid(a, workers: int = 1, device=None):
+        return linalg.elementwise(ElementwiseOp.Sigmoid, a, device=device)
+
+    @staticmethod
+    def ew_hinge_indicator(a, workers: int = 1, device=None):
+        return linalg.elementwise(ElementwiseOp.HingeIndicator, a, device=device)
+
+    @staticmethod
+    def axpy(w: np.ndarray, alpha: float, g, workers: int = 1, device=None) -> None:
+        """w <- w - alpha g in place (linalg.cpp:179-183)."""
+        dev = device or default_device()
+        g = _f64(g)
+        if not (isinstance(w, np.ndarray) and w.dtype == np.float64 and w.flags.c_contiguous):
+            raise TypeError("axpy: w must be a contiguous float64 array (updated in place)")
+        if w.size != g.size:
+            raise ValueError("axpy: length mismatch")
+        check(_lib().sgdb_axpy(dev.handle, _dptr(w), float(alpha), _dptr(g), w.size))
+
+
 # ---- async_engine.hpp -------------------------------------------------------------------
 @dataclass
 class Options:  # async_engine.hpp:77-82

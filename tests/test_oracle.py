@@ -164,3 +164,22 @@ def test_live_reference_dual_and_thread(O, ref):
     sm, sl, _ = O.hogwild_serial(ds, 0, 0.08, 4, 0, 0, 0, 1)
     assert np.array_equal(dm, sm[-1]) and np.array_equal(dl, sl)
     assert int(de[0]) == 2 * ds.n_examples
+
+
+def test_live_reference_linalg(O, ref):
+    """The linalg:: wrappers the operator-API GPU tests compare against: the
+    reference is bit-identical for any worker count and agrees with numpy."""
+    ds = O.fixture_sparse(256 * 5 + 9, 300, 10.0, 77)
+    dense = np.zeros((ds.n_examples, ds.n_features))
+    for i in range(ds.n_examples):
+        lo, hi = int(ds.row_offsets[i]), int(ds.row_offsets[i + 1])
+        dense[i, ds.indices[lo:hi]] = ds.values[lo:hi]
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal(ds.n_examples)
+    v = rng.standard_normal(ds.n_features)
+    t1 = ref.matvec_transposed(ds, a, workers=1)
+    assert np.array_equal(t1, ref.matvec_transposed(ds, a, workers=3))
+    assert np.allclose(t1, dense.T @ a, rtol=1e-12, atol=1e-12)
+    assert np.allclose(ref.matvec(ds, v), dense @ v, rtol=1e-12, atol=1e-12)
+    assert np.array_equal(ref.elementwise(3, a), -a)
+    assert np.array_equal(ref.axpy(v, 0.5, v), v - 0.5 * v)
