@@ -197,9 +197,8 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def step():
-        S.hogwild_epoch(dds, model, task, alpha, plan)
-        if world > 1:
-            SD.average_ranks(dev, model, world)
+        # N > 1: rank replicas averaged args.segments times per epoch (§8(e)).
+        SD.hogwild_epoch_ranks(dev, dds, model, task, alpha, plan, world, args.segments)
 
     def barrier():
         if world > 1:
@@ -276,6 +275,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference fixtures, seed+rank)",
         "config": {"workload": WORKLOAD, "plan": PLAN, "workers": plan.workers,
+                   "replica_averages_per_epoch": args.segments if world > 1 else 0,
                    "lanes_per_worker": "auto", "alpha": alpha, "n_per_gpu": N_EX, "d": D,
                    "nnz_per_gpu": dds.nnz, "l2": "flushed before every step (256 MiB memset, "
                                                   "outside the event window)"},
@@ -452,6 +452,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workers", type=int, default=0, help="0 = every resident lane group")
     ap.add_argument("--alpha", type=float, default=0.01)
+    ap.add_argument("--segments", type=int, default=1,
+                    help="N > 1: cross-rank replica averages per Hogwild epoch")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-convergence", action="store_true")
     ap.add_argument("--no-extra", action="store_true")

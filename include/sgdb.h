@@ -270,6 +270,16 @@ sgdb_status sgdb_epoch_batch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int
  * read the model, before using results on the host. */
 sgdb_status sgdb_hogwild_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
                                double alpha, const sgdb_plan* plan, uint64_t* evals_out);
+/* Segment seg of nseg of that epoch: every worker runs positions
+ * [t*seg/nseg, t*(seg+1)/nseg) of its assign() list (t = its length), with
+ * replica prepare/merge around it. Running segments 0..nseg-1 back to back
+ * is one epoch with a barrier after each segment; the multi-GPU Hogwild
+ * path averages the rank replicas at those barriers (the
+ * numa_dual_train merge, async_engine.cpp:478-501, made k times per epoch).
+ * *evals_out = evaluations in this segment. */
+sgdb_status sgdb_hogwild_segment(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
+                                 double alpha, const sgdb_plan* plan, uint32_t seg, uint32_t nseg,
+                                 uint64_t* evals_out);
 /* merge_models (async_engine.cpp:133-156) over device models: out = weighted
  * mean (weights NULL = unweighted); when refresh != 0 every input is set to it. */
 sgdb_status sgdb_models_average(sgdb_ctx* ctx, sgdb_model* const* models, uint64_t count,

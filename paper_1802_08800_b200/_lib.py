@@ -93,6 +93,7 @@ PROTOTYPES = {
     "sgdb_batch_gradient": (_S, [vp, vp, i32, P(u32), u64, P(dbl), P(dbl)]),
     "sgdb_epoch_batch": (_S, [vp, vp, vp, i32, dbl, P(dbl)]),
     "sgdb_hogwild_epoch": (_S, [vp, vp, vp, i32, dbl, P(Plan), P(u64)]),
+    "sgdb_hogwild_segment": (_S, [vp, vp, vp, i32, dbl, P(Plan), u32, u32, P(u64)]),
     "sgdb_models_average": (_S, [vp, P(vp), u64, P(dbl), vp, i32]),
     "sgdb_loss": (_S, [vp, vp, vp, i32, P(dbl)]),
     "sgdb_matvec": (_S, [vp, vp, P(u32), u64, P(dbl), u64, P(dbl)]),

@@ -541,11 +541,13 @@ def sync_epoch(dds: DeviceDataset, model: DeviceModel, task: Task, alpha: float,
 
 
 def hogwild_epoch(dds: DeviceDataset, model: DeviceModel, task: Task, alpha: float,
-                  plan: ExecutionPlan) -> int:
+                  plan: ExecutionPlan, segment: int = 0, segments: int = 1) -> int:
+    """One Hogwild epoch (or segment `segment` of `segments`, see
+    sgdb_hogwild_segment); returns the number of example evaluations."""
     p = plan.to_c()
     ev = L.u64(0)
-    check(_lib().sgdb_hogwild_epoch(dds.dev.handle, dds.handle, model.handle, int(task), alpha,
-                                    C.byref(p), C.byref(ev)))
+    check(_lib().sgdb_hogwild_segment(dds.dev.handle, dds.handle, model.handle, int(task), alpha,
+                                      C.byref(p), int(segment), int(segments), C.byref(ev)))
     return int(ev.value)
 
 

@@ -113,6 +113,31 @@ uint64_t nonempty_workers(uint64_t n, uint64_t T, bool rr) {
   return (n + chunk - 1) / chunk;
 }
 
+// Evaluations in segment seg of nseg: per worker, list positions
+// [total*seg/nseg, total*(seg+1)/nseg) of its assign() list (n + k per
+// non-empty worker in all), as run_worker splits them.
+uint64_t segment_evals(uint64_t n, uint64_t T, bool rr, uint64_t k, uint32_t seg, uint32_t nseg) {
+  if (nseg == 1) return n + nonempty_workers(n, T, rr) * k;
+  const uint64_t chunk = (n + T - 1) / T;
+  uint64_t total_evals = 0;
+  for (uint64_t w = 0; w < T; ++w) {
+    uint64_t cnt;
+    if (rr) {
+      cnt = w < n ? (n - 1 - w) / T + 1 : 0;
+    } else {
+      const uint64_t b = std::min(n, w * chunk), e = std::min(n, b + chunk);
+      cnt = e - b;
+    }
+    if (cnt == 0) {
+      if (!rr) break;  // chunk lists are empty from here on
+      continue;
+    }
+    const uint64_t t = cnt + k;
+    total_evals += t * (seg + 1) / nseg - t * seg / nseg;
+  }
+  return total_evals;
+}
+
 // The finite flag is any nonzero value while every gradient entry was
 // finite; kernels write 0. Reset with a device memset (no host staging) and
 // read back through pinned memory.
@@ -651,8 +676,15 @@ sgdb_status sgdb_epoch_batch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int
 
 sgdb_status sgdb_hogwild_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
                                double alpha, const sgdb_plan* plan, uint64_t* evals_out) {
+  return sgdb_hogwild_segment(ctx, ds, m, task, alpha, plan, 0, 1, evals_out);
+}
+
+sgdb_status sgdb_hogwild_segment(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
+                                 double alpha, const sgdb_plan* plan, uint32_t seg, uint32_t nseg,
+                                 uint64_t* evals_out) {
   return sgdb_guard([&] {
     require(ctx && ds && m && plan, "null argument");
+    require(nseg >= 1 && seg < nseg, "segment out of range");
     require(m->d == ds->d, "model/dataset dim mismatch");
     require(ds->n >= 1, "cannot train on an empty dataset");
     validate_device_plan(*plan, ds->layout_in);
@@ -674,10 +706,12 @@ sgdb_status sgdb_hogwild_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, i
     if (const char* e = std::getenv("SGDB_HOGWILD_REFRESH"))
       a.refresh = static_cast<uint32_t>(std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("SGDB_HOGWILD_SPREAD")) a.spread = std::atoi(e) != 0;
+    a.seg = seg;
+    a.nseg = nseg;
     hogwild_epoch(*ds, *m, a);
     if (evals_out) {
       const bool rr = plan->access_path == SGDB_ACCESS_ROW_RR || plan->access_path == SGDB_ACCESS_COL_RR;
-      *evals_out = ds->n + nonempty_workers(ds->n, plan->workers, rr) * plan->data_replication_k;
+      *evals_out = segment_evals(ds->n, plan->workers, rr, plan->data_replication_k, seg, nseg);
     }
   });
 }

@@ -202,6 +202,7 @@ struct HogwildArgs {
   int model_mode = 1;    // kernel scope: 0 plain ld/st, 1 red.add, 2 smem mirror + red.add
   uint32_t refresh = 4;  // mirror: refresh a read from L2 on every refresh-th example id
   bool spread = true;    // kernel scope: 256 B-strided model copy during the epoch
+  uint32_t seg = 0, nseg = 1;  // run list positions [total*seg/nseg, total*(seg+1)/nseg)
 };
 int hogwild_auto_lanes(const Dataset& ds, int access);
 uint64_t hogwild_resident_workers(const Ctx& c, int lanes);

@@ -52,6 +52,7 @@ struct HogParams {
   float alpha;
   uint32_t refresh;  // mirror kernel: refresh reads from L2 every `refresh` examples
   uint32_t ms;       // kernel scope: float stride between model coordinates in global
+  uint32_t seg, nseg;  // this launch runs list positions [total*seg/nseg, total*(seg+1)/nseg)
 };
 
 template <int G>
@@ -274,15 +275,18 @@ template <int G, int TASK, int KIND, class M>
 __device__ __forceinline__ void run_worker(const HogParams& p, const M& m, uint64_t w, int lg,
                                            unsigned mask) {
   const WorkerList l = worker_list(p, w);
-  if (l.total == 0) return;
-  Row cur = make_row<KIND>(p, list_at(p, l, 0));
-  Row nxt = l.total > 1 ? make_row<KIND>(p, list_at(p, l, 1)) : cur;
+  // Segment of the list (multi-GPU replicas averaged every segment; 0 of 1 = epoch).
+  const uint32_t lo = static_cast<uint32_t>(uint64_t(l.total) * p.seg / p.nseg);
+  const uint32_t hi = static_cast<uint32_t>(uint64_t(l.total) * (p.seg + 1) / p.nseg);
+  if (lo >= hi) return;
+  Row cur = make_row<KIND>(p, list_at(p, l, lo));
+  Row nxt = lo + 1 < hi ? make_row<KIND>(p, list_at(p, l, lo + 1)) : cur;
   Batch bcur = load_batch<G, KIND>(p, cur, lg, row_len<KIND>(cur));
-  for (uint32_t i = 0; i < l.total; ++i) {
+  for (uint32_t i = lo; i < hi; ++i) {
     Batch bnxt = bcur;
     Row after = nxt;
-    if (i + 1 < l.total) bnxt = load_batch<G, KIND>(p, nxt, lg, row_len<KIND>(nxt));
-    if (i + 2 < l.total) after = make_row<KIND>(p, list_at(p, l, i + 2));
+    if (i + 1 < hi) bnxt = load_batch<G, KIND>(p, nxt, lg, row_len<KIND>(nxt));
+    if (i + 2 < hi) after = make_row<KIND>(p, list_at(p, l, i + 2));
     process_example<G, TASK, KIND>(p, m.at(cur.e), cur, bcur, w, lg, mask);
     cur = nxt;
     bcur = bnxt;
@@ -536,6 +540,9 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
   p.rr = rr ? 1 : 0;
   p.offsets = a.offsets ? 1 : 0;
   p.alpha = a.alpha;
+  if (a.nseg == 0 || a.seg >= a.nseg) throw std::invalid_argument("hogwild segment out of range");
+  p.seg = a.seg;
+  p.nseg = a.nseg;
   const int G = a.lanes;
 
 

@@ -12,8 +12,11 @@ averaging (proj/src/async_engine.cpp:462-520). Here:
   rank walks the same global mini-batch schedule, computes the partial
   gradient of its members, the engine SUM-all-reduces g (fp64) and applies
   the identical update on every rank.
-* Hogwild: each rank runs the Hogwild kernels on its replica and the models
-  are averaged every ``merge_period`` epochs (``average_ranks``).
+* Hogwild: each rank runs the Hogwild kernels on its replica (its row shard,
+  or the full data for the numa_dual_train-style mode) and the replicas are
+  averaged ``segments`` times per epoch (``hogwild_epoch_ranks``): every
+  worker's assign() list is cut into ``segments`` equal position ranges and
+  the ranks all-reduce the model after each ("every k batches").
 """
 from __future__ import annotations
 
@@ -21,7 +24,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib as L
-from .api import Device, DeviceModel
+from .api import Device, DeviceDataset, DeviceModel, ExecutionPlan, Task, hogwild_epoch
 
 
 def shard_rows(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -70,3 +73,18 @@ def attach(dev: Device, group=None) -> None:
 def average_ranks(dev: Device, model: DeviceModel, world: int) -> None:
     """Replica averaging across ranks: SUM all-reduce of the fp64 model, / world."""
     L.check(L.load().sgdb_model_average_ranks(dev.handle, model.handle, world))
+
+
+def hogwild_epoch_ranks(dev: Device, dds: DeviceDataset, model: DeviceModel, task: Task,
+                        alpha: float, plan: ExecutionPlan, world: int, segments: int = 1) -> int:
+    """One multi-GPU Hogwild epoch: ``segments`` segments of this rank's replica
+    epoch (sgdb_hogwild_segment), each followed by the cross-rank average of
+    the replicas. segments=1 is a per-epoch merge (numa_dual_train with
+    merge_period 1, async_engine.cpp:478-501). Returns this rank's evaluations."""
+    if segments < 1:
+        raise ValueError("segments must be >= 1")
+    evals = 0
+    for s in range(segments):
+        evals += hogwild_epoch(dds, model, task, alpha, plan, s, segments)
+        average_ranks(dev, model, world)
+    return evals
