@@ -30,8 +30,10 @@
  * (proj/src/sync_engine.cpp:107-113).
  *
  * Precision: the interface is fp64 like the reference (dataset.hpp:46-48);
- * device storage and per-example arithmetic are fp32, reductions and the
- * synchronous master model fp64.
+ * by default device storage and per-example arithmetic are fp32, reductions
+ * and the synchronous master model fp64. Datasets
+ * uploaded with SGDB_UPLOAD_EXACT_FP64 run every op in fp64 in the
+ * reference's operation order instead (bit-identical results).
  */
 #ifndef SGDB_H_
 #define SGDB_H_
@@ -209,6 +211,16 @@ sgdb_status sgdb_ctx_resident_workers(sgdb_ctx* ctx, const sgdb_dataset* ds,
  * (multi-GPU); pass 0 / n_examples for a whole dataset. */
 sgdb_status sgdb_dataset_upload(sgdb_ctx* ctx, const sgdb_dataset_view* view, uint64_t row_base,
                                 uint64_t n_global, sgdb_dataset** out);
+/* Upload with flags. SGDB_UPLOAD_EXACT_FP64 also keeps the fp64 values and
+ * switches every op on the dataset to the exact-fp64 mode: sync epochs,
+ * batch_gradient and epoch_batch run the reference's primitive chain in its
+ * summation order, Hogwild runs process_examples in fp64 (bit-identical with
+ * one worker), the loss sums in id order, and exp is glibc's, restated
+ * (kernels_linalg.cu, libm_exp.hpp). Results then equal the reference's bit
+ * for bit (LR losses to the ulp of log1p). Whole (unsharded) datasets only. */
+#define SGDB_UPLOAD_EXACT_FP64 1u
+sgdb_status sgdb_dataset_upload_ex(sgdb_ctx* ctx, const sgdb_dataset_view* view, uint64_t row_base,
+                                   uint64_t n_global, uint32_t flags, sgdb_dataset** out);
 /* Re-copy host arrays of the same shape into an existing device dataset
  * (the e2e leg of bench.py): fp32 values/labels straight from (pinned) host
  * buffers, asynchronously on the context stream. indices/row_offsets may be
@@ -256,10 +268,12 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
                             double alpha, const uint32_t* order, uint64_t batch_b,
                             int32_t* finite_out);
 /* sync::batch_gradient (sync_engine.hpp:33-36): g over `rows` (global ids;
- * n_rows == 0 = all) at the host model w. No update. */
+ * n_rows == 0 = all) at the host model w. No update. `transposed` != 0 says
+ * the caller would pass the materialised column-major transpose: in the
+ * exact-fp64 mode it selects the per-column summation order for dense data. */
 sgdb_status sgdb_batch_gradient(sgdb_ctx* ctx, sgdb_dataset* ds, int32_t task,
                                 const uint32_t* rows, uint64_t n_rows, const double* w,
-                                double* g_out);
+                                int32_t transposed, double* g_out);
 /* sync::epoch_batch (sync_engine.hpp:40-41): one B=N step, returns ||g||_2. */
 sgdb_status sgdb_epoch_batch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t task,
                              double alpha, double* grad_norm_out);

@@ -167,10 +167,17 @@ class Device {
   sgdb_ctx* ctx_ = nullptr;
 };
 
+// Arithmetic of device datasets: Fp32 = the fused fp32 kernels (default);
+// ExactFp64 = SGDB_UPLOAD_EXACT_FP64, results bit-identical to the reference.
+// The process default starts from the environment (SGDB_PRECISION=exact).
+enum class Precision { Fp32, ExactFp64 };
+void set_default_precision(Precision p);
+Precision default_precision();
+
 class DeviceDataset {
  public:
   DeviceDataset(Device& dev, const Dataset& ds, std::size_t row_base = 0,
-                std::size_t n_global = 0);
+                std::size_t n_global = 0, Precision precision = default_precision());
   ~DeviceDataset();
   DeviceDataset(const DeviceDataset&) = delete;
   DeviceDataset& operator=(const DeviceDataset&) = delete;

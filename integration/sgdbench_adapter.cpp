@@ -8,16 +8,23 @@
 //   sgdbench::sync::train            proj/include/sgdbench/sync_engine.hpp:51-52
 //   sgdbench::hogwild::train         proj/include/sgdbench/async_engine.hpp:96-97
 //   sgdbench::hogwild::numa_dual_train proj/include/sgdbench/async_engine.hpp:102-104
+//   sgdbench::linalg::{matvec, matvec_transposed, ew_*, elementwise, axpy}
+//                                    proj/include/sgdbench/linalg.hpp:23-58
+// Datasets are uploaded in the exact-fp64 mode (SGDB_UPLOAD_EXACT_FP64), so
+// results are bit-identical to the reference's; SGDB_PRECISION=fp32 selects
+// the fused fp32 kernels (the benchmarked path) instead.
 // Everything else (dataset I/O, plan grammar, harness, warp simulator) stays
 // the reference's. See INTEGRATION.md for the two ways to link it (replace
 // sync_engine.cpp / the engine half of async_engine.cpp, or interpose the
 // shared library ahead of libsgdbench).
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
 
 #include "sgdb.h"
 #include "sgdbench/async_engine.hpp"
+#include "sgdbench/linalg.hpp"
 #include "sgdbench/sync_engine.hpp"
 
 namespace {
@@ -60,11 +67,19 @@ sgdb_dataset_view view_of(const sgdbench::Dataset& ds) {
   return v;
 }
 
+uint32_t upload_flags() {
+  static const uint32_t flags = [] {
+    const char* e = std::getenv("SGDB_PRECISION");
+    return e && std::string(e) == "fp32" ? 0u : SGDB_UPLOAD_EXACT_FP64;
+  }();
+  return flags;
+}
+
 struct Uploaded {
   sgdb_dataset* ds = nullptr;
   explicit Uploaded(const sgdbench::Dataset& d) {
     const sgdb_dataset_view v = view_of(d);
-    throw_for(sgdb_dataset_upload(context(), &v, 0, 0, &ds));
+    throw_for(sgdb_dataset_upload_ex(context(), &v, 0, 0, upload_flags(), &ds));
   }
   ~Uploaded() { sgdb_dataset_free(ds); }
 };
@@ -159,12 +174,13 @@ namespace sync {
 
 linalg::DenseVector batch_gradient(Task task, const Dataset& ds,
                                    std::span<const std::uint32_t> rows,
-                                   std::span<const double> w, unsigned, const Dataset*) {
+                                   std::span<const double> w, unsigned,
+                                   const Dataset* transposed) {
   if (w.size() != ds.n_features) throw std::invalid_argument("matvec: dimension mismatch");
   Uploaded up(ds);
   linalg::DenseVector g(ds.n_features, 0.0);
   throw_for(sgdb_batch_gradient(context(), up.ds, static_cast<int32_t>(task), rows.data(),
-                                rows.size(), w.data(), g.data()));
+                                rows.size(), w.data(), transposed != nullptr, g.data()));
   return g;
 }
 
@@ -212,4 +228,86 @@ Result numa_dual_train(Task task, const Dataset& ds, const Hyperparams& hyper,
 }
 
 }  // namespace hogwild
+namespace linalg {
+
+DenseVector matvec(const Dataset& x, std::span<const std::uint32_t> rows, std::span<const double> v,
+                   unsigned) {
+  if (v.size() != x.n_features) throw std::invalid_argument("matvec: dimension mismatch");
+  Uploaded up(x);
+  DenseVector out(rows.empty() ? x.n_examples : rows.size(), 0.0);
+  throw_for(sgdb_matvec(context(), up.ds, rows.data(), rows.size(), v.data(), v.size(),
+                        out.data()));
+  return out;
+}
+
+DenseVector matvec(const Dataset& x, std::span<const double> v, unsigned workers) {
+  return matvec(x, std::span<const std::uint32_t>{}, v, workers);
+}
+
+DenseVector matvec_transposed(const Dataset& x, std::span<const std::uint32_t> rows,
+                              std::span<const double> a_by_position, unsigned) {
+  const std::size_t n = rows.empty() ? x.n_examples : rows.size();
+  if (a_by_position.size() != n)
+    throw std::invalid_argument("matvec_transposed: dimension mismatch");
+  if (n == 0) return DenseVector(x.n_features, 0.0);
+  Uploaded up(x);
+  DenseVector out(x.n_features, 0.0);
+  throw_for(sgdb_matvec_transposed(context(), up.ds, rows.data(), rows.size(),
+                                   a_by_position.data(), a_by_position.size(), out.data()));
+  return out;
+}
+
+DenseVector matvec_transposed(const Dataset& x, std::span<const double> a, unsigned workers) {
+  return matvec_transposed(x, std::span<const std::uint32_t>{}, a, workers);
+}
+
+namespace {
+DenseVector ew(int32_t op, std::span<const double> a, std::span<const double> b, double s) {
+  DenseVector out(a.size());
+  throw_for(sgdb_elementwise(context(), op, a.data(), b.empty() ? nullptr : b.data(), a.size(), s,
+                             out.data()));
+  return out;
+}
+void same_length(std::span<const double> a, std::span<const double> b, const char* what) {
+  if (a.size() != b.size()) throw std::invalid_argument(std::string(what) + ": length mismatch");
+}
+}  // namespace
+
+DenseVector ew_mul(std::span<const double> a, std::span<const double> b, unsigned) {
+  same_length(a, b, "ew_mul");
+  return ew(SGDB_EW_MUL, a, b, 0.0);
+}
+DenseVector ew_div(std::span<const double> a, std::span<const double> b, unsigned) {
+  same_length(a, b, "ew_div");
+  return ew(SGDB_EW_DIV, a, b, 0.0);
+}
+DenseVector ew_exp(std::span<const double> a, unsigned) { return ew(SGDB_EW_EXP, a, {}, 0.0); }
+DenseVector ew_neg(std::span<const double> a, unsigned) { return ew(SGDB_EW_NEG, a, {}, 0.0); }
+DenseVector ew_add_scalar(double s, std::span<const double> a, unsigned) {
+  return ew(SGDB_EW_ADD_SCALAR, a, {}, s);
+}
+DenseVector ew_sigmoid(std::span<const double> a, unsigned) {
+  return ew(SGDB_EW_SIGMOID, a, {}, 0.0);
+}
+DenseVector ew_hinge_indicator(std::span<const double> a, unsigned) {
+  return ew(SGDB_EW_HINGE_INDICATOR, a, {}, 0.0);
+}
+DenseVector elementwise(ElementwiseOp op, std::span<const double> a, std::span<const double> b,
+                        double scalar, unsigned workers) {
+  switch (op) {
+    case ElementwiseOp::Mul: return ew_mul(a, b, workers);
+    case ElementwiseOp::Div: return ew_div(a, b, workers);
+    case ElementwiseOp::Exp: return ew_exp(a, workers);
+    case ElementwiseOp::Neg: return ew_neg(a, workers);
+    case ElementwiseOp::AddScalar: return ew_add_scalar(scalar, a, workers);
+  }
+  throw std::invalid_argument("unknown elementwise op");
+}
+
+void axpy(std::span<double> w, double alpha, std::span<const double> g, unsigned) {
+  if (w.size() != g.size()) throw std::invalid_argument("axpy: length mismatch");
+  throw_for(sgdb_axpy(context(), w.data(), alpha, g.data(), w.size()));
+}
+
+}  // namespace linalg
 }  // namespace sgdbench

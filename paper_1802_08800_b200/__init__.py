@@ -12,7 +12,8 @@ from .api import (  # noqa: F401
     Hyperparams, Layout, LossTrace, ModelReplication, Options, Result, Schedule, Strategy, Task,
     TrainOptions, TrainResult, assign, convert_layout, dataset_loss, default_device,
     device_loss, fixtures, generate_hidden_model, hogwild, hogwild_epoch, linalg, load_binary, models_average, parse_libsvm,
-    parse_plan, plan_to_string, save_binary, sync, sync_epoch, validate_plan, write_libsvm,
+    parse_plan, plan_to_string, save_binary, set_default_precision, sync, sync_epoch,
+    validate_plan, write_libsvm,
 )
 from ._lib import CapacityError, CudaError, ParseError, SgdbError, UnsupportedError  # noqa: F401
 

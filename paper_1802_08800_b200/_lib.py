@@ -16,6 +16,7 @@ u64, i64, i32, u32, dbl, vp = C.c_uint64, C.c_int64, C.c_int32, C.c_uint32, C.c_
 P = C.POINTER
 
 SGDB_OK = 0
+SGDB_UPLOAD_EXACT_FP64 = 1
 STATUS_NAMES = {
     1: "invalid_argument", 2: "domain_error", 3: "parse_error", 4: "capacity_error",
     5: "runtime_error", 6: "cuda_error", 7: "unsupported",
@@ -77,6 +78,7 @@ PROTOTYPES = {
     "sgdb_ctx_kernel_stats": (_S, [vp, u64, C.c_char_p, u64, P(u64), P(dbl), P(u64)]),
     "sgdb_model_average_ranks": (_S, [vp, vp, u64]),
     "sgdb_dataset_upload": (_S, [vp, P(DatasetView), u64, u64, P(vp)]),
+    "sgdb_dataset_upload_ex": (_S, [vp, P(DatasetView), u64, u64, u32, P(vp)]),
     "sgdb_dataset_refresh_f32": (_S, [vp, vp, vp, vp, vp, vp]),
     "sgdb_dataset_free": (_S, [vp]),
     "sgdb_dataset_generate_dense": (_S, [vp, u64, u64, u64, u64, u64, dbl, P(vp)]),
@@ -90,7 +92,7 @@ PROTOTYPES = {
     "sgdb_model_device_ptrs": (_S, [vp, P(vp), P(vp)]),
     "sgdb_model_free": (_S, [vp]),
     "sgdb_sync_epoch": (_S, [vp, vp, vp, i32, dbl, P(u32), u64, P(i32)]),
-    "sgdb_batch_gradient": (_S, [vp, vp, i32, P(u32), u64, P(dbl), P(dbl)]),
+    "sgdb_batch_gradient": (_S, [vp, vp, i32, P(u32), u64, P(dbl), i32, P(dbl)]),
     "sgdb_epoch_batch": (_S, [vp, vp, vp, i32, dbl, P(dbl)]),
     "sgdb_hogwild_epoch": (_S, [vp, vp, vp, i32, dbl, P(Plan), P(u64)]),
     "sgdb_hogwild_segment": (_S, [vp, vp, vp, i32, dbl, P(Plan), u32, u32, P(u64)]),

@@ -421,20 +421,45 @@ class Device:
             pass
 
 
+_DEFAULT_EXACT: Optional[bool] = None
+
+
+def set_default_precision(precision: str) -> None:
+    """'fp32' (fused fp32 kernels, the default) or 'exact' (SGDB_UPLOAD_EXACT_FP64:
+    fp64 in the reference's operation order, bit-identical results) for
+    datasets uploaded without an explicit ``exact=``. The initial default
+    comes from the SGDB_PRECISION environment variable."""
+    global _DEFAULT_EXACT
+    if precision not in ("fp32", "exact"):
+        raise ValueError("precision must be 'fp32' or 'exact'")
+    _DEFAULT_EXACT = precision == "exact"
+
+
+def default_exact() -> bool:
+    global _DEFAULT_EXACT
+    if _DEFAULT_EXACT is None:
+        import os
+        _DEFAULT_EXACT = os.environ.get("SGDB_PRECISION", "fp32") in ("exact", "fp64")
+    return _DEFAULT_EXACT
+
+
 class DeviceDataset:
-    """Device-resident dataset (fp32 storage), optionally a row shard."""
+    """Device-resident dataset (fp32 storage; plus fp64 values in the exact
+    mode), optionally a row shard."""
 
     def __init__(self, dev: Device, ds: Optional[Dataset], row_base: int = 0, n_global: int = 0,
-                 _handle=None):
+                 exact: Optional[bool] = None, _handle=None):
         self.dev = dev
         self.host = ds
+        self.exact = bool(default_exact() if exact is None else exact) if _handle is None else False
         if _handle is not None:
             self._h = _handle
         else:
             self._h = L.vp()
             v = ds.view()
-            check(_lib().sgdb_dataset_upload(dev.handle, C.byref(v), row_base, n_global,
-                                             C.byref(self._h)))
+            check(_lib().sgdb_dataset_upload_ex(dev.handle, C.byref(v), row_base, n_global,
+                                                L.SGDB_UPLOAD_EXACT_FP64 if self.exact else 0,
+                                                C.byref(self._h)))
         n, d, nnz, rb, ng = (L.u64() for _ in range(5))
         check(_lib().sgdb_dataset_shape(self._h, C.byref(n), C.byref(d), C.byref(nnz),
                                         C.byref(rb), C.byref(ng)))
@@ -686,7 +711,8 @@ class sync:  # noqa: N801 — namespace mirror of sgdbench::sync
         r = np.ascontiguousarray(rows if rows is not None else [], np.uint32)
         g = np.zeros(dds.n_features, np.float64)
         check(_lib().sgdb_batch_gradient(dds.dev.handle, dds.handle, int(task), _u32ptr(r),
-                                         r.size, _dptr(w), _dptr(g)))
+                                         r.size, _dptr(w), int(transposed is not None),
+                                         _dptr(g)))
         return g
 
     @staticmethod

@@ -325,8 +325,14 @@ sgdb_status sgdb_ctx_resident_workers(sgdb_ctx* ctx, const sgdb_dataset* ds, int
 
 sgdb_status sgdb_dataset_upload(sgdb_ctx* ctx, const sgdb_dataset_view* v, uint64_t row_base,
                                 uint64_t n_global, sgdb_dataset** out) {
+  return sgdb_dataset_upload_ex(ctx, v, row_base, n_global, 0, out);
+}
+
+sgdb_status sgdb_dataset_upload_ex(sgdb_ctx* ctx, const sgdb_dataset_view* v, uint64_t row_base,
+                                   uint64_t n_global, uint32_t flags, sgdb_dataset** out) {
   return sgdb_guard([&] {
     require(ctx && v && out, "null argument");
+    require((flags & ~uint32_t(SGDB_UPLOAD_EXACT_FP64)) == 0, "unknown upload flags");
     const uint64_t n = v->n_examples, d = v->n_features;
     require(n == 0 || v->labels != nullptr, "labels missing");
     if (n_global == 0) n_global = n;
@@ -426,6 +432,29 @@ sgdb_status sgdb_dataset_upload(sgdb_ctx* ctx, const sgdb_dataset_view* v, uint6
       }
       default:
         throw std::invalid_argument("unknown layout");
+    }
+    if (flags & SGDB_UPLOAD_EXACT_FP64) {
+      // fp64 copy aligned with the fp32 storage built above.
+      std::vector<double> v64;
+      if (v->layout == SGDB_LAYOUT_DENSE_ROW || v->layout == SGDB_LAYOUT_DENSE_COL) {
+        const bool colmajor = v->layout == SGDB_LAYOUT_DENSE_COL;
+        v64.resize(n * d);
+        for (uint64_t e = 0; e < n; ++e)
+          for (uint64_t j = 0; j < d; ++j)
+            v64[e * d + j] = colmajor ? v->values[j * n + e] : v->values[e * d + j];
+      } else if (v->layout == SGDB_LAYOUT_CSR) {
+        v64.assign(v->values, v->values + v->n_values);
+      } else {
+        const uint64_t pw = v->padded_width;
+        for (uint64_t e = 0; e < n; ++e)
+          for (uint64_t sl = 0; sl < pw; ++sl)
+            if (v->indices[sl * n + e] != d) v64.push_back(v->values[sl * n + e]);
+      }
+      DBuf<double>& dst = ds->kind == Kind::Dense ? ds->x64 : ds->val64;
+      dst.alloc(std::max<uint64_t>(1, v64.size()));
+      h2d(dst.p, v64.data(), v64.size(), s);
+      check(cudaStreamSynchronize(s), "upload sync");
+      ds->exact = true;
     }
     ds->order.alloc(std::max<uint64_t>(1, n_global));
     check(cudaStreamSynchronize(s), "upload sync");
@@ -530,6 +559,11 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
     materialize(*m);
     dense_written(*m);
     set_finite(m);
+    if (ds->exact) {
+      exact_sync_epoch(*ds, *m, task, alpha, order, std::min<uint64_t>(batch_b, ds->n));
+      if (finite_out) *finite_out = read_finite(m);
+      return;
+    }
     const bool hook = c.allreduce != nullptr;
     StepArgs a;
     a.task = task;
@@ -618,9 +652,13 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
 
 sgdb_status sgdb_batch_gradient(sgdb_ctx* ctx, sgdb_dataset* ds, int32_t task,
                                 const uint32_t* rows, uint64_t n_rows, const double* w,
-                                double* g_out) {
+                                int32_t transposed, double* g_out) {
   return sgdb_guard([&] {
     require(ctx && ds && w && g_out, "null argument");
+    if (ds->exact) {
+      exact_batch_gradient(*ds, rows, n_rows, w, task, transposed != 0, g_out);
+      return;
+    }
     Ctx& c = *ctx;
     sgdb_model tmp;
     model_init(&tmp, ctx, ds->d);
@@ -652,6 +690,15 @@ sgdb_status sgdb_epoch_batch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int
   return sgdb_guard([&] {
     require(m->d == ds->d, "model/dataset dim mismatch");
     Ctx& c = *ctx;
+    if (ds->exact) {
+      exact_epoch_batch(*ds, *m, task, alpha);
+      double sq = 0.0;
+      check(cudaMemcpyAsync(&sq, m->scal.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+            "D2H norm");
+      check(cudaStreamSynchronize(c.stream), "epoch_batch sync");
+      if (grad_norm_out) *grad_norm_out = std::sqrt(sq);
+      return;
+    }
     materialize(*m);
     dense_written(*m);
     check(cudaMemsetAsync(m->scal.p, 0, sizeof(double), c.stream), "memset norm");
@@ -708,7 +755,9 @@ sgdb_status sgdb_hogwild_segment(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m,
     if (const char* e = std::getenv("SGDB_HOGWILD_SPREAD")) a.spread = std::atoi(e) != 0;
     a.seg = seg;
     a.nseg = nseg;
-    hogwild_epoch(*ds, *m, a);
+    a.alpha_f64 = alpha;
+    if (ds->exact) exact_hogwild(*ds, *m, a);
+    else hogwild_epoch(*ds, *m, a);
     if (evals_out) {
       const bool rr = plan->access_path == SGDB_ACCESS_ROW_RR || plan->access_path == SGDB_ACCESS_COL_RR;
       *evals_out = segment_evals(ds->n, plan->workers, rr, plan->data_replication_k, seg, nseg);
@@ -738,7 +787,8 @@ sgdb_status sgdb_loss(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t ta
     require(m->d == ds->d, "model/dataset dim mismatch");
     Ctx& c = *ctx;
     materialize(*m);
-    loss_launch(*ds, *m, task);
+    if (ds->exact) exact_loss(*ds, *m, task);
+    else loss_launch(*ds, *m, task);
     call_allreduce(c, c.loss_out.p, 1, 1);
     double l = 0.0;
     check(cudaMemcpyAsync(&l, c.loss_out.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream),

@@ -124,4 +124,34 @@ __host__ __device__ __forceinline__ uint32_t round_up16(uint64_t b) {
   return static_cast<uint32_t>((b + 15) & ~uint64_t(15));
 }
 
+// Worker w's assign() list (dataset.cpp:470-503), generated on the fly:
+// base ids then k wrapped extras after the last base id. Round robin: ids
+// w, w+T, ...; chunk: [w*ceil(n/T), min((w+1)*ceil(n/T), n)).
+// (Example ids fit 32 bits: n_global <= 2^32 is enforced at upload.)
+struct WorkerList {
+  uint32_t first, step, cnt, total, last;
+};
+__device__ __forceinline__ WorkerList assign_list(uint64_t n, uint64_t T, uint64_t k, bool rr,
+                                                  uint64_t w) {
+  WorkerList l;
+  if (rr) {
+    l.cnt = w < n ? static_cast<uint32_t>((n - 1 - w) / T + 1) : 0u;
+    l.first = static_cast<uint32_t>(w);
+    l.step = static_cast<uint32_t>(T);
+  } else {
+    const uint64_t chunk = (n + T - 1) / T;
+    const uint64_t b = w * chunk, e = min(n, b + chunk);
+    l.cnt = e > b ? static_cast<uint32_t>(e - b) : 0u;
+    l.first = static_cast<uint32_t>(min(b, n));
+    l.step = 1;
+  }
+  l.total = l.cnt ? l.cnt + static_cast<uint32_t>(k) : 0u;
+  l.last = l.cnt ? l.first + (l.cnt - 1) * l.step : 0u;
+  return l;
+}
+__device__ __forceinline__ uint32_t assign_at(uint64_t n, const WorkerList& l, uint32_t i) {
+  return i < l.cnt ? l.first + i * l.step
+                   : static_cast<uint32_t>((uint64_t(l.last) + 1 + (i - l.cnt)) % n);
+}
+
 }  // namespace sgdb::dev

@@ -128,6 +128,13 @@ struct Dataset {
   // Scratch.
   DBuf<float> coef;        // per local row coefficient (sparse full batch)
   DBuf<uint32_t> order;    // n_global ids of the current epoch
+  // Exact-fp64 mode (SGDB_UPLOAD_EXACT_FP64): fp64 copies of the values and
+  // the scratch of the reference-order kernels (kernels_linalg.cu).
+  bool exact = false;
+  DBuf<double> x64;        // dense: n*d row-major
+  DBuf<double> val64;      // CSR (and wide dense): nnz, aligned with idx
+  DBuf<double> ex_a, ex_c, ex_part, ex_stack, ex_reps;
+  DBuf<int> ex_live;
 };
 
 struct Model {
@@ -203,6 +210,7 @@ struct HogwildArgs {
   uint32_t refresh = 4;  // mirror: refresh a read from L2 on every refresh-th example id
   bool spread = true;    // kernel scope: 256 B-strided model copy during the epoch
   uint32_t seg = 0, nseg = 1;  // run list positions [total*seg/nseg, total*(seg+1)/nseg)
+  double alpha_f64 = 0.0;      // exact-fp64 mode step size
 };
 int hogwild_auto_lanes(const Dataset& ds, int access);
 uint64_t hogwild_resident_workers(const Ctx& c, int lanes);
@@ -220,6 +228,18 @@ inline void dense_written(Model& m) {
 void scale_model(Model& m, double scale);
 
 uint64_t next_dataset_uid();
+
+// fp64 operator primitives and the exact-fp64 mode (kernels_linalg.cu).
+void lin_matvec(Dataset& ds, const uint32_t* rows, uint64_t nr, const double* v, double* out);
+void lin_matvec_t(Dataset& ds, const uint32_t* rows, uint64_t nr, const double* a, bool col_order,
+                  double* out);
+void exact_batch_gradient(Dataset& ds, const uint32_t* rows_host, uint64_t n_rows,
+                          const double* w_host, int task, bool transposed, double* g_host);
+void exact_sync_epoch(Dataset& ds, Model& m, int task, double alpha, const uint32_t* order,
+                      uint64_t batch_b);
+void exact_epoch_batch(Dataset& ds, Model& m, int task, double alpha);
+void exact_loss(Dataset& ds, Model& m, int task);
+void exact_hogwild(Dataset& ds, Model& m, const HogwildArgs& a);
 void build_csc(Dataset& ds);
 void build_col(Dataset& ds);
 

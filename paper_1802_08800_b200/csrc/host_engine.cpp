@@ -11,6 +11,7 @@
 // epoch hook, divergence reported in-band and the wall-clock budget checked
 // after the loss.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -224,10 +225,30 @@ Device& Device::default_device() {
   return dev;
 }
 
+namespace {
+std::atomic<int> g_precision{-1};
+}
+
+void set_default_precision(Precision p) { g_precision = static_cast<int>(p); }
+
+Precision default_precision() {
+  int p = g_precision.load();
+  if (p < 0) {
+    const char* e = std::getenv("SGDB_PRECISION");
+    p = static_cast<int>(e && (std::string(e) == "exact" || std::string(e) == "fp64")
+                             ? Precision::ExactFp64
+                             : Precision::Fp32);
+    g_precision = p;
+  }
+  return static_cast<Precision>(p);
+}
+
 DeviceDataset::DeviceDataset(Device& dev, const Dataset& ds, std::size_t row_base,
-                             std::size_t n_global) {
+                             std::size_t n_global, Precision precision) {
   const sgdb_dataset_view v = ds.view();
-  throw_status(sgdb_dataset_upload(dev.get(), &v, row_base, n_global, &ds_));
+  throw_status(sgdb_dataset_upload_ex(
+      dev.get(), &v, row_base, n_global,
+      precision == Precision::ExactFp64 ? SGDB_UPLOAD_EXACT_FP64 : 0u, &ds_));
 }
 DeviceDataset::~DeviceDataset() { sgdb_dataset_free(ds_); }
 
@@ -260,13 +281,14 @@ double dataset_loss(Task task, const Dataset& ds, std::span<const double> w) {
 namespace sync {
 
 std::vector<double> batch_gradient(Task task, const Dataset& ds, std::span<const std::uint32_t> rows,
-                                   std::span<const double> w, unsigned, const Dataset*) {
+                                   std::span<const double> w, unsigned,
+                                   const Dataset* transposed) {
   if (w.size() != ds.n_features) throw std::invalid_argument("matvec: dimension mismatch");
   Device& dev = Device::default_device();
   DeviceDataset dds(dev, ds);
   std::vector<double> g(ds.n_features, 0.0);
   throw_status(sgdb_batch_gradient(dev.get(), dds.get(), static_cast<int32_t>(task), rows.data(),
-                                   rows.size(), w.data(), g.data()));
+                                   rows.size(), w.data(), transposed != nullptr, g.data()));
   return g;
 }
 

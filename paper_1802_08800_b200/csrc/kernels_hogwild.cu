@@ -130,33 +130,11 @@ struct MirrorModel {
 
 constexpr int kU = 4;  // slots per lane per batch (U loads / gathers in flight)
 
-// Worker w's assign() list (dataset.cpp:470-503), generated on the fly:
-// base ids then k wrapped extras after the last base id.
-// (Example ids fit 32 bits: n_global <= 2^32 is enforced at upload.)
-struct WorkerList {
-  uint32_t first, step, cnt, total, last;
-};
 __device__ __forceinline__ WorkerList worker_list(const HogParams& p, uint64_t w) {
-  WorkerList l;
-  const uint64_t n = p.n;
-  if (p.rr) {
-    l.cnt = w < n ? static_cast<uint32_t>((n - 1 - w) / p.T + 1) : 0u;
-    l.first = static_cast<uint32_t>(w);
-    l.step = static_cast<uint32_t>(p.T);
-  } else {
-    const uint64_t chunk = (n + p.T - 1) / p.T;
-    const uint64_t b = w * chunk, e = min(n, b + chunk);
-    l.cnt = e > b ? static_cast<uint32_t>(e - b) : 0u;
-    l.first = static_cast<uint32_t>(min(b, n));
-    l.step = 1;
-  }
-  l.total = l.cnt ? l.cnt + static_cast<uint32_t>(p.k) : 0u;
-  l.last = l.cnt ? l.first + (l.cnt - 1) * l.step : 0u;
-  return l;
+  return assign_list(p.n, p.T, p.k, p.rr != 0, w);
 }
 __device__ __forceinline__ uint32_t list_at(const HogParams& p, const WorkerList& l, uint32_t i) {
-  return i < l.cnt ? l.first + i * l.step
-                   : static_cast<uint32_t>((uint64_t(l.last) + 1 + (i - l.cnt)) % p.n);
+  return assign_at(p.n, l, i);
 }
 
 // Example e's slots. Contiguous kinds (CSR, dense row): slots [b, bend).
