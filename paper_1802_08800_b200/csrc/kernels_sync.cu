@@ -611,8 +611,18 @@ __global__ void apply_partials_kernel(uint64_t d, uint32_t nblk, const double* _
   int bad = 0;
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
        j += (uint64_t)gridDim.x * blockDim.x) {
+    // Sum over blocks in block order; 16 loads in flight per thread (only
+    // ~d threads exist, so memory parallelism has to come from each one).
     double g = 0.0;
-    for (uint32_t b = 0; b < nblk; ++b) g += partials[static_cast<uint64_t>(b) * d + j];
+    uint32_t b = 0;
+    for (; b + 16 <= nblk; b += 16) {
+      double v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = partials[static_cast<uint64_t>(b + k) * d + j];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) g += v[k];
+    }
+    for (; b < nblk; ++b) g += partials[static_cast<uint64_t>(b) * d + j];
     if (!isfinite(g)) bad = 1;
     if (apply) {
       const double w = w64[j] - alpha * g;

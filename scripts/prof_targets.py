@@ -1,6 +1,6 @@
 """Small driver for ncu captures: runs a few epochs of one target op.
 
-    python scripts/prof_targets.py {hogwild_w8a|sync_covtype|sync_rcv1|sync_dense1000} [epochs]
+    python scripts/prof_targets.py {hogwild_w8a|sync_covtype|sync_rcv1|sync_dense1000|sync_c5} [epochs]
 """
 import os
 import sys
@@ -26,6 +26,12 @@ def main():
         for _ in range(epochs):
             flush.zero_()
             S.hogwild_epoch(dds, model, S.Task.SVM, 0.01, plan)
+    elif target == "sync_c5":
+        # C5 shape (d = 1000), device Philox generator; 2M rows = 8 GB > L2.
+        dds = S.DeviceDataset.generate_dense(dev, 2_000_000, 1000, 20250814)
+        model = S.DeviceModel(dev, 1000)
+        for _ in range(epochs):
+            S.sync_epoch(dds, model, S.Task.LR, 1e-7, None, 2_000_000)
     else:
         name = target.split("_")[1]
         if name == "covtype":
