@@ -177,17 +177,32 @@ struct Batch {
   uint32_t j[kU];
   float x[kU];
 };
-// Lane lg's U slots s0, s0+G, ... of row r (zeros past the end).
+// Lane lg's U slots s0, s0+G, ... of row r (zeros past the end). Slots
+// 1..U-1 sit behind a group-uniform branch (s0 - lg + G < len), so rows that
+// fit one slot per lane — most rows of the sparse configs — do not issue
+// their loads at all.
 template <int G, int KIND>
 __device__ __forceinline__ Batch load_batch(const HogParams& p, const Row& r, uint32_t s0,
-                                            uint32_t len) {
+                                            uint32_t len, int lg) {
   Batch bt;
+  {
+    const bool ok = s0 < len;
+    bt.j[0] = ok ? slot_index<KIND>(p, r, s0) : 0u;
+    bt.x[0] = ok ? slot_value<KIND>(p, r, s0) : 0.f;
+  }
 #pragma unroll
-  for (int u = 0; u < kU; ++u) {
-    const uint32_t s = s0 + u * G;
-    const bool ok = s < len;
-    bt.j[u] = ok ? slot_index<KIND>(p, r, s) : 0u;
-    bt.x[u] = ok ? slot_value<KIND>(p, r, s) : 0.f;
+  for (int u = 1; u < kU; ++u) {
+    bt.j[u] = 0u;
+    bt.x[u] = 0.f;
+  }
+  if (s0 - lg + G < len) {
+#pragma unroll
+    for (int u = 1; u < kU; ++u) {
+      const uint32_t s = s0 + u * G;
+      const bool ok = s < len;
+      bt.j[u] = ok ? slot_index<KIND>(p, r, s) : 0u;
+      bt.x[u] = ok ? slot_value<KIND>(p, r, s) : 0.f;
+    }
   }
   return bt;
 }
@@ -205,16 +220,21 @@ __device__ __forceinline__ void process_example(const HogParams& p, const M& m, 
   // under independent thread scheduling a lane with fewer slots could
   // otherwise run ahead into this dot product.
   __syncwarp(mask);
+  const bool wide = G < len;  // group-uniform: slots 1..U-1 of the first batch in use
   float z = 0.f;
   {
     float mv[kU];
+    mv[0] = lg < static_cast<int>(len) ? m.load(first.j[0]) : 0.f;
+    z = first.x[0] * mv[0];
+    if (wide) {
 #pragma unroll
-    for (int u = 0; u < kU; ++u) mv[u] = (lg + u * G < len) ? m.load(first.j[u]) : 0.f;
+      for (int u = 1; u < kU; ++u) mv[u] = (lg + u * G < len) ? m.load(first.j[u]) : 0.f;
 #pragma unroll
-    for (int u = 0; u < kU; ++u) z = fmaf(first.x[u], mv[u], z);
+      for (int u = 1; u < kU; ++u) z = fmaf(first.x[u], mv[u], z);
+    }
   }
   for (uint32_t s0 = lg + G * kU; s0 < len; s0 += G * kU) {
-    const Batch bt = load_batch<G, KIND>(p, r, s0, len);
+    const Batch bt = load_batch<G, KIND>(p, r, s0, len, lg);
     float mv[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) mv[u] = (s0 + u * G < len) ? m.load(bt.j[u]) : 0.f;
@@ -234,11 +254,14 @@ __device__ __forceinline__ void process_example(const HogParams& p, const M& m, 
     }
     return;
   }
+  if (lg < static_cast<int>(len)) m.add(first.j[0], -(ac * (c * first.x[0])));
+  if (wide) {
 #pragma unroll
-  for (int u = 0; u < kU; ++u)
-    if (lg + u * G < len) m.add(first.j[u], -(ac * (c * first.x[u])));
+    for (int u = 1; u < kU; ++u)
+      if (lg + u * G < len) m.add(first.j[u], -(ac * (c * first.x[u])));
+  }
   for (uint32_t s0 = lg + G * kU; s0 < len; s0 += G * kU) {
-    const Batch bt = load_batch<G, KIND>(p, r, s0, len);
+    const Batch bt = load_batch<G, KIND>(p, r, s0, len, lg);
 #pragma unroll
     for (int u = 0; u < kU; ++u)
       if (s0 + u * G < len) m.add(bt.j[u], -(ac * (c * bt.x[u])));
@@ -259,11 +282,11 @@ __device__ __forceinline__ void run_worker(const HogParams& p, const M& m, uint6
   if (lo >= hi) return;
   Row cur = make_row<KIND>(p, list_at(p, l, lo));
   Row nxt = lo + 1 < hi ? make_row<KIND>(p, list_at(p, l, lo + 1)) : cur;
-  Batch bcur = load_batch<G, KIND>(p, cur, lg, row_len<KIND>(cur));
+  Batch bcur = load_batch<G, KIND>(p, cur, lg, row_len<KIND>(cur), lg);
   for (uint32_t i = lo; i < hi; ++i) {
     Batch bnxt = bcur;
     Row after = nxt;
-    if (i + 1 < hi) bnxt = load_batch<G, KIND>(p, nxt, lg, row_len<KIND>(nxt));
+    if (i + 1 < hi) bnxt = load_batch<G, KIND>(p, nxt, lg, row_len<KIND>(nxt), lg);
     if (i + 2 < hi) after = make_row<KIND>(p, list_at(p, l, i + 2));
     process_example<G, TASK, KIND>(p, m.at(cur.e), cur, bcur, w, lg, mask);
     cur = nxt;
