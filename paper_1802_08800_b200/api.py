@@ -494,14 +494,18 @@ class DeviceDataset:
         check(_lib().sgdb_dataset_sweep_bytes(self._h, C.byref(b)))
         return int(b.value)
 
-    def refresh_f32(self, values=None, labels=None, indices=None, row_offsets32=None):
-        """Async H2D re-copy of fp32 host arrays (pinned torch tensors or numpy)."""
+    def refresh_f32(self, values=None, labels=None, indices=None, row_offsets32=None,
+                    device: Optional[Device] = None):
+        """Async H2D re-copy of fp32 host arrays (pinned torch tensors or numpy), on
+        `device`'s stream (default: the dataset's own context) — pass a context on a
+        copy stream to overlap the transfer with epochs on another buffer."""
         def p(a):
             if a is None:
                 return None
             return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
-        check(_lib().sgdb_dataset_refresh_f32(self.dev.handle, self._h, p(values), p(labels),
-                                              p(indices), p(row_offsets32)))
+        ctx = (device or self.dev).handle
+        check(_lib().sgdb_dataset_refresh_f32(ctx, self._h, p(values), p(labels), p(indices),
+                                              p(row_offsets32)))
 
     def close(self):
         if getattr(self, "_h", None):
