@@ -145,6 +145,8 @@ struct Model {
   DBuf<double> g64;      // d, gradient accumulator (kept zeroed between steps)
   DBuf<double> partials; // per-block gradient partials, deterministic full batch
   DBuf<unsigned> ticket; // [0] grad ticket
+  DBuf<double> g3;       // 3*d rotating gradient buffers of the persistent epoch (K1c)
+  DBuf<unsigned> gbar;   // grid barrier words (K1c), zero between uses
   DBuf<int> finite;      // [0] 1 while every gradient entry was finite
   DBuf<double> scal;     // [0] ||g||^2
   DBuf<float> replicas;  // Hogwild replicas, R x ld
@@ -182,6 +184,10 @@ struct StepArgs {
 // Dense, all local rows: one full-batch gradient (deterministic).
 void dense_full_step(Dataset& ds, Model& m, const StepArgs& a);
 // Dense, rows = global ids ids[0..nb) (device pointer), mini-batch gradient.
+// K1c: a whole dense mini-batch epoch (ids in ds.order, batches of B) in one
+// persistent cooperative launch; no allreduce hook. Returns false (nothing
+// launched) for shapes the per-step kernels serve better.
+bool dense_epoch(Dataset& ds, Model& m, int task, double alpha, uint64_t B);
 void dense_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb,
                       const StepArgs& a);
 // Sparse, all local rows: margin/coef pass + CSC gradient pass.

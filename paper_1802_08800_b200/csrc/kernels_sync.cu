@@ -300,6 +300,159 @@ __global__ void __launch_bounds__(32 * W) dense_batch_kernel(DenseBatchParams p)
   if (threadIdx.x == 0) *p.ticket = 0u;
 }
 
+// Barrier across a co-resident grid (cooperative launch). `count` only grows:
+// barrier k of the launch completes when it reaches k * gridDim.x, so an
+// arrival is one atomic and the wait one acquire-load poll (no reset, no
+// generation word). Thread 0 fences the block's global writes (the gradient
+// REDs, ordered before it by the __syncthreads) before arriving.
+__device__ __forceinline__ void grid_sync(unsigned* count, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(count, 1u);
+    unsigned v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+      if (v >= target) break;
+      __nanosleep(20);
+    }
+  }
+  __syncthreads();
+}
+
+// K1c: a whole dense mini-batch epoch in one persistent launch. Step s takes
+// ids order[s*B, s*B+nb): warps compute margins, coefficients and CTA partial
+// gradients as in K1b and fold them into g3[s % 3] with fp64 REDs; one grid
+// barrier; then EVERY CTA applies the identical fp64 step to its own shared
+// copy of the master model (so no second barrier), and CTA 0 clears the
+// buffer of step s+2. The next step's first rows do not depend on the model,
+// so they are loaded before the barrier. Non-finite gradients stop every CTA
+// at the same step, after its update (sync_engine.cpp:94-97).
+struct DenseEpochParams {
+  const float* x;
+  const float* y;
+  uint64_t n_local, row_base;
+  int d;
+  const uint32_t* order;
+  uint64_t n_ids, B;
+  double* g3;     // 3*d, zero on entry
+  unsigned* bar;  // arrivals (monotonic within the launch, zero on entry)
+  int* finite;
+  double* w64;
+  float* w32;
+  double alpha;
+};
+
+template <int L, int F, int TASK, int W>
+__global__ void __launch_bounds__(32 * W) dense_epoch_kernel(DenseEpochParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* w64s = reinterpret_cast<double*>(smem_raw);  // [d] master copy
+  float* red = reinterpret_cast<float*>(w64s + p.d);    // [W][d]
+  constexpr int RS = 32 / L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = lane % L, slot = lane / L, d = p.d;
+  const uint64_t gw = (uint64_t)blockIdx.x * W + warp, tw = (uint64_t)gridDim.x * W;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) w64s[j] = p.w64[j];
+  __syncthreads();
+  float wr[F];
+#pragma unroll
+  for (int k = 0; k < F; ++k) {
+    const int j = q + L * k;
+    wr[k] = j < d ? static_cast<float>(w64s[j]) : 0.f;
+  }
+  auto load_row = [&](uint64_t lo, uint64_t nb, uint64_t pb, float(&xv)[F], float& yv,
+                      bool& valid) {
+    const uint64_t pos = pb + slot;
+    valid = pos < nb;
+    uint64_t row = 0;
+    if (valid) {
+      row = static_cast<uint64_t>(p.order[lo + pos]) - p.row_base;
+      valid = row < p.n_local;
+    }
+    const float* xr = p.x + row * d;
+#pragma unroll
+    for (int k = 0; k < F; ++k) {
+      const int j = q + L * k;
+      xv[k] = (valid && j < d) ? __ldg(xr + j) : 0.f;
+    }
+    yv = valid ? __ldg(p.y + row) : 0.f;
+  };
+  const uint64_t nsteps = (p.n_ids + p.B - 1) / p.B;
+  float xn[F], yn;
+  bool vn;
+  load_row(0, min(p.B, p.n_ids), gw * RS, xn, yn, vn);
+  for (uint64_t s = 0; s < nsteps; ++s) {
+    const uint64_t lo = s * p.B, nb = min(p.B, p.n_ids - lo);
+    double* g = p.g3 + (s % 3) * static_cast<uint64_t>(d);
+    float acc[F];
+    {
+      float z = 0.f;
+#pragma unroll
+      for (int k = 0; k < F; ++k) z = fmaf(xn[k], wr[k], z);
+      z = group_sum<L>(z);
+      const float c = vn ? coef_f<TASK>(z, yn) : 0.f;
+#pragma unroll
+      for (int k = 0; k < F; ++k) acc[k] = c * xn[k];
+    }
+    for (uint64_t pb = (gw + tw) * RS; pb < nb; pb += tw * RS) {
+      float xv[F], yv;
+      bool v;
+      load_row(lo, nb, pb, xv, yv, v);
+      float z = 0.f;
+#pragma unroll
+      for (int k = 0; k < F; ++k) z = fmaf(xv[k], wr[k], z);
+      z = group_sum<L>(z);
+      const float c = v ? coef_f<TASK>(z, yv) : 0.f;
+#pragma unroll
+      for (int k = 0; k < F; ++k) acc[k] = fmaf(c, xv[k], acc[k]);
+    }
+    if (s + 1 < nsteps) load_row(lo + p.B, min(p.B, p.n_ids - lo - p.B), gw * RS, xn, yn, vn);
+#pragma unroll
+    for (int k = 0; k < F; ++k) acc[k] = cross_group_sum<L>(acc[k]);
+    if (slot == 0) {
+#pragma unroll
+      for (int k = 0; k < F; ++k) {
+        const int j = q + L * k;
+        if (j < d) red[warp * d + j] = acc[k];
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) sum += red[w * d + j];
+      if (sum != 0.0) atomicAdd(&g[j], sum);
+    }
+    grid_sync(p.bar, static_cast<unsigned>(s + 1) * gridDim.x);
+    int bad = 0;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      const double gj = __ldcg(&g[j]);
+      if (!isfinite(gj)) bad = 1;
+      w64s[j] = w64s[j] - p.alpha * gj;
+    }
+    if (blockIdx.x == 0) {
+      double* g2 = p.g3 + ((s + 2) % 3) * static_cast<uint64_t>(d);
+      for (int j = threadIdx.x; j < d; j += blockDim.x) g2[j] = 0.0;
+    }
+    bad = __syncthreads_or(bad);
+#pragma unroll
+    for (int k = 0; k < F; ++k) {
+      const int j = q + L * k;
+      wr[k] = j < d ? static_cast<float>(w64s[j]) : 0.f;
+    }
+    if (bad) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) *p.finite = 0;
+      break;
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      p.w64[j] = w64s[j];
+      p.w32[j] = static_cast<float>(w64s[j]);
+    }
+  }
+}
+
 // Lane-strided sparse dot x_row . w over slots [b, e): U slots per batch so
 // U index loads and then U independent model gathers are in flight at once.
 template <int G, bool SMEM = false>
@@ -888,6 +1041,36 @@ void launch_dense_batch_LF(Dataset& ds, Model& m, const uint32_t* ids, uint64_t 
   launched(c, "dense_batch_kernel");
 }
 
+template <int L, int F, int TASK, int W>
+void launch_dense_epoch_LFW(Dataset& ds, Model& m, uint64_t B, double alpha) {
+  Ctx& c = *ds.ctx;
+  constexpr int RS = 32 / L;
+  const int d = static_cast<int>(ds.d);
+  const size_t smem = static_cast<size_t>(d) * 8 + static_cast<size_t>(W) * d * 4;
+  auto kern = dense_epoch_kernel<L, F, TASK, W>;
+  if (smem > 48 * 1024)
+    check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)),
+          "cudaFuncSetAttribute(dense_epoch)");
+  int per_sm = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem), "occupancy");
+  const uint64_t want = (B + W * RS - 1) / (W * RS);
+  const unsigned grid = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(std::max(1, per_sm)) * c.num_sms)));
+  m.g3.alloc(3 * ds.d);
+  m.gbar.alloc(2);
+  check(cudaMemsetAsync(m.g3.p, 0, 3 * ds.d * sizeof(double), c.stream), "memset g3");
+  check(cudaMemsetAsync(m.gbar.p, 0, 2 * sizeof(unsigned), c.stream), "memset barrier");
+  DenseEpochParams p{ds.x.p, ds.labels.p, ds.n, ds.row_base, d, ds.order.p, ds.n_global, B,
+                     m.g3.p, m.gbar.p, m.finite.p, m.w64.p, m.w32.p, alpha};
+  void* args[] = {&p};
+  prof_begin(c, "dense_epoch_kernel");
+  check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(32 * W), args,
+                                    smem, c.stream),
+        "cudaLaunchCooperativeKernel(dense_epoch)");
+  launched(c, "dense_epoch_kernel");
+}
+
 template <int L, int F>
 void launch_dense_loss_LF(Dataset& ds, Model& m, int task) {
   Ctx& c = *ds.ctx;
@@ -1028,6 +1211,30 @@ void dense_full_step(Dataset& ds, Model& m, const StepArgs& a) {
     if (a.task == kTaskLR) launch_dense_full_LF<L, F, kTaskLR>(ds, m, a);
     else launch_dense_full_LF<L, F, kTaskSVM>(ds, m, a);
   });
+}
+
+bool dense_epoch(Dataset& ds, Model& m, int task, double alpha, uint64_t B) {
+  const char* e = std::getenv("SGDB_EPOCH_WARPS");
+  const int w_env = e ? std::atoi(e) : 0;
+  bool handled = true;
+  dispatch_dense(ds.d, [&]<int L, int F>() {
+    // Large batches of wide rows stream better through the per-step kernels
+    // (measured: d = 1000, B = 65536: 72 vs 86 us per step).
+    if (F > 16 && B > 16384) {
+      handled = false;
+      return;
+    }
+    // Measured (scripts/minibatch_time.py): 16 warps per CTA for F <= 8, else 8.
+    const int w = w_env ? w_env : (F <= 8 ? 16 : 8);
+    auto go = [&]<int W>() {
+      if (task == kTaskLR) launch_dense_epoch_LFW<L, F, kTaskLR, W>(ds, m, B, alpha);
+      else launch_dense_epoch_LFW<L, F, kTaskSVM, W>(ds, m, B, alpha);
+    };
+    if (w == 16) go.template operator()<16>();
+    else if (w == 32) go.template operator()<32>();
+    else go.template operator()<8>();
+  });
+  return handled;
 }
 
 void dense_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb,

@@ -171,6 +171,17 @@ def test_divergence_stops_minibatch_epoch(sgdb, dev):
     assert r.trace.diverged and len(r.trace.epochs) < 50
 
 
+def test_divergence_stops_dense_minibatch_epoch(sgdb, dev):
+    """Dense mini-batch epochs run as one persistent kernel (K1c): a non-finite
+    gradient must stop every CTA at the same step and be reported."""
+    S = sgdb
+    ds = S.fixtures.dense_classification(3000, 40, 4)
+    hp = S.Hyperparams(alpha=1e308, batch_b=64, epochs=50, task=S.Task.LR)
+    r = S.sync.train(S.Task.LR, ds, hp, 3, device=dev)
+    assert r.trace.diverged and len(r.trace.epochs) < 50
+    assert "non-finite" in r.trace.divergence_note
+
+
 def test_epoch_timing_excludes_loss_and_hook(sgdb, dev):
     """test_sync_engine.cpp:172-192: every clock read advances 0.25 s; the hook 1000 s."""
     S = sgdb
