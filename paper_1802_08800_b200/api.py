@@ -561,11 +561,13 @@ class DeviceModel:
 
 # ---- device ops (layer 1) -------------------------------------------------------------
 def sync_epoch(dds: DeviceDataset, model: DeviceModel, task: Task, alpha: float,
-               order: Optional[np.ndarray], batch_b: int) -> bool:
+               order: Optional[np.ndarray], batch_b: int, check_finite: bool = True) -> bool:
+    """One synchronous epoch. check_finite=False leaves the epoch fully
+    asynchronous on the device stream (no flag read-back; returns True)."""
     o = None if order is None else np.ascontiguousarray(order, np.uint32)
     f = L.i32(1)
     check(_lib().sgdb_sync_epoch(dds.dev.handle, dds.handle, model.handle, int(task), alpha,
-                                 _u32ptr(o), batch_b, C.byref(f)))
+                                 _u32ptr(o), batch_b, C.byref(f) if check_finite else None))
     return bool(f.value)
 
 

@@ -4,6 +4,10 @@
 // kernels_sync.cu / kernels_hogwild.cu.
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -36,6 +40,7 @@ void require(bool cond, const char* msg) {
   if (!cond) throw std::invalid_argument(msg);
 }
 
+
 template <class T>
 void h2d(T* dst, const T* src, uint64_t count, cudaStream_t s) {
   if (count) check(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
@@ -51,7 +56,8 @@ void csc_blocked_from_csr(uint64_t n, uint64_t d, const std::vector<uint32_t>& r
   const uint64_t nnz = idx.size();
   uint64_t want = std::clamp<uint64_t>((nnz * 2) / ((d + 1) * 4), 1, 16);
   want = std::max<uint64_t>(want, (n + 49151) / 49152);  // slice <= 192 KB of SMEM
-  rb = static_cast<uint32_t>(std::max<uint64_t>(1, (n + want - 1) / want));
+  // rb % 4 == 0 keeps every block's coefficient slice 16-byte aligned (bulk copies).
+  rb = static_cast<uint32_t>(std::max<uint64_t>(4, ((n + want - 1) / want + 3) & ~uint64_t(3)));
   nblk = static_cast<uint32_t>(std::max<uint64_t>(1, (n + rb - 1) / rb));
   colptr.assign(static_cast<uint64_t>(nblk) * (d + 1), 0);
   crow.resize(nnz);
@@ -96,14 +102,18 @@ void upload_csr(sgdb_dataset* ds, std::vector<uint32_t>& rowptr, std::vector<uin
   std::vector<uint16_t> crow;
   std::vector<float> cval;
   csc_blocked_from_csr(ds->n, ds->d, rowptr, idx, val, ds->csc_rb, ds->csc_nblk, colptr, crow, cval);
-  ds->cval.alloc(std::max<uint64_t>(1, ds->nnz));
-  ds->crow.alloc(std::max<uint64_t>(1, ds->nnz));
+  // +8 zeroed slack: K3v reads whole aligned 4-slot windows around a column.
+  ds->cval.alloc(ds->nnz + 8);
+  ds->crow.alloc(ds->nnz + 8);
+  ds->cval.zero(s);
+  ds->crow.zero(s);
   ds->colptr.alloc(colptr.size());
   h2d(ds->cval.p, cval.data(), ds->nnz, s);
   h2d(ds->crow.p, crow.data(), ds->nnz, s);
   h2d(ds->colptr.p, colptr.data(), colptr.size(), s);
   ds->csc_built = true;
-  ds->coef.alloc(std::max<uint64_t>(1, ds->n));
+  ds->coef.alloc(ds->n + 8);  // 16-byte slack: K3v bulk-copies whole slices
+  ds->coef.zero(s);
   check(cudaStreamSynchronize(s), "upload sync");  // host vectors die with the caller
 }
 
@@ -168,7 +178,7 @@ void validate_device_plan(const sgdb_plan& p, int layout) {
 void model_init(sgdb_model* m, Ctx* c, uint64_t d) {
   m->ctx = c;
   m->d = d;
-  m->w32.alloc(d + 1);
+  m->w32.alloc(((d + 1) + 3) & ~uint64_t(3));  // whole 16-byte groups (bulk copies)
   m->w64.alloc(std::max<uint64_t>(1, d));
   m->g64.alloc(std::max<uint64_t>(1, d));
   m->ticket.alloc(1);
@@ -803,6 +813,53 @@ sgdb_status sgdb_loss(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int32_t ta
 }
 
 }  // extern "C"
+
+namespace sgdb::dev {
+
+namespace {
+std::mutex g_cfg_mu;
+std::map<std::pair<int, const void*>, size_t> g_dyn_smem;
+std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;
+std::map<std::pair<int, const void*>, size_t> g_static_smem;
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+}  // namespace
+
+void set_max_dyn_smem(const void* kern, size_t smem, const char* what) {
+  if (smem <= 48 * 1024) return;
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  size_t& cur = g_dyn_smem[{current_device(), kern}];
+  if (smem <= cur) return;
+  check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)), what);
+  cur = smem;
+}
+
+int blocks_per_sm(const void* kern, int threads, size_t smem) {
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  const auto key = std::make_tuple(current_device(), kern, threads, smem);
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) return it->second;
+  int per_sm = 0;
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem), "occupancy");
+  g_occ[key] = per_sm;
+  return per_sm;
+}
+
+size_t static_smem_of(const void* kern) {
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  const auto key = std::make_pair(current_device(), kern);
+  auto it = g_static_smem.find(key);
+  if (it != g_static_smem.end()) return it->second;
+  cudaFuncAttributes fa{};
+  check(cudaFuncGetAttributes(&fa, kern), "cudaFuncGetAttributes");
+  g_static_smem[key] = fa.sharedSizeBytes;
+  return fa.sharedSizeBytes;
+}
+
+}  // namespace sgdb::dev
 
 namespace sgdb::dev {
 uint64_t next_dataset_uid() {

@@ -29,6 +29,21 @@ __device__ __forceinline__ float coef_f(float z, float y) {
   return m < 1.0f ? -y : 0.0f;
 }
 
+// coef_f with the fast-math exponential and division (__expf, __fdividef:
+// a few ulp) for the streaming passes, where the exact division's slow path
+// would cost more issue slots than the rest of a row. Same stable split.
+template <int TASK>
+__device__ __forceinline__ float coef_fast(float z, float y) {
+  const float m = y * z;
+  if (TASK == kTaskLR) {
+    const float u = -m;
+    const float e = __expf(-fabsf(u));
+    const float s = u <= 0.0f ? __fdividef(e, 1.0f + e) : __fdividef(1.0f, 1.0f + e);
+    return s * -y;
+  }
+  return m < 1.0f ? -y : 0.0f;
+}
+
 // Point loss in fp64 (glm.cpp:24-28, math.hpp:19-22).
 __device__ __forceinline__ double softplus_d(double u) {
   if (u > 0.0) return u + log1p(exp(-u));

@@ -86,6 +86,14 @@ inline void launched(Ctx& c, const char* what) {
   if (c.profiling && !c.recs.empty()) check(cudaEventRecord(c.recs.back().stop, c.stream), "cudaEventRecord");
 }
 
+// Launch-configuration queries cached per (device, kernel, threads, smem):
+// cudaFuncSetAttribute / cudaOccupancy* / cudaFuncGetAttributes cost host
+// microseconds each, which showed up as idle GPU time between the kernels of
+// one small epoch. Defined in capi_device.cu.
+void set_max_dyn_smem(const void* kern, size_t smem, const char* what);
+int blocks_per_sm(const void* kern, int threads, size_t smem);
+size_t static_smem_of(const void* kern);
+
 // Device storage kind chosen at upload.
 enum class Kind { Dense, Csr };
 

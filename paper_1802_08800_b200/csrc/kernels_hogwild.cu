@@ -486,7 +486,7 @@ int hogwild_auto_lanes(const Dataset& ds, int access) {
 template <class K>
 unsigned wave_grid(const Ctx& c, K kern, size_t smem, uint64_t workers, int lanes) {
   int per_sm = 0;
-  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem), "occupancy");
+  per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), 256, smem);
   const uint64_t cap = static_cast<uint64_t>(std::max(1, per_sm)) * c.num_sms;
   const uint64_t need = (workers * static_cast<uint64_t>(lanes) + 255) / 256;
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min(need, cap)));
@@ -635,9 +635,7 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
       dispatch_kind(kind, [&]<int KD>() {
         auto kern = a.task == kTaskLR ? hogwild_smem_kernel<GL, kTaskLR, KD>
                                       : hogwild_smem_kernel<GL, kTaskSVM, KD>;
-        check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(rep_bytes)),
-              "cudaFuncSetAttribute(hogwild_smem)");
+        set_max_dyn_smem(reinterpret_cast<const void*>(kern), rep_bytes, "cudaFuncSetAttribute(hogwild_smem)");
         prof_begin(c, "hogwild_smem_kernel");
         kern<<<grid, static_cast<unsigned>(threads), rep_bytes, c.stream>>>(p, m.w32.p, R);
       });

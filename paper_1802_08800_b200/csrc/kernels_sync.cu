@@ -13,6 +13,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "segstream.cuh"
 #include "device.hpp"
 
 namespace sgdb::dev {
@@ -676,6 +677,199 @@ __global__ void __launch_bounds__(256) csr_coef_vec_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// K2s: margin pass with the fp32 model staged in shared memory (d <= ~56K
+// floats). Every model gather becomes an LDS — a 32-lane random gather costs
+// a few bank wavefronts — instead of one L1 tag lookup per lane, which is
+// what bounds K2v (l1tex ~79 %, one wavefront per nonzero). The model
+// arrives by bulk copy (1-D TMA) while the first rows' windows are already
+// in flight. Each warp walks a contiguous row range; G lanes per row read
+// aligned float4/uint4 windows of 4G slots; three rows deep (windows of rows
+// i+1, i+2 and the extent of row i+3 are in flight while row i reduces).
+// ---------------------------------------------------------------------------
+// Window dot product without divergence: slots outside [b, e) get x = 0
+// (their indices are still valid model coordinates — a neighbouring row's or
+// the zero slack — so the gathers stay in bounds).
+__device__ __forceinline__ float vec_dot_masked(const VecGroup& g, uint32_t a, uint32_t b, uint32_t e,
+                                                const float* w) {
+  const int lo = static_cast<int>(b - a), hi = static_cast<int>(e - a);
+  const float x0 = (0 >= lo && 0 < hi) ? g.v.x : 0.f;
+  const float x1 = (1 >= lo && 1 < hi) ? g.v.y : 0.f;
+  const float x2 = (2 >= lo && 2 < hi) ? g.v.z : 0.f;
+  const float x3 = (3 >= lo && 3 < hi) ? g.v.w : 0.f;
+  float z = x0 * w[g.j.x];
+  z = fmaf(x1, w[g.j.y], z);
+  z = fmaf(x2, w[g.j.z], z);
+  return fmaf(x3, w[g.j.w], z);
+}
+
+// Extents of a warp's contiguous row (or column) range, cached 32 at a time:
+// lane l holds the pointer (and label) of entry r0 + 32q + l, `end` the
+// pointer after the chunk. Extents are read with shuffles, so the only
+// dependent global load left in an entry's chain is its own window.
+struct RowChunk {
+  uint32_t rp, end;
+  float y;
+};
+
+// One pipeline stage: an entry's extent and its first window.
+template <class W>
+struct Stage {
+  uint32_t b, e;
+  float y;
+  W g;
+};
+
+template <int G, int TASK, int NT>
+__global__ void __launch_bounds__(NT, 1) csr_coef_smem_kernel(
+    const float* __restrict__ val, const uint32_t* __restrict__ idx,
+    const uint32_t* __restrict__ rowptr, const float* __restrict__ y, uint32_t n,
+    const float* __restrict__ w32, uint32_t d, float* __restrict__ coef) {
+  extern __shared__ __align__(16) float ws[];
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    const uint32_t total = round_up16(uint64_t(d) * 4);  // w32 is allocated in 16-byte groups
+    mbar_arrive_expect_tx(&bar, total);
+    for (uint32_t off = 0; off < total; off += 32768)
+      bulk_g2s(reinterpret_cast<char*>(ws) + off, reinterpret_cast<const char*>(w32) + off,
+               min(32768u, total - off), &bar);
+  }
+  constexpr uint32_t RW = 32 / G;   // rows per warp step
+  constexpr uint32_t SPC = 32 / RW;  // steps per 32-row chunk
+  const int lane = threadIdx.x & 31, lg = lane % G, gi = lane / G;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t r0 = static_cast<uint32_t>(uint64_t(n) * gw / nw);
+  const uint32_t r1 = static_cast<uint32_t>(uint64_t(n) * (gw + 1) / nw);
+  const uint32_t nsteps = (r1 - r0 + RW - 1) / RW;
+  auto load_chunk = [&](uint32_t q) {
+    RowChunk ch;
+    const uint32_t row = r0 + 32 * q + lane;
+    ch.rp = rowptr[min(row, r1)];
+    ch.y = row < r1 ? y[row] : 0.f;
+    ch.end = rowptr[min(r0 + 32 * q + 32, r1)];
+    return ch;
+  };
+  // Chunks qa (the issue front) and qa+1 are loaded (and qa+2 when a chunk
+  // is only a few steps long).
+  constexpr bool kThird = SPC < 8;
+  RowChunk A = load_chunk(0), B = load_chunk(1), C;
+  if constexpr (kThird) C = load_chunk(2);
+  uint32_t qa = 0;
+  auto issue = [&](uint32_t s, Stage<VecGroup>& st) {
+    if (s / SPC != qa) {  // warp-uniform; issue steps only move forward by one
+      A = B;
+      ++qa;
+      if constexpr (kThird) {
+        B = C;
+        C = load_chunk(qa + 2);
+      } else {
+        B = load_chunk(qa + 1);
+      }
+    }
+    const uint32_t l = (s % SPC) * RW + gi;
+    st.b = __shfl_sync(0xffffffffu, A.rp, l);
+    const uint32_t nx = __shfl_sync(0xffffffffu, A.rp, (l + 1) & 31);
+    st.y = __shfl_sync(0xffffffffu, A.y, l);
+    st.e = l == 31 ? A.end : nx;
+    if (s >= nsteps) st.e = st.b;
+    const uint32_t a = (st.b & ~3u) + 4u * lg;
+    st.g = vec_group(val, idx, a < st.e ? a : 0u);
+  };
+  auto consume = [&](uint32_t k, const Stage<VecGroup>& st) {
+    const uint32_t a = (st.b & ~3u) + 4u * lg;
+    float z = vec_dot_masked(st.g, a, st.b, st.e, ws);
+    for (uint32_t aa = a + 4 * G; aa < st.e; aa += 4 * G)
+      z += vec_dot_masked(vec_group(val, idx, aa), aa, st.b, st.e, ws);
+    z = group_sum<G>(z);
+    const uint32_t r = r0 + k * RW + gi;
+    if (r < r1 && lg == 0) coef[r] = coef_f<TASK>(z, st.y);
+  };
+  Stage<VecGroup> s0, s1, s2;
+  issue(0, s0);
+  issue(1, s1);
+  __syncthreads();  // barrier initialised before anyone polls it
+  mbar_wait(&bar, 0);
+  // Unrolled by the ring size, so the stages never move between registers.
+  for (uint32_t k = 0; k < nsteps; k += 3) {
+    issue(k + 2, s2);
+    consume(k, s0);
+    if (k + 1 >= nsteps) break;
+    issue(k + 3, s0);
+    consume(k + 1, s1);
+    if (k + 2 >= nsteps) break;
+    issue(k + 4, s1);
+    consume(k + 2, s2);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2t: margin pass as a segmented warp stream (segstream.cuh): each warp
+// walks the nonzeros of a contiguous row range in 128-slot tiles regardless
+// of row lengths; the model is staged in SMEM when it fits (SMEM), else
+// gathered through L1/L2. Per-row sums are fp32, as in K2/K2v.
+// ---------------------------------------------------------------------------
+// Elements per lane per tile: 4 = one float4 + one index vector, so every
+// warp-wide load is a contiguous 512 B (E = 8 doubles L1 wavefronts per load
+// and made the kernels L1-bound; ncu l1tex 90 %).
+constexpr int kSegE = 4;
+
+template <int TASK, bool SMEM, int NT>
+__global__ void __launch_bounds__(NT, 1) csr_coef_seg_kernel(
+    const float* __restrict__ val, const uint32_t* __restrict__ idx,
+    const uint32_t* __restrict__ rowptr, const float* __restrict__ y, uint32_t n,
+    const float* __restrict__ w32, uint32_t d, float* __restrict__ coef) {
+  // Dynamic SMEM: [model (SMEM) | per-warp scratch].
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float* ws = reinterpret_cast<float*>(dsm);
+  auto* scratch = reinterpret_cast<SegScratch<float, kSegE>*>(
+      dsm + (SMEM ? round_up16(uint64_t(d) * 4) : 0u));
+  __shared__ uint64_t bar;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = lane; k < kSegE * 8; k += 32) scratch[warp].flags[k] = 0u;
+  if (SMEM && threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    const uint32_t total = round_up16(uint64_t(d) * 4);  // w32 is allocated in 16-byte groups
+    mbar_arrive_expect_tx(&bar, total);
+    for (uint32_t off = 0; off < total; off += 32768)
+      bulk_g2s(reinterpret_cast<char*>(ws) + off, reinterpret_cast<const char*>(w32) + off,
+               min(32768u, total - off), &bar);
+  }
+  __syncthreads();
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t r0 = static_cast<uint32_t>(uint64_t(n) * gw / nw);
+  const uint32_t r1 = static_cast<uint32_t>(uint64_t(n) * (gw + 1) / nw);
+  if (SMEM) mbar_wait(&bar, 0);
+  const float* w = SMEM ? ws : w32;
+  segment_stream<float, kSegE, 2, VecGroup>(
+      rowptr, y, r0, r1, [&](uint32_t a, int k) { return vec_group(val, idx, a + 4 * k); },
+      [&](const VecGroup (&g)[kSegE / 4], float* p) {
+#pragma unroll
+        for (int k = 0; k < kSegE / 4; ++k) {
+          if (SMEM) {
+            p[4 * k + 0] = g[k].v.x * w[g[k].j.x];
+            p[4 * k + 1] = g[k].v.y * w[g[k].j.y];
+            p[4 * k + 2] = g[k].v.z * w[g[k].j.z];
+            p[4 * k + 3] = g[k].v.w * w[g[k].j.w];
+          } else {
+            p[4 * k + 0] = g[k].v.x * __ldg(w + g[k].j.x);
+            p[4 * k + 1] = g[k].v.y * __ldg(w + g[k].j.y);
+            p[4 * k + 2] = g[k].v.z * __ldg(w + g[k].j.z);
+            p[4 * k + 3] = g[k].v.w * __ldg(w + g[k].j.w);
+          }
+        }
+      },
+      [&](uint32_t r, float z, float yy, bool ok) {
+        const float c = coef_fast<TASK>(z, yy);
+        if (ok) coef[r] = c;
+      },
+      scratch[warp]);
+}
+
+// ---------------------------------------------------------------------------
 // K3: g = X^T c over the row-blocked CSC. CTA (block b, column range k)
 // stages c[rows of b] in SMEM, then G lanes per column reduce
 // cval * c_smem[crow] in fp64 into partials[b][j]; K3f sums the partials over
@@ -753,6 +947,182 @@ __global__ void __launch_bounds__(1024) csc_block_kernel(
     cb = nb, ce = ne;
     nb = ab, ne = ae;
   }
+}
+
+// K3v: K3 with the coefficient slice bulk-copied (1-D TMA) into SMEM, each
+// warp walking a contiguous column range with its column pointers cached 32
+// at a time (read by shuffles), and aligned 4-slot windows (float4 values +
+// 4 packed u16 rows) two columns ahead, so no dependent load sits in a
+// column's chain except its own window. Per lane, a window's four fp32
+// products are summed in fp32 and added to the fp64 accumulator; the
+// per-(block, column) sum order is fixed, so the gradient is deterministic.
+struct CscWin {
+  float4 v;
+  uint2 r;
+};
+
+template <int G>
+__global__ void __launch_bounds__(1024, 1) csc_vec_kernel(
+    const float* __restrict__ cval, const uint16_t* __restrict__ crow,
+    const uint32_t* __restrict__ colptr, const float* __restrict__ coef, uint64_t n, uint32_t d,
+    uint32_t rb, uint32_t nblk, uint32_t cpb, double* __restrict__ partials) {
+  extern __shared__ __align__(16) float cs[];
+  __shared__ uint64_t bar;
+  const uint32_t b = blockIdx.x / cpb, k = blockIdx.x % cpb;
+  if (b >= nblk) return;
+  const uint64_t r0 = static_cast<uint64_t>(b) * rb;  // rb % 4 == 0: 16-byte aligned slice
+  const uint32_t rows = static_cast<uint32_t>(min(static_cast<uint64_t>(rb), n - r0));
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    const uint32_t total = round_up16(uint64_t(rows) * 4);  // coef carries 16-byte slack
+    mbar_arrive_expect_tx(&bar, total);
+    for (uint32_t off = 0; off < total; off += 32768)
+      bulk_g2s(reinterpret_cast<char*>(cs) + off, reinterpret_cast<const char*>(coef + r0) + off,
+               min(32768u, total - off), &bar);
+  }
+  constexpr uint32_t CW = 32 / G;   // columns per warp step
+  constexpr uint32_t SPC = 32 / CW;  // steps per 32-column chunk
+  const int lane = threadIdx.x & 31, lg = lane % G, gi = lane / G;
+  const uint32_t warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t j0 = static_cast<uint32_t>(static_cast<uint64_t>(d) * k / cpb);
+  const uint32_t j1 = static_cast<uint32_t>(static_cast<uint64_t>(d) * (k + 1) / cpb);
+  const uint32_t c0 = j0 + static_cast<uint32_t>(static_cast<uint64_t>(j1 - j0) * warp / nw);
+  const uint32_t c1 = j0 + static_cast<uint32_t>(static_cast<uint64_t>(j1 - j0) * (warp + 1) / nw);
+  const uint32_t nsteps = (c1 - c0 + CW - 1) / CW;
+  const uint32_t* cp = colptr + static_cast<uint64_t>(b) * (d + 1);
+  auto load_chunk = [&](uint32_t q) {
+    RowChunk ch;
+    ch.rp = cp[min(c0 + 32 * q + lane, c1)];
+    ch.end = cp[min(c0 + 32 * q + 32, c1)];
+    ch.y = 0.f;
+    return ch;
+  };
+  auto window = [&](uint32_t a) {
+    CscWin w;
+    w.v = __ldg(reinterpret_cast<const float4*>(cval + a));
+    w.r = __ldg(reinterpret_cast<const uint2*>(crow + a));
+    return w;
+  };
+  auto dot = [&](const CscWin& w, uint32_t a, uint32_t sb, uint32_t se) {
+    const int lo = static_cast<int>(sb - a), hi = static_cast<int>(se - a);
+    const float x0 = (0 >= lo && 0 < hi) ? w.v.x : 0.f;
+    const float x1 = (1 >= lo && 1 < hi) ? w.v.y : 0.f;
+    const float x2 = (2 >= lo && 2 < hi) ? w.v.z : 0.f;
+    const float x3 = (3 >= lo && 3 < hi) ? w.v.w : 0.f;
+    float t = x0 * cs[w.r.x & 0xffffu];
+    t = fmaf(x1, cs[w.r.x >> 16], t);
+    t = fmaf(x2, cs[w.r.y & 0xffffu], t);
+    t = fmaf(x3, cs[w.r.y >> 16], t);
+    return static_cast<double>(t);
+  };
+  constexpr bool kThird = SPC < 8;
+  RowChunk A = load_chunk(0), B = load_chunk(1), C;
+  if constexpr (kThird) C = load_chunk(2);
+  uint32_t qa = 0;
+  auto issue = [&](uint32_t s, Stage<CscWin>& st) {
+    if (s / SPC != qa) {
+      A = B;
+      ++qa;
+      if constexpr (kThird) {
+        B = C;
+        C = load_chunk(qa + 2);
+      } else {
+        B = load_chunk(qa + 1);
+      }
+    }
+    const uint32_t l = (s % SPC) * CW + gi;
+    st.b = __shfl_sync(0xffffffffu, A.rp, l);
+    const uint32_t nx = __shfl_sync(0xffffffffu, A.rp, (l + 1) & 31);
+    st.e = l == 31 ? A.end : nx;
+    if (s >= nsteps) st.e = st.b;
+    const uint32_t a = (st.b & ~3u) + 4u * lg;
+    st.g = window(a < st.e ? a : 0u);
+  };
+  auto consume = [&](uint32_t s, const Stage<CscWin>& st) {
+    const uint32_t a = (st.b & ~3u) + 4u * lg;
+    double acc = dot(st.g, a, st.b, st.e);
+    for (uint32_t aa = a + 4 * G; aa < st.e; aa += 4 * G) acc += dot(window(aa), aa, st.b, st.e);
+    acc = group_sum<G>(acc);
+    const uint32_t j = c0 + s * CW + gi;
+    if (j < c1 && lg == 0) partials[static_cast<uint64_t>(b) * d + j] = acc;
+  };
+  Stage<CscWin> s0, s1, s2;
+  issue(0, s0);
+  issue(1, s1);
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  for (uint32_t s = 0; s < nsteps; s += 3) {
+    issue(s + 2, s2);
+    consume(s, s0);
+    if (s + 1 >= nsteps) break;
+    issue(s + 3, s0);
+    consume(s + 1, s1);
+    if (s + 2 >= nsteps) break;
+    issue(s + 4, s1);
+    consume(s + 2, s2);
+  }
+}
+
+// K3t: the gradient pass over the blocked CSC as a segmented warp stream:
+// CTA (block b, column range k) stages c[rows of b] in SMEM by bulk copy;
+// each warp streams the nonzeros of a contiguous column range (columns are
+// segments) in 128-slot tiles; fp32 products, fp64 segment sums.
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) csc_seg_kernel(
+    const float* __restrict__ cval, const uint16_t* __restrict__ crow,
+    const uint32_t* __restrict__ colptr, const float* __restrict__ coef, uint64_t n, uint32_t d,
+    uint32_t rb, uint32_t nblk, uint32_t cpb, double* __restrict__ partials) {
+  // Dynamic SMEM: [coefficient slice | per-warp scratch].
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float* cs = reinterpret_cast<float*>(dsm);
+  auto* scratch = reinterpret_cast<SegScratch<double, kSegE>*>(dsm + round_up16(uint64_t(rb) * 4));
+  __shared__ uint64_t bar;
+  const uint32_t b = blockIdx.x / cpb, k = blockIdx.x % cpb;
+  if (b >= nblk) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int q = lane; q < kSegE * 8; q += 32) scratch[warp].flags[q] = 0u;
+  const uint64_t r0 = static_cast<uint64_t>(b) * rb;  // rb % 4 == 0: 16-byte aligned slice
+  const uint32_t rows = static_cast<uint32_t>(min(static_cast<uint64_t>(rb), n - r0));
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    const uint32_t total = round_up16(uint64_t(rows) * 4);  // coef carries 16-byte slack
+    mbar_arrive_expect_tx(&bar, total);
+    for (uint32_t off = 0; off < total; off += 32768)
+      bulk_g2s(reinterpret_cast<char*>(cs) + off, reinterpret_cast<const char*>(coef + r0) + off,
+               min(32768u, total - off), &bar);
+  }
+  __syncthreads();
+  const uint32_t nw = blockDim.x >> 5;
+  const uint32_t j0 = static_cast<uint32_t>(static_cast<uint64_t>(d) * k / cpb);
+  const uint32_t j1 = static_cast<uint32_t>(static_cast<uint64_t>(d) * (k + 1) / cpb);
+  const uint32_t c0 = j0 + static_cast<uint32_t>(static_cast<uint64_t>(j1 - j0) * warp / nw);
+  const uint32_t c1 = j0 + static_cast<uint32_t>(static_cast<uint64_t>(j1 - j0) * (warp + 1) / nw);
+  const uint32_t* cp = colptr + static_cast<uint64_t>(b) * (d + 1);
+  double* out = partials + static_cast<uint64_t>(b) * d;
+  mbar_wait(&bar, 0);
+  segment_stream<double, kSegE, 2, CscWin>(
+      cp, nullptr, c0, c1,
+      [&](uint32_t a, int q) {
+        CscWin w;
+        w.v = __ldg(reinterpret_cast<const float4*>(cval + a + 4 * q));
+        w.r = __ldg(reinterpret_cast<const uint2*>(crow + a + 4 * q));
+        return w;
+      },
+      [&](const CscWin (&w)[kSegE / 4], float* p) {
+#pragma unroll
+        for (int q = 0; q < kSegE / 4; ++q) {
+          p[4 * q + 0] = w[q].v.x * cs[w[q].r.x & 0xffffu];
+          p[4 * q + 1] = w[q].v.y * cs[w[q].r.x >> 16];
+          p[4 * q + 2] = w[q].v.z * cs[w[q].r.y & 0xffffu];
+          p[4 * q + 3] = w[q].v.w * cs[w[q].r.y >> 16];
+        }
+      },
+      [&](uint32_t j, double v, float, bool ok) {
+        if (ok) out[j] = v;
+      },
+      scratch[warp]);
 }
 
 // K3f: g_j = sum_b partials[b][j] (fixed order), fused w -= alpha*g_j (one
@@ -1010,9 +1380,7 @@ void launch_dense_full_LF(Dataset& ds, Model& m, const StepArgs& a) {
   p.tail = GradTail{m.partials.p, m.ticket.p, d, a.alpha, a.apply ? 1 : 0, a.want_norm ? 1 : 0,
                     m.w64.p, m.w32.p, m.g64.p, m.finite.p, m.scal.p};
   auto kern = dense_full_kernel<L, F, TASK, WC>;
-  check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem)),
-        "cudaFuncSetAttribute(dense_full)");
+  set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(dense_full)");
   prof_begin(c, "dense_full_kernel");
   kern<<<grid, 32 * (WC + 1), smem, c.stream>>>(p);
   launched(c, "dense_full_kernel");
@@ -1033,9 +1401,7 @@ void launch_dense_batch_LF(Dataset& ds, Model& m, const uint32_t* ids, uint64_t 
   const size_t smem = static_cast<size_t>(W) * d * 4;
   auto kern = dense_batch_kernel<L, F, TASK, W>;
   if (smem > 48 * 1024)
-    check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)),
-          "cudaFuncSetAttribute(dense_batch)");
+    set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(dense_batch)");
   prof_begin(c, "dense_batch_kernel");
   kern<<<grid, 32 * W, smem, c.stream>>>(p);
   launched(c, "dense_batch_kernel");
@@ -1049,11 +1415,9 @@ void launch_dense_epoch_LFW(Dataset& ds, Model& m, uint64_t B, double alpha) {
   const size_t smem = static_cast<size_t>(d) * 8 + static_cast<size_t>(W) * d * 4;
   auto kern = dense_epoch_kernel<L, F, TASK, W>;
   if (smem > 48 * 1024)
-    check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)),
-          "cudaFuncSetAttribute(dense_epoch)");
+    set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(dense_epoch)");
   int per_sm = 0;
-  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem), "occupancy");
+  per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), 32 * W, smem);
   const uint64_t want = (B + W * RS - 1) / (W * RS);
   const unsigned grid = static_cast<unsigned>(
       std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(std::max(1, per_sm)) * c.num_sms)));
@@ -1113,10 +1477,9 @@ void launch_csr_coef_pipe_G(Dataset& ds, Model& m) {
   const int threads = SMEM ? 1024 : 256;
   auto kern = csr_coef_pipe_kernel<G, TASK, SMEM>;
   if (smem > 48 * 1024)
-    check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-          "cudaFuncSetAttribute(csr_coef_pipe)");
+    set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(csr_coef_pipe)");
   int per_sm = 0;
-  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem), "occupancy");
+  per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), threads, smem);
   const uint64_t want = (ds.n * G + threads - 1) / threads;
   const unsigned grid = static_cast<unsigned>(
       std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(std::max(1, per_sm)) * c.num_sms)));
@@ -1131,7 +1494,7 @@ void launch_csr_coef_vec(Dataset& ds, Model& m) {
   Ctx& c = *ds.ctx;
   auto kern = csr_coef_vec_kernel<TASK>;
   int per_sm = 0;
-  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0), "occupancy");
+  per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), 256, 0);
   const uint64_t want = (ds.n * 32 + 255) / 256;
   const unsigned grid = static_cast<unsigned>(
       std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(std::max(1, per_sm)) * c.num_sms)));
@@ -1140,16 +1503,48 @@ void launch_csr_coef_vec(Dataset& ds, Model& m) {
   launched(c, "csr_coef_kernel");
 }
 
+template <int G, int TASK, int NT>
+void launch_csr_coef_smem_GN(Dataset& ds, Model& m) {
+  constexpr uint32_t kCoefSmemThreads = NT;
+  Ctx& c = *ds.ctx;
+  const size_t smem = round_up16(ds.d * sizeof(float));
+  auto kern = csr_coef_smem_kernel<G, TASK, NT>;
+  set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(csr_coef_smem)");
+  int per_sm = 0;
+  per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kCoefSmemThreads, smem);
+  const uint64_t want = (ds.n * G + kCoefSmemThreads - 1) / kCoefSmemThreads;
+  const unsigned grid = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(std::max(1, per_sm)) * c.num_sms)));
+  prof_begin(c, "csr_coef_kernel");
+  kern<<<grid, kCoefSmemThreads, smem, c.stream>>>(ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p,
+                                                   static_cast<uint32_t>(ds.n), m.w32.p,
+                                                   static_cast<uint32_t>(ds.d), ds.coef.p);
+  launched(c, "csr_coef_kernel");
+}
+
+// CTA size: the model copy limits SMEM to one CTA per SM for large d, so the
+// thread count trades resident warps against registers per thread
+// (SGDB_COEF_THREADS = 1024 | 768 | 512; measured in scripts/sync_sweep.py).
+template <int G, int TASK>
+void launch_csr_coef_smem_G(Dataset& ds, Model& m) {
+  static const int nt = [] {
+    const char* e = std::getenv("SGDB_COEF_THREADS");
+    return e ? std::atoi(e) : 768;
+  }();
+  if (nt == 1024) launch_csr_coef_smem_GN<G, TASK, 1024>(ds, m);
+  else if (nt == 512) launch_csr_coef_smem_GN<G, TASK, 512>(ds, m);
+  else launch_csr_coef_smem_GN<G, TASK, 768>(ds, m);
+}
+
 template <int G>
 void launch_csc_block_G(Dataset& ds, Model& m) {
   Ctx& c = *ds.ctx;
   const size_t smem = static_cast<size_t>(ds.csc_rb) * sizeof(float);
   auto kern = csc_block_kernel<G>;
   if (smem > 48 * 1024)
-    check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-          "cudaFuncSetAttribute(csc_block)");
+    set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(csc_block)");
   int per_sm = 0;
-  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, smem), "occupancy");
+  per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), 1024, smem);
   const uint32_t slots = static_cast<uint32_t>(std::max(1, per_sm) * c.num_sms);
   const uint32_t cpb = std::max<uint32_t>(1, slots / ds.csc_nblk);
   m.partials.alloc(static_cast<uint64_t>(ds.csc_nblk) * ds.d);
@@ -1160,9 +1555,107 @@ void launch_csc_block_G(Dataset& ds, Model& m) {
   launched(c, "csc_grad_kernel");
 }
 
+template <int G>
+void launch_csc_vec_G(Dataset& ds, Model& m) {
+  Ctx& c = *ds.ctx;
+  const size_t smem = round_up16(static_cast<uint64_t>(ds.csc_rb) * sizeof(float));
+  auto kern = csc_vec_kernel<G>;
+  set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(csc_vec)");
+  int per_sm = 0;
+  per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), 1024, smem);
+  const uint32_t slots = static_cast<uint32_t>(std::max(1, per_sm) * c.num_sms);
+  const uint32_t cpb = std::max<uint32_t>(1, slots / ds.csc_nblk);
+  m.partials.alloc(static_cast<uint64_t>(ds.csc_nblk) * ds.d);
+  prof_begin(c, "csc_grad_kernel");
+  kern<<<cpb * ds.csc_nblk, 1024, smem, c.stream>>>(ds.cval.p, ds.crow.p, ds.colptr.p, ds.coef.p, ds.n,
+                                                    static_cast<uint32_t>(ds.d), ds.csc_rb,
+                                                    ds.csc_nblk, cpb, m.partials.p);
+  launched(c, "csc_grad_kernel");
+}
+
+template <int TASK, bool SMEM, int NT>
+bool launch_csr_coef_seg_N(Dataset& ds, Model& m) {
+  Ctx& c = *ds.ctx;
+  const size_t smem = (SMEM ? round_up16(ds.d * sizeof(float)) : 0) +
+                      (NT / 32) * sizeof(SegScratch<float, kSegE>);
+  auto kern = csr_coef_seg_kernel<TASK, SMEM, NT>;
+  const size_t static_smem = static_smem_of(reinterpret_cast<const void*>(kern));
+  if (static_smem + smem > c.max_smem_optin) return false;  // try fewer threads
+  if (smem > 48 * 1024)
+    set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(csr_coef_seg)");
+  int per_sm = 0;
+  per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), NT, smem);
+  if (per_sm < 1) return false;
+  // ~2 tiles per warp at least keeps short inputs spread out.
+  const uint64_t want = std::max<uint64_t>(1, (ds.nnz / 512 + NT / 32 - 1) / (NT / 32));
+  const unsigned grid = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(per_sm) * c.num_sms)));
+  prof_begin(c, "csr_coef_kernel");
+  kern<<<grid, NT, smem, c.stream>>>(ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p,
+                                     static_cast<uint32_t>(ds.n), m.w32.p,
+                                     static_cast<uint32_t>(ds.d), ds.coef.p);
+  launched(c, "csr_coef_kernel");
+  return true;
+}
+
+template <int NT>
+bool launch_csc_seg_N(Dataset& ds, Model& m) {
+  Ctx& c = *ds.ctx;
+  const size_t smem = round_up16(static_cast<uint64_t>(ds.csc_rb) * sizeof(float)) +
+                      (NT / 32) * sizeof(SegScratch<double, kSegE>);
+  auto kern = csc_seg_kernel<NT>;
+  const size_t static_smem = static_smem_of(reinterpret_cast<const void*>(kern));
+  if (static_smem + smem > c.max_smem_optin) return false;
+  set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(csc_seg)");
+  int per_sm = 0;
+  per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), NT, smem);
+  if (per_sm < 1) return false;
+  const uint32_t slots = static_cast<uint32_t>(per_sm * c.num_sms);
+  const uint32_t cpb = std::max<uint32_t>(1, slots / ds.csc_nblk);
+  m.partials.alloc(static_cast<uint64_t>(ds.csc_nblk) * ds.d);
+  prof_begin(c, "csc_grad_kernel");
+  kern<<<cpb * ds.csc_nblk, NT, smem, c.stream>>>(ds.cval.p, ds.crow.p, ds.colptr.p, ds.coef.p, ds.n,
+                                                  static_cast<uint32_t>(ds.d), ds.csc_rb,
+                                                  ds.csc_nblk, cpb, m.partials.p);
+  launched(c, "csc_grad_kernel");
+  return true;
+}
+
+// CTA size: the largest of 1024 / 768 / 512 threads whose per-warp scratch
+// fits next to the staged model (or coefficient slice); SGDB_SEG_THREADS
+// caps it for A/B runs.
+int seg_threads() {
+  static const int nt = [] {
+    const char* e = std::getenv("SGDB_SEG_THREADS");
+    return e ? std::atoi(e) : 1024;
+  }();
+  return nt;
+}
+
+template <int TASK>
+void launch_csr_coef_seg(Dataset& ds, Model& m, bool smem_model) {
+  const int nt = seg_threads();
+  auto go = [&]<bool SM>() {
+    if (nt >= 1024 && launch_csr_coef_seg_N<TASK, SM, 1024>(ds, m)) return true;
+    if (nt >= 768 && launch_csr_coef_seg_N<TASK, SM, 768>(ds, m)) return true;
+    return launch_csr_coef_seg_N<TASK, SM, 512>(ds, m);
+  };
+  if (smem_model && go.template operator()<true>()) return;
+  if (!go.template operator()<false>()) throw CudaError("csr_coef_seg: no launchable configuration");
+}
+
+void launch_csc_seg(Dataset& ds, Model& m) {
+  const int nt = seg_threads();
+  if (nt >= 1024 && launch_csc_seg_N<1024>(ds, m)) return;
+  if (nt >= 768 && launch_csc_seg_N<768>(ds, m)) return;
+  if (!launch_csc_seg_N<512>(ds, m)) throw CudaError("csc_seg: no launchable configuration");
+}
+
 void launch_apply_partials(Dataset& ds, Model& m, const StepArgs& a) {
   Ctx& c = *ds.ctx;
-  const unsigned grid = grid_for(c, 256ull * 4, ds.d, 8);
+  // One coordinate per thread: each thread's 16-deep load batch is the only
+  // memory parallelism this d-sized pass has.
+  const unsigned grid = grid_for(c, 256, ds.d, 16);
   prof_begin(c, "apply_partials_kernel");
   apply_partials_kernel<<<grid, 256, 0, c.stream>>>(ds.d, ds.csc_nblk, m.partials.p, a.alpha,
                                                     a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p,
@@ -1253,14 +1746,33 @@ void csr_full_step(Dataset& ds, Model& m, const StepArgs& a) {
     // rcv1 because one 189 KB CTA per SM halves the resident warps.
     static const bool smem_pref = [] {
       const char* e = std::getenv("SGDB_COEF_SMEM");
-      return e && std::atoi(e) != 0;
+      return e && std::atoi(e) == 1;
     }();
     const bool smem_model = smem_pref && ds.d * sizeof(float) <= 192 * 1024;
     static const bool vec_pref = [] {
       const char* e = std::getenv("SGDB_ROW_VEC");
       return !e || std::atoi(e) != 0;
     }();
-    if (g == 32 && vec_pref && !smem_model) {
+    // Model staged in SMEM with vector windows (K2s) whenever it fits
+    // (SGDB_COEF_SMEM=0 disables it for A/B runs).
+    static const int smem_env = [] {
+      const char* e = std::getenv("SGDB_COEF_SMEM");
+      return e ? std::atoi(e) : 2;
+    }();
+    static const bool seg = [] {
+      const char* e = std::getenv("SGDB_SEG");
+      return !e || std::atoi(e) != 0;
+    }();
+    const bool fits = round_up16(ds.d * sizeof(float)) + 8192 <= ds.ctx->max_smem_optin;
+    if (seg) {
+      if (a.task == kTaskLR) launch_csr_coef_seg<kTaskLR>(ds, m, fits && smem_env != 0);
+      else launch_csr_coef_seg<kTaskSVM>(ds, m, fits && smem_env != 0);
+    } else if (smem_env == 2 && fits) {
+      dispatch_G(g, [&]<int G>() {
+        if (a.task == kTaskLR) launch_csr_coef_smem_G<G, kTaskLR>(ds, m);
+        else launch_csr_coef_smem_G<G, kTaskSVM>(ds, m);
+      });
+    } else if (g == 32 && vec_pref && !smem_model) {
       if (a.task == kTaskLR) launch_csr_coef_vec<kTaskLR>(ds, m);
       else launch_csr_coef_vec<kTaskSVM>(ds, m);
     } else dispatch_G(g, [&]<int G>() {
@@ -1278,7 +1790,31 @@ void csr_full_step(Dataset& ds, Model& m, const StepArgs& a) {
   // Column segments: narrow groups amortise the per-column reduction over
   // more columns per warp (measured: rcv1 8 lanes, news20/real-sim 4).
   const int gc = per_col <= 16.0 ? 4 : (per_col <= 128.0 ? 8 : 16);
-  dispatch_G(env_lanes("SGDB_COL_LANES", gc), [&]<int G>() { launch_csc_block_G<G>(ds, m); });
+  static const bool csc_vec = [] {
+    const char* e = std::getenv("SGDB_CSC_VEC");
+    return !e || std::atoi(e) != 0;
+  }();
+  // SGDB_CSC: 0 = K3, 1 = K3v, 2 = K3t, unset = by column length. Measured
+  // (profiles/round1_sync_kernels_ab.jsonl): the segmented stream wins when
+  // columns are a few slots long (news20: 72 vs 84 us), K3v with 8-lane
+  // groups when they run to tens of slots (rcv1: 82 vs 125-143 us).
+  static const int csc_mode = [] {
+    const char* e = std::getenv("SGDB_CSC");
+    if (e) return std::atoi(e);
+    const char* v = std::getenv("SGDB_CSC_VEC");
+    return v && std::atoi(v) == 0 ? 0 : -1;
+  }();
+  const bool aligned = ds.csc_rb % 4 == 0;
+  const int mode = !aligned ? 0 : (csc_mode >= 0 ? csc_mode : (per_col < 12.0 ? 2 : 1));
+  if (mode == 2) {
+    launch_csc_seg(ds, m);
+  } else if (mode == 1) {
+    // 4-slot windows: one window per lane group covers 4G slots of a column.
+    const int gv = per_col <= 24.0 ? 4 : 8;
+    dispatch_G(env_lanes("SGDB_COL_LANES", gv), [&]<int G>() { launch_csc_vec_G<G>(ds, m); });
+  } else {
+    dispatch_G(env_lanes("SGDB_COL_LANES", gc), [&]<int G>() { launch_csc_block_G<G>(ds, m); });
+  }
   launch_apply_partials(ds, m, a);
 }
 

@@ -1,0 +1,79 @@
+"""Edge cases of the full-batch sparse passes (segmented warp stream, K2t/K3t).
+
+The margin pass and the blocked-CSC gradient pass walk each warp's nonzeros
+in 128-slot tiles and recover per-row / per-column sums with a segmented warp
+scan (paper_1802_08800_b200/csrc/segstream.cuh). These inputs put segment
+boundaries where that bookkeeping can go wrong: empty rows (single, in runs
+longer than the 32-entry pointer chunk, leading and trailing), one-slot rows,
+more rows in one tile than a chunk holds, rows spanning many tiles, and a
+model too wide to stage in shared memory. Full-batch gradients are compared
+with the CPU oracle (proj/src/sync_engine.cpp:22-42 restated) at the sync
+tolerance of DESIGN.md §Numerics.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _csr(S, lengths, d, seed):
+    rng = np.random.default_rng(seed)
+    rows, idx, val = [0], [], []
+    for ln in lengths:
+        cols = np.sort(rng.choice(d, size=ln, replace=False)) if ln else np.zeros(0, np.int64)
+        idx.extend(cols.tolist())
+        val.extend(rng.uniform(-1, 1, ln).astype(np.float32).astype(np.float64).tolist())
+        rows.append(rows[-1] + ln)
+    n = len(lengths)
+    y = np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    return S.Dataset(n, d, S.Layout.Csr, labels=y, values=np.array(val, np.float64),
+                     indices=np.array(idx, np.uint32), row_offsets=np.array(rows, np.uint64))
+
+
+def _shapes():
+    rng = np.random.default_rng(3)
+    out = {}
+    out["empty_runs"] = [0] * 40 + [5, 0, 0, 3] + [0] * 70 + [1] * 100 + [0] * 33
+    out["one_slot_rows"] = [1] * 3000
+    out["mixed_pareto"] = np.minimum(
+        (rng.pareto(2.0, 5000) + 1) * 6, 900).astype(int).tolist()
+    out["long_rows"] = [700, 0, 1300, 2, 129, 128, 127, 0, 511, 513] * 5
+    out["tiny_n"] = [3, 0, 7]
+    out["single_row"] = [37]
+    out["many_short"] = rng.integers(0, 4, 20000).tolist()
+    return out
+
+
+SHAPES = _shapes()
+
+
+@pytest.mark.parametrize("name", sorted(SHAPES))
+@pytest.mark.parametrize("d", [600, 100_000])
+def test_full_batch_gradient_segments(sgdb, dev, orc, name, d):
+    S = sgdb
+    lengths = [min(ln, d) for ln in SHAPES[name]]
+    ds = _csr(S, lengths, d, seed=len(lengths) + d)
+    rng = np.random.default_rng(1)
+    w = rng.normal(0, 0.5, d)
+    for task in (0, 1):
+        g = S.sync.batch_gradient(S.Task(task), ds, None, w, device=dev)
+        og = orc.batch_gradient(ds, task, None, w)
+        if np.linalg.norm(og) == 0.0:
+            assert np.linalg.norm(g) == 0.0
+        else:
+            assert rel_l2(g, og) <= 1e-5, (name, d, task, rel_l2(g, og))
+
+
+@pytest.mark.parametrize("name", ["mixed_pareto", "empty_runs", "long_rows"])
+def test_full_batch_epochs_segments(sgdb, dev, orc, name):
+    """Several B = N epochs (margin pass reads the updated model each time)."""
+    S = sgdb
+    ds = _csr(S, SHAPES[name], 3000, seed=5)
+    dds = S.DeviceDataset(dev, ds)
+    model = S.DeviceModel(dev, ds.n_features)
+    om, ol, _ = orc.sync_train(ds, 0, 0.05, ds.n_examples, 4, 7)
+    for e in range(4):
+        assert S.sync_epoch(dds, model, S.Task.LR, 0.05, None, ds.n_examples)
+        assert rel_l2(model.get(), om[e]) <= 1e-5
