@@ -426,19 +426,42 @@ def extra_c5(S, dev, world, rank, rows_per_gpu, barrier):
     return out
 
 
+def _time_hogwild(S, dds, model, task, alpha, plan, epochs, warmup, flush):
+    import torch
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        S.hogwild_epoch(dds, model, task, alpha, plan)
+    evs = []
+    for _ in range(epochs):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        S.hogwild_epoch(dds, model, task, alpha, plan)
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    return float(np.mean([x.elapsed_time(y) for x, y in evs]))
+
+
 def extra_sync_shapes(S, dev):
-    """Full-batch synchronous epochs on the other BASELINE shapes."""
+    """Full-batch synchronous epochs on the other BASELINE shapes,
+    and Hogwild epochs with the paper's plan for the shapes BASELINE.json runs
+    asynchronously (C3, C4a, C4b; kernel scope, every resident warp a worker)."""
     import torch
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     shapes = {
-        "C1_covtype_lr": (lambda: S.fixtures.dense_classification(581012, 54, 20250810), S.Task.LR, 1e-6),
-        "C3_rcv1_lr": (lambda: S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813), S.Task.LR, 1e-6),
-        "C4a_news20_svm": (lambda: S.fixtures.sparse_classification(19996, 1355191, 455.0, 20250814), S.Task.SVM, 1e-5),
-        "C4b_realsim_svm": (lambda: S.fixtures.sparse_classification(72309, 20958, 51.3, 20250812), S.Task.SVM, 1e-5),
+        "C1_covtype_lr": (lambda: S.fixtures.dense_classification(581012, 54, 20250810), S.Task.LR, 1e-6,
+                          None, None),
+        "C3_rcv1_lr": (lambda: S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813), S.Task.LR, 1e-6,
+                       "row-ch:kernel:0", 1e-2),
+        "C4a_news20_svm": (lambda: S.fixtures.sparse_classification(19996, 1355191, 455.0, 20250814), S.Task.SVM, 1e-5,
+                           "row-ch:kernel:0", 1e-4),
+        "C4b_realsim_svm": (lambda: S.fixtures.sparse_classification(72309, 20958, 51.3, 20250812), S.Task.SVM, 1e-5,
+                            "row-ch:kernel:0", 1e-3),
     }
     peak, _ = _peaks()
     out = {}
-    for name, (make, task, alpha) in shapes.items():
+    for name, (make, task, alpha, plan_text, async_alpha) in shapes.items():
         host = make()
         dds = S.DeviceDataset(dev, host)
         model = S.DeviceModel(dev, host.n_features)
@@ -447,6 +470,18 @@ def extra_sync_shapes(S, dev):
         out[name] = {"n": host.n_examples, "d": host.n_features, "epoch_ms": ms,
                      "value": host.n_examples / (ms / 1e3), "unit": UNIT,
                      "alg_GBps": sweep / (ms / 1e3) / 1e9, "frac": sweep / (ms / 1e3) / 1e9 / peak}
+        if plan_text:
+            plan = S.parse_plan(plan_text)
+            plan.workers = dev.resident_workers(dds)
+            hm = S.DeviceModel(dev, host.n_features)
+            ams = _time_hogwild(S, dds, hm, task, async_alpha, plan, 5, 2, flush)
+            out[name]["hogwild"] = {
+                "plan": plan_text, "workers": plan.workers, "epoch_ms": ams,
+                "value": host.n_examples / (ams / 1e3), "unit": UNIT,
+                "alg_GBps": sweep / (ams / 1e3) / 1e9, "frac": sweep / (ams / 1e3) / 1e9 / peak,
+                "note": "bound by L2 transactions (one model gather + one red.add per nonzero) and "
+                        "the per-example gather chain, not HBM (DESIGN.md §4)"}
+            del hm
         del dds, model, host
     return out
 

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(32 * (WC + 1), 1) dense_full_kernel(DenseFullP
           z = fmaf(xv[k], wr[k], z);
         }
         z = group_sum<L>(z);
-        const float c = valid ? coef_f<TASK>(z, ys[r]) : 0.f;
+        const float c = valid ? coef_fast<TASK>(z, ys[r]) : 0.f;
 #pragma unroll
         for (int k = 0; k < F; ++k) acc[k] = fmaf(c, xv[k], acc[k]);
       }
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(32 * W) dense_epoch_kernel(DenseEpochParams p)
 #pragma unroll
       for (int k = 0; k < F; ++k) z = fmaf(xn[k], wr[k], z);
       z = group_sum<L>(z);
-      const float c = vn ? coef_f<TASK>(z, yn) : 0.f;
+      const float c = vn ? coef_fast<TASK>(z, yn) : 0.f;
 #pragma unroll
       for (int k = 0; k < F; ++k) acc[k] = c * xn[k];
     }
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(32 * W) dense_epoch_kernel(DenseEpochParams p)
 #pragma unroll
       for (int k = 0; k < F; ++k) z = fmaf(xv[k], wr[k], z);
       z = group_sum<L>(z);
-      const float c = v ? coef_f<TASK>(z, yv) : 0.f;
+      const float c = v ? coef_fast<TASK>(z, yv) : 0.f;
 #pragma unroll
       for (int k = 0; k < F; ++k) acc[k] = fmaf(c, xv[k], acc[k]);
     }
@@ -1357,7 +1357,11 @@ void launch_dense_full_LF(Dataset& ds, Model& m, const StepArgs& a) {
   // Rows per tile: ~32 KB, a multiple of the rows all consumer warps take per
   // pass (balanced warps) and of 4 (16-byte bulk-copy granularity).
   const int unit = std::max(4, WC * RS);
-  int R = std::max(unit, ((32768 / row_bytes) / unit) * unit);
+  static const int tile_bytes = [] {
+    const char* e = std::getenv("SGDB_DENSE_TILE");
+    return e ? std::atoi(e) : 32768;
+  }();
+  int R = std::max(unit, ((tile_bytes / row_bytes) / unit) * unit);
   R = (R + 3) & ~3;
   DenseFullParams p{};
   p.x = ds.x.p;
