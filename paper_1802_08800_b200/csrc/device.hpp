@@ -133,6 +133,12 @@ struct Dataset {
   std::vector<uint32_t> h_idx;
   std::vector<uint32_t> h_rowptr;
   std::vector<float> h_xcol;
+  // Example-scope Hogwild replicas (async_engine.cpp:266-290): one fp32 copy
+  // of the model at every stored slot (aligned with val/idx), plus the
+  // per-example claim / ready epoch words of ensure_replica (:333-344).
+  DBuf<float> ex_rep;
+  DBuf<unsigned> ex_claim, ex_ready;
+  unsigned ex_epoch = 0;
   // Scratch.
   DBuf<float> coef;        // per local row coefficient (sparse full batch)
   DBuf<uint32_t> order;    // n_global ids of the current epoch

@@ -295,6 +295,85 @@ __device__ __forceinline__ void run_worker(const HogParams& p, const M& m, uint6
   }
 }
 
+// K5x: example-scope replication (ModelReplication::Example,
+// async_engine.cpp:346-370). Every example owns a replica of the model
+// restricted to its support, stored at its slots (rep[s] for s in the row's
+// CSR range). The first worker to reach an example in an epoch claims it and
+// copies the shared model into the replica (ensure_replica, :333-344; the
+// claim is an atomicExch of the epoch number, readiness a release/acquire
+// epoch word); the example's margin and update use only its replica; when a
+// worker has walked its list it stores the replicas of the examples it
+// processed into the shared model (plain stores, last writer wins, :365-369).
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int G, int TASK>
+__global__ void __launch_bounds__(256) hogwild_example_kernel(HogParams p, float* rep,
+                                                              unsigned* claim, unsigned* ready,
+                                                              unsigned epoch) {
+  const int lg = threadIdx.x % G;
+  const unsigned mask = group_mask<G>();
+  const int leader = (threadIdx.x & 31) & ~(G - 1);
+  const uint64_t hg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const uint64_t HG = ((uint64_t)gridDim.x * blockDim.x) / G;
+  for (uint64_t w = hg; w < p.T; w += HG) {
+    const WorkerList l = worker_list(p, w);
+    const uint32_t lo = static_cast<uint32_t>(uint64_t(l.total) * p.seg / p.nseg);
+    const uint32_t hi = static_cast<uint32_t>(uint64_t(l.total) * (p.seg + 1) / p.nseg);
+    for (uint32_t i = lo; i < hi; ++i) {
+      const uint32_t e = list_at(p, l, i);
+      const uint32_t b = __ldg(p.rowptr + e), en = __ldg(p.rowptr + e + 1);
+      // ensure_replica
+      int role = 0;  // 0 ready, 1 initialise, 2 wait
+      if (lg == 0 && ld_acquire_u32(ready + e) != epoch)
+        role = atomicExch(claim + e, epoch) != epoch ? 1 : 2;
+      role = __shfl_sync(mask, role, leader);
+      if (role == 1) {
+        for (uint32_t s = b + lg; s < en; s += G) __stcg(rep + s, ld_model(p.model + __ldg(p.idx + s)));
+        __syncwarp(mask);
+        if (lg == 0) {
+          __threadfence();
+          st_release_u32(ready + e, epoch);
+        }
+      } else if (role == 2) {
+        if (lg == 0)
+          while (ld_acquire_u32(ready + e) != epoch) __nanosleep(32);
+        __syncwarp(mask);
+      }
+      const uint32_t len = en - b;
+      if (len == 0) continue;
+      float z = 0.f;
+      for (uint32_t s = b + lg; s < en; s += G) z = fmaf(__ldg(p.val + s), __ldcg(rep + s), z);
+      z = group_sum_m<G>(z, mask);
+      const float c = coef_f<TASK>(z, __ldg(p.y + e));
+      if (c != 0.f) {
+        const float ac = p.alpha;
+        // Circular offsets (async_engine.cpp:357-362) for one-lane workers.
+        const uint32_t s0 = (G == 1 && p.offsets) ? static_cast<uint32_t>(w % len) : 0u;
+        for (uint32_t t = lg; t < len; t += G) {
+          uint32_t q = s0 + t;
+          if (q >= len) q -= len;
+          const uint32_t s = b + q;
+          __stcg(rep + s, __ldcg(rep + s) - ac * (c * __ldg(p.val + s)));
+        }
+      }
+      __syncwarp(mask);
+    }
+    // Copy the replicas of the processed examples into the shared model.
+    for (uint32_t i = lo; i < hi; ++i) {
+      const uint32_t e = list_at(p, l, i);
+      const uint32_t b = __ldg(p.rowptr + e), en = __ldg(p.rowptr + e + 1);
+      for (uint32_t s = b + lg; s < en; s += G) st_model(p.model + __ldg(p.idx + s), __ldcg(rep + s));
+    }
+  }
+}
+
 // K5 (kernel scope, shared model) and the global-replica variant (block scope
 // with replicas too large for shared memory, thread scope).
 template <int G, int TASK, int KIND, int SCOPE>
@@ -506,8 +585,6 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
   Ctx& c = *ds.ctx;
   const bool col = a.access == SGDB_ACCESS_COL_RR || a.access == SGDB_ACCESS_COL_CH;
   const bool rr = a.access == SGDB_ACCESS_ROW_RR || a.access == SGDB_ACCESS_COL_RR;
-  if (a.replication == SGDB_REPL_EXAMPLE)
-    throw Unsupported("example-scope replication is not implemented on the device");
   if (ds.n_global != ds.n || ds.row_base != 0)
     throw Unsupported("Hogwild epochs run on whole (replicated) datasets");
 
@@ -546,6 +623,32 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
   p.nseg = a.nseg;
   const int G = a.lanes;
 
+
+  if (a.replication == SGDB_REPL_EXAMPLE) {
+    if (kind != kKindCsr) throw std::invalid_argument("example replication requires a sparse layout");
+    materialize(m);
+    m.spread_current = false;
+    if (ds.ex_rep.n < ds.nnz || !ds.ex_rep.p) {
+      ds.ex_rep.alloc(std::max<uint64_t>(1, ds.nnz));
+      ds.ex_claim.alloc(ds.n);
+      ds.ex_ready.alloc(ds.n);
+      ds.ex_claim.zero(c.stream);
+      ds.ex_ready.zero(c.stream);
+      ds.ex_epoch = 0;
+    }
+    if (a.seg == 0) ++ds.ex_epoch;  // one replica generation per epoch (segments share it)
+    p.model = m.w32.p;
+    p.ms = 1;
+    dispatch_lanes(G, [&]<int GL>() {
+      auto kern = a.task == kTaskLR ? hogwild_example_kernel<GL, kTaskLR> : hogwild_example_kernel<GL, kTaskSVM>;
+      const unsigned grid = wave_grid(c, kern, 0, a.workers, GL);
+      prof_begin(c, "hogwild_example_kernel");
+      kern<<<grid, 256, 0, c.stream>>>(p, ds.ex_rep.p, ds.ex_claim.p, ds.ex_ready.p, ds.ex_epoch);
+    });
+    launched(c, "hogwild_example_kernel");
+    sync_w64_from_w32(m);
+    return;
+  }
 
   if (a.replication == SGDB_REPL_KERNEL) {
     p.gs = 1;

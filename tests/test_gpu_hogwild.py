@@ -142,12 +142,50 @@ def test_invalid_plan_layout_rejected(sgdb, dev):
         S.hogwild.train(S.Task.LR, csr, _inc(S, S.Task.LR, 0.1, 1), plan, 0, device=dev)
 
 
-def test_example_scope_is_reported_unsupported(sgdb, dev):
+@pytest.mark.parametrize("name,plan_text", [("csr", "row-ch:example:0"), ("csr", "row-rr:example:0"),
+                                             ("padded", "row-ch:example:0"), ("csr", "row-ch:example:3")])
+@pytest.mark.parametrize("task", [0, 1])
+@pytest.mark.parametrize("lanes", [1, 32])
+def test_example_scope_one_worker_matches_reference(sgdb, dev, ref, datasets, name, plan_text, task,
+                                                    lanes):
+    """Example-scope replication (async_engine.cpp:266-370) with one worker is
+    deterministic: every example's replica starts from the epoch-start model,
+    and the shared model takes the replicas in list order at the end of the
+    epoch. Compared with the unmodified reference's hogwild::train."""
     S = sgdb
-    csr = S.fixtures.sparse_classification(10, 5, 2.0, 19)
-    plan = S.parse_plan("row-ch:example:0")
-    with pytest.raises(S.UnsupportedError):
-        S.hogwild.train(S.Task.LR, csr, _inc(S, S.Task.LR, 0.1, 1), plan, 0, device=dev)
+    ds = datasets[name]
+    plan = S.parse_plan(plan_text)
+    plan.workers = 1
+    plan.lanes_per_worker = lanes
+    alpha, epochs = 0.1, 4
+    r = S.hogwild.train(S.Task(task), ds, _inc(S, S.Task(task), alpha, epochs), plan, 0, device=dev)
+    model, losses, _, evals = ref.hogwild_train(ds, task, alpha, epochs, plan_text, workers=1)
+    assert rel_l2(r.model, model) <= MODEL_TOL, rel_l2(r.model, model)
+    for e in range(epochs):
+        assert rel(r.trace.epochs[e].loss, losses[e]) <= LOSS_TOL
+    assert list(r.evals_per_epoch) == [int(x) for x in evals]
+
+
+def test_example_scope_racing_workers_converge(sgdb, dev, ref):
+    """Racing workers with example replicas (and k-rep duplicates claimed by
+    two workers). The result depends on when replicas are initialised relative
+    to other workers' end-of-list stores: a single worker initialises every
+    replica from the epoch-start model, the reference's staggered threads let
+    later replicas see earlier stores. Every interleaving is legal, so the
+    device's final loss must fall within that range (10 % slack either side)."""
+    S = sgdb
+    ds = S.fixtures.sparse_classification(3000, 400, 12.0, 23).rounded_f32()
+    plan = S.parse_plan("row-ch:example:2")
+    plan.workers = 8
+    hp = _inc(S, S.Task.SVM, 0.05, 8)
+    r = S.hogwild.train(S.Task.SVM, ds, hp, plan, 0, device=dev)
+    _, ref1, _, _ = ref.hogwild_train(ds, 1, 0.05, 8, "row-ch:example:2", workers=1)
+    _, ref8, _, _ = ref.hogwild_train(ds, 1, 0.05, 8, "row-ch:example:2", workers=8)
+    losses = r.trace.losses()
+    assert all(np.isfinite(losses)) and losses[-1] < losses[0]
+    lo, hi = min(ref1[-1], ref8[-1]), max(ref1[-1], ref8[-1])
+    assert 0.9 * lo <= losses[-1] <= 1.1 * hi, (losses[-1], ref1[-1], ref8[-1])
+    assert r.evals_per_epoch[0] == ds.n_examples + 8 * 2
 
 
 @pytest.fixture(scope="module")
