@@ -417,13 +417,29 @@ __global__ void __launch_bounds__(256) hogwild_mirror_kernel(HogParams p) {
 template <int G, int TASK, int KIND>
 __global__ void __launch_bounds__(1024) hogwild_smem_kernel(HogParams p, const float* w32,
                                                             uint64_t R) {
-  extern __shared__ float rep[];
+  extern __shared__ __align__(16) float rep[];
+  __shared__ uint64_t bar;
   const int lg = threadIdx.x % G;
   const unsigned mask = group_mask<G>();
   const uint64_t gi = threadIdx.x / G, NG = blockDim.x / G;
-  for (uint64_t r = blockIdx.x; r < R; r += gridDim.x) {
-    for (uint64_t j = threadIdx.x; j <= p.d; j += blockDim.x) rep[j] = j < p.d ? w32[j] : 0.f;
-    __syncthreads();
+  // The replica (w32 and its zero guard slot, allocated in whole 16-byte
+  // groups) arrives by bulk copy: a thread loop left ~10 % of the epoch's
+  // stall samples on the stores waiting for their loads (ncu, rcv1 block).
+  const uint32_t bytes = round_up16((p.d + 1) * 4ull);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (uint64_t r = blockIdx.x; r < R; r += gridDim.x, phase ^= 1u) {
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&bar, bytes);
+      for (uint32_t off = 0; off < bytes; off += 32768)
+        bulk_g2s(reinterpret_cast<char*>(rep) + off, reinterpret_cast<const char*>(w32) + off,
+                 min(32768u, bytes - off), &bar);
+    }
+    mbar_wait(&bar, phase);
     for (uint64_t t = gi; t < p.gs; t += NG) {
       const uint64_t w = r * p.gs + t;
       if (w >= p.T) break;
@@ -471,8 +487,17 @@ __global__ void replicas_merge_kernel(const float* reps, uint64_t R, uint64_t ld
                                       double* w64, float* w32) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
        j += (uint64_t)gridDim.x * blockDim.x) {
+    // Replica order as merge_models sums; eight loads in flight per thread.
     double s = 0.0;
-    for (uint64_t r = 0; r < R; ++r) s += 1.0 * static_cast<double>(reps[r * ld + j]);
+    uint64_t r = 0;
+    for (; r + 8 <= R; r += 8) {
+      float v8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v8[k] = reps[(r + k) * ld + j];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += 1.0 * static_cast<double>(v8[k]);
+    }
+    for (; r < R; ++r) s += 1.0 * static_cast<double>(reps[r * ld + j]);
     const double v = s / static_cast<double>(R);
     w64[j] = v;
     w32[j] = static_cast<float>(v);
@@ -724,7 +749,7 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
   p.ld = ld;
   p.ms = 1;
   p.model = m.replicas.p;
-  const size_t rep_bytes = (ds.d + 1) * sizeof(float);
+  const size_t rep_bytes = round_up16((ds.d + 1) * sizeof(float));
   const bool smem_ok = a.replication == SGDB_REPL_BLOCK && rep_bytes + 1024 <= c.max_smem_optin;
   if (smem_ok) {
     uint64_t threads = std::min<uint64_t>(1024, gs * G);

@@ -1,6 +1,6 @@
 """Small driver for ncu captures: runs a few epochs of one target op.
 
-    python scripts/prof_targets.py {hogwild_w8a|sync_covtype|sync_rcv1|sync_dense1000|sync_c5} [epochs]
+    python scripts/prof_targets.py {hogwild_w8a|hogwild_rcv1_block|sync_covtype|sync_rcv1|sync_dense1000|sync_c5} [epochs]
 """
 import os
 import sys
@@ -26,6 +26,15 @@ def main():
         for _ in range(epochs):
             flush.zero_()
             S.hogwild_epoch(dds, model, S.Task.SVM, 0.01, plan)
+    elif target == "hogwild_rcv1_block":
+        host = S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813)
+        dds = S.DeviceDataset(dev, host)
+        plan = S.parse_plan("row-ch:block:0")
+        plan.workers = dev.resident_workers(dds)
+        model = S.DeviceModel(dev, host.n_features)
+        for _ in range(epochs):
+            flush.zero_()
+            S.hogwild_epoch(dds, model, S.Task.LR, 0.01, plan)
     elif target == "sync_c5":
         # C5 shape (d = 1000), device Philox generator; 2M rows = 8 GB > L2.
         dds = S.DeviceDataset.generate_dense(dev, 2_000_000, 1000, 20250814)
