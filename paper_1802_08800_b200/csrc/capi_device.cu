@@ -329,7 +329,7 @@ sgdb_status sgdb_ctx_resident_workers(sgdb_ctx* ctx, const sgdb_dataset* ds, int
                                       uint64_t* out) {
   return sgdb_guard([&] {
     int g = lanes > 0 ? lanes : hogwild_auto_lanes(*ds, SGDB_ACCESS_ROW_CH);
-    *out = hogwild_resident_workers(*ctx, g);
+    *out = hogwild_resident_workers(*ctx, *ds, g);
   });
 }
 

@@ -233,7 +233,9 @@ struct HogwildArgs {
   double alpha_f64 = 0.0;      // exact-fp64 mode step size
 };
 int hogwild_auto_lanes(const Dataset& ds, int access);
-uint64_t hogwild_resident_workers(const Ctx& c, int lanes);
+// Lane groups of one resident wave of the kernel-scope Hogwild kernel this
+// dataset would use (the long-row variant holds more registers).
+uint64_t hogwild_resident_workers(const Ctx& c, const Dataset& ds, int lanes);
 void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a);
 
 // Make w32/w64 current (gathers the spread Hogwild copy if it is newer).

@@ -210,7 +210,7 @@ __device__ __forceinline__ Batch load_batch(const HogParams& p, const Row& r, ui
 // One example: margin over every slot (padded sentinels read the guard slot
 // w[d] == 0), coefficient (glm.cpp:30-34), lock-free update. `first` holds
 // this lane's first batch, prefetched by the worker loop.
-template <int G, int TASK, int KIND, class M>
+template <int G, int TASK, int KIND, class M, bool LONG = false>
 __device__ __forceinline__ void process_example(const HogParams& p, const M& m, const Row& r,
                                                 const Batch& first, uint64_t wid, int lg,
                                                 unsigned mask) {
@@ -233,13 +233,29 @@ __device__ __forceinline__ void process_example(const HogParams& p, const M& m, 
       for (int u = 1; u < kU; ++u) z = fmaf(first.x[u], mv[u], z);
     }
   }
-  for (uint32_t s0 = lg + G * kU; s0 < len; s0 += G * kU) {
+  // Remaining slots. LONG (datasets whose rows run to thousands of slots —
+  // news20's Pareto tail reaches 9,100, all walked by one worker): two
+  // batches per trip, so each dependent round trip carries 2U loads and 2U
+  // gathers per lane (same summation order). Off by default: the second
+  // batch costs ~16 registers, i.e. a quarter of the resident workers.
+  for (uint32_t s0 = lg + G * kU; s0 < len; s0 += (LONG ? 2 : 1) * G * kU) {
     const Batch bt = load_batch<G, KIND>(p, r, s0, len, lg);
-    float mv[kU];
+    const bool two = LONG && s0 - lg + G * kU < len;  // group-uniform
+    Batch b2{};
+    if (two) b2 = load_batch<G, KIND>(p, r, s0 + G * kU, len, lg);
+    float mv[kU], mv2[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) mv[u] = (s0 + u * G < len) ? m.load(bt.j[u]) : 0.f;
+    if (two) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) mv2[u] = (s0 + (kU + u) * G < len) ? m.load(b2.j[u]) : 0.f;
+    }
 #pragma unroll
     for (int u = 0; u < kU; ++u) z = fmaf(bt.x[u], mv[u], z);
+    if (two) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) z = fmaf(b2.x[u], mv2[u], z);
+    }
   }
   z = group_sum_m<G>(z, mask);
   const float c = coef_f<TASK>(z, r.y);
@@ -260,11 +276,19 @@ __device__ __forceinline__ void process_example(const HogParams& p, const M& m, 
     for (int u = 1; u < kU; ++u)
       if (lg + u * G < len) m.add(first.j[u], -(ac * (c * first.x[u])));
   }
-  for (uint32_t s0 = lg + G * kU; s0 < len; s0 += G * kU) {
+  for (uint32_t s0 = lg + G * kU; s0 < len; s0 += (LONG ? 2 : 1) * G * kU) {
     const Batch bt = load_batch<G, KIND>(p, r, s0, len, lg);
+    const bool two = LONG && s0 - lg + G * kU < len;  // group-uniform
+    Batch b2{};
+    if (two) b2 = load_batch<G, KIND>(p, r, s0 + G * kU, len, lg);
 #pragma unroll
     for (int u = 0; u < kU; ++u)
       if (s0 + u * G < len) m.add(bt.j[u], -(ac * (c * bt.x[u])));
+    if (two) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (s0 + (kU + u) * G < len) m.add(b2.j[u], -(ac * (c * b2.x[u])));
+    }
   }
 }
 
@@ -272,7 +296,7 @@ __device__ __forceinline__ void process_example(const HogParams& p, const M& m, 
 // runs, the row extent of example i+2 and the first slot batch of example
 // i+1 are already in flight (data only — the model is always read fresh, so
 // the single-worker schedule is exactly sequential Alg. 3).
-template <int G, int TASK, int KIND, class M>
+template <int G, int TASK, int KIND, class M, bool LONG = false>
 __device__ __forceinline__ void run_worker(const HogParams& p, const M& m, uint64_t w, int lg,
                                            unsigned mask) {
   const WorkerList l = worker_list(p, w);
@@ -288,7 +312,7 @@ __device__ __forceinline__ void run_worker(const HogParams& p, const M& m, uint6
     Row after = nxt;
     if (i + 1 < hi) bnxt = load_batch<G, KIND>(p, nxt, lg, row_len<KIND>(nxt), lg);
     if (i + 2 < hi) after = make_row<KIND>(p, list_at(p, l, i + 2));
-    process_example<G, TASK, KIND>(p, m.at(cur.e), cur, bcur, w, lg, mask);
+    process_example<G, TASK, KIND, decltype(m.at(cur.e)), LONG>(p, m.at(cur.e), cur, bcur, w, lg, mask);
     cur = nxt;
     bcur = bnxt;
     nxt = after;
@@ -376,7 +400,7 @@ __global__ void __launch_bounds__(256) hogwild_example_kernel(HogParams p, float
 
 // K5 (kernel scope, shared model) and the global-replica variant (block scope
 // with replicas too large for shared memory, thread scope).
-template <int G, int TASK, int KIND, int SCOPE>
+template <int G, int TASK, int KIND, int SCOPE, bool LONG = false>
 __global__ void __launch_bounds__(256) hogwild_kernel(HogParams p) {
   const int lg = threadIdx.x % G;
   const unsigned mask = group_mask<G>();
@@ -384,9 +408,10 @@ __global__ void __launch_bounds__(256) hogwild_kernel(HogParams p) {
   const uint64_t HG = ((uint64_t)gridDim.x * blockDim.x) / G;
   for (uint64_t w = hg; w < p.T; w += HG) {
     if (SCOPE == kScopeSharedAtomic) {
-      run_worker<G, TASK, KIND>(p, GlobalAtomicModel<kSpread>{p.model}, w, lg, mask);
+      run_worker<G, TASK, KIND, GlobalAtomicModel<kSpread>, LONG>(p, GlobalAtomicModel<kSpread>{p.model}, w, lg,
+                                                                 mask);
     } else if (SCOPE == kScopeSharedAtomicFlat) {
-      run_worker<G, TASK, KIND>(p, GlobalAtomicModel<1>{p.model}, w, lg, mask);
+      run_worker<G, TASK, KIND, GlobalAtomicModel<1>, LONG>(p, GlobalAtomicModel<1>{p.model}, w, lg, mask);
     } else {
       run_worker<G, TASK, KIND>(
           p,
@@ -596,11 +621,19 @@ unsigned wave_grid(const Ctx& c, K kern, size_t smem, uint64_t workers, int lane
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min(need, cap)));
 }
 
-uint64_t hogwild_resident_workers(const Ctx& c, int lanes) {
+bool hogwild_long_rows(const Dataset& ds) {
+  return ds.kind == Kind::Csr && ds.n && ds.nnz / ds.n >= 256;
+}
+
+uint64_t hogwild_resident_workers(const Ctx& c, const Dataset& ds, int lanes) {
   uint64_t out = 0;
   dispatch_lanes(lanes, [&]<int GL>() {
-    const unsigned grid = wave_grid(c, hogwild_kernel<GL, kTaskSVM, kKindCsr, kScopeSharedAtomic>, 0,
-                                    ~uint64_t(0) / 64, GL);
+    const unsigned grid =
+        (GL == 32 && hogwild_long_rows(ds))
+            ? wave_grid(c, hogwild_kernel<GL, kTaskSVM, kKindCsr, kScopeSharedAtomic, true>, 0,
+                        ~uint64_t(0) / 64, GL)
+            : wave_grid(c, hogwild_kernel<GL, kTaskSVM, kKindCsr, kScopeSharedAtomic>, 0,
+                        ~uint64_t(0) / 64, GL);
     out = static_cast<uint64_t>(grid) * 256 / GL;
   });
   return out;
@@ -701,6 +734,9 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
     int mode = a.model_mode;
     if (mode == 2 && mirror_bytes > 48 * 1024) mode = 1;  // mirror needs d+1 floats per CTA
     p.refresh = a.refresh;
+    // Average row of hundreds of slots (news20: 461): the batch chain of the
+    // longest rows dominates, and the worker count (n / chunk) is small anyway.
+    const bool long_rows = kind == kKindCsr && hogwild_long_rows(ds);
     dispatch_lanes(G, [&]<int GL>() {
       dispatch_kind(kind, [&]<int KD>() {
         void (*kern)(HogParams);
@@ -709,6 +745,14 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
           kern = a.task == kTaskLR ? hogwild_mirror_kernel<GL, kTaskLR, KD>
                                    : hogwild_mirror_kernel<GL, kTaskSVM, KD>;
           smem = mirror_bytes;
+        } else if (mode == 1 && long_rows && GL == 32 && KD == kKindCsr) {
+          // Long rows: two slot batches per round trip (see process_example).
+          if (ms > 1)
+            kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomic, true>
+                                     : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomic, true>;
+          else
+            kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomicFlat, true>
+                                     : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomicFlat, true>;
         } else if (mode == 1 && ms > 1) {
           kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomic>
                                    : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomic>;
