@@ -137,6 +137,7 @@ struct Dataset {
   // of the model at every stored slot (aligned with val/idx), plus the
   // per-example claim / ready epoch words of ensure_replica (:333-344).
   DBuf<float> ex_rep;
+  DBuf<double> ex_rep64;  // exact-fp64 mode
   DBuf<unsigned> ex_claim, ex_ready;
   unsigned ex_epoch = 0;
   // Scratch.

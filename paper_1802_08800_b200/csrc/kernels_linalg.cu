@@ -337,6 +337,73 @@ __global__ void __launch_bounds__(256) hogwild_exact_kernel(ExactHog p) {
   }
 }
 
+// Example scope in the reference's order (async_engine.cpp:333-370): the
+// claim/ready protocol of K5x (kernels_hogwild.cu) with fp64 replicas; margin
+// summed in slot order, updates cur - alpha*(c*x), replicas stored into the
+// shared model when the worker's list is done.
+template <int TASK>
+__global__ void __launch_bounds__(256) hogwild_exact_example_kernel(ExactHog p, double* rep,
+                                                                    unsigned* claim, unsigned* ready,
+                                                                    unsigned epoch) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t hw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const uint64_t HW = ((uint64_t)gridDim.x * blockDim.x) / 32;
+  double* m = p.model;
+  for (uint64_t w = hw; w < p.T; w += HW) {
+    const WorkerList l = assign_list(p.n, p.T, p.k, p.rr != 0, w);
+    const uint32_t lo = static_cast<uint32_t>(uint64_t(l.total) * p.seg / p.nseg);
+    const uint32_t hi = static_cast<uint32_t>(uint64_t(l.total) * (p.seg + 1) / p.nseg);
+    for (uint32_t i = lo; i < hi; ++i) {
+      const uint32_t e = assign_at(p.n, l, i);
+      const uint32_t b = p.rowptr[e], len = p.rowptr[e + 1] - b;
+      int role = 0;
+      if (lane == 0) {
+        unsigned r;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(ready + e) : "memory");
+        if (r != epoch) role = atomicExch(claim + e, epoch) != epoch ? 1 : 2;
+      }
+      role = __shfl_sync(0xffffffffu, role, 0);
+      if (role == 1) {
+        for (uint32_t s = lane; s < len; s += 32) __stcg(rep + b + s, __ldcg(m + p.idx[b + s]));
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ready + e), "r"(epoch) : "memory");
+        }
+      } else if (role == 2) {
+        if (lane == 0) {
+          unsigned r;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(ready + e) : "memory");
+          } while (r != epoch);
+        }
+        __syncwarp();
+      }
+      if (len == 0) continue;
+      double z = 0.0;
+      for (uint32_t base = 0; base < len; base += 32) {
+        double prod = 0.0;
+        if (base + lane < len) prod = __dmul_rn(p.val[b + base + lane], __ldcg(rep + b + base + lane));
+        const uint32_t cnt = min(32u, len - base);
+        for (uint32_t t = 0; t < cnt; ++t) z = __dadd_rn(z, __shfl_sync(0xffffffffu, prod, t));
+      }
+      const double y = static_cast<double>(p.y[e]);
+      const double mm = __dmul_rn(y, z);
+      const double c = TASK == 0 ? __dmul_rn(libm::stable_sigmoid(-mm), -y) : (mm < 1.0 ? -y : 0.0);
+      for (uint32_t s = lane; s < len; s += 32) {
+        const double upd = __dmul_rn(p.alpha, __dmul_rn(c, p.val[b + s]));
+        __stcg(rep + b + s, __dsub_rn(__ldcg(rep + b + s), upd));
+      }
+      __syncwarp();
+    }
+    for (uint32_t i = lo; i < hi; ++i) {
+      const uint32_t e = assign_at(p.n, l, i);
+      const uint32_t b = p.rowptr[e], len = p.rowptr[e + 1] - b;
+      for (uint32_t s = lane; s < len; s += 32) __stcg(m + p.idx[b + s], __ldcg(rep + b + s));
+    }
+  }
+}
+
 // Replica prepare (async_engine.cpp:372-383): every replica = the global
 // model, guard slot 0.
 __global__ void replicas_fill_kernel(double* reps, uint64_t R, uint64_t d, const double* w) {
@@ -585,8 +652,6 @@ void exact_loss(Dataset& ds, Model& m, int task) {
 
 void exact_hogwild(Dataset& ds, Model& m, const HogwildArgs& a) {
   require_exact(ds);
-  if (a.replication == SGDB_REPL_EXAMPLE)
-    throw Unsupported("example-scope replication is not implemented on the device");
   Ctx& c = *ds.ctx;
   materialize(m);
   ExactHog p{};
@@ -604,6 +669,31 @@ void exact_hogwild(Dataset& ds, Model& m, const HogwildArgs& a) {
   p.seg = a.seg;
   p.nseg = a.nseg;
   uint64_t R = 0;
+  if (a.replication == SGDB_REPL_EXAMPLE) {
+    if (dense) throw std::invalid_argument("example replication requires a sparse layout");
+    if (ds.ex_rep64.n < ds.nnz || !ds.ex_rep64.p || ds.ex_claim.n < ds.n || !ds.ex_claim.p) {
+      ds.ex_rep64.alloc(std::max<uint64_t>(1, ds.nnz));
+      ds.ex_claim.alloc(ds.n);
+      ds.ex_ready.alloc(ds.n);
+      ds.ex_claim.zero(c.stream);
+      ds.ex_ready.zero(c.stream);
+      ds.ex_epoch = 0;
+    }
+    if (a.seg == 0) ++ds.ex_epoch;
+    p.model = m.w64.p;
+    const unsigned egrid = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>((a.workers + 7) / 8, c.num_sms * 8ull)));
+    prof_begin(c, "hogwild_exact_kernel");
+    if (a.task == 0)
+      hogwild_exact_example_kernel<0><<<egrid, 256, 0, c.stream>>>(p, ds.ex_rep64.p, ds.ex_claim.p,
+                                                                   ds.ex_ready.p, ds.ex_epoch);
+    else
+      hogwild_exact_example_kernel<1><<<egrid, 256, 0, c.stream>>>(p, ds.ex_rep64.p, ds.ex_claim.p,
+                                                                   ds.ex_ready.p, ds.ex_epoch);
+    launched(c, "hogwild_exact_kernel");
+    refresh_w32(m);
+    return;
+  }
   if (a.replication == SGDB_REPL_KERNEL) {
     p.model = m.w64.p;
     p.gs = a.workers;  // one "group": w / gs == 0

@@ -135,6 +135,25 @@ def test_hogwild_one_worker_bitwise(sgdb, ref, dev, layout, access, scope):
         assert r.evals_per_epoch == [int(e) for e in evals]
 
 
+@pytest.mark.parametrize("layout", [2, 3])
+@pytest.mark.parametrize("access", ["row-rr", "row-ch"])
+def test_hogwild_example_scope_one_worker_bitwise(sgdb, ref, dev, layout, access):
+    """Example-scope replication (async_engine.cpp:266-370), one worker, exact mode."""
+    S = sgdb
+    ds = _data(S, S.Layout(layout), 400, 40, 78, 8.0)
+    dds = _exact(S, dev, ds)
+    for task, k in ((0, 0), (1, 2)):
+        rep = "0" if k == 0 else f"rep-{k}"
+        plan = S.parse_plan(f"{access}:example:{rep}")
+        plan.workers = 1
+        hp = S.Hyperparams(alpha=0.05, batch_b=1, epochs=3, task=S.Task(task))
+        r = S.hogwild.train(S.Task(task), dds, hp, plan)
+        model, losses, _, evals = ref.hogwild_train(ds, task, 0.05, 3, f"{access}:example:{rep}")
+        assert np.array_equal(r.model, model), (task, k)
+        _losses_match(task, r.trace.losses(), losses)
+        assert r.evals_per_epoch == [int(e) for e in evals]
+
+
 def test_numa_dual_one_worker_bitwise(sgdb, ref, dev):
     S = sgdb
     ds = _data(S, S.Layout.Csr, 600, 50, 91, 6.0)
