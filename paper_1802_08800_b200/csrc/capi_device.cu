@@ -89,6 +89,9 @@ void upload_csr(sgdb_dataset* ds, std::vector<uint32_t>& rowptr, std::vector<uin
   cudaStream_t s = ds->ctx->stream;
   ds->kind = Kind::Csr;
   ds->nnz = idx.size();
+  ds->max_row = 0;
+  for (size_t r = 0; r + 1 < rowptr.size(); ++r)
+    ds->max_row = std::max<uint64_t>(ds->max_row, rowptr[r + 1] - rowptr[r]);
   // +8 slack: vectorised kernels read whole aligned 16-byte groups around a row.
   ds->val.alloc(ds->nnz + 8);
   ds->idx.alloc(ds->nnz + 8);

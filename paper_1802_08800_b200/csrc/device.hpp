@@ -106,6 +106,7 @@ struct Dataset {
   int layout_in = SGDB_LAYOUT_CSR;
   Kind kind = Kind::Csr;
   uint64_t nnz = 0;  // stored entries (CSR) or n*d (dense)
+  uint64_t max_row = 0;  // longest CSR row (slots)
   DBuf<float> labels;  // n (padded to a multiple of 4 + tile slack)
   // Dense row-major fp32, n*d (+ slack so bulk copies may round up to 16 B).
   DBuf<float> x;
@@ -140,6 +141,11 @@ struct Dataset {
   DBuf<double> ex_rep64;  // exact-fp64 mode
   DBuf<unsigned> ex_claim, ex_ready;
   unsigned ex_epoch = 0;
+  // Warp partition of the nonzeros for the segmented margin pass (K2t):
+  // first owned row per warp, and the partial sums of rows cut by warps.
+  DBuf<uint32_t> seg_orow;
+  DBuf<float> seg_pf, seg_pl;
+  uint32_t seg_nw = 0;
   // Scratch.
   DBuf<float> coef;        // per local row coefficient (sparse full batch)
   DBuf<uint32_t> order;    // n_global ids of the current epoch

@@ -815,11 +815,24 @@ __global__ void __launch_bounds__(NT, 1) csr_coef_smem_kernel(
 // and made the kernels L1-bound; ncu l1tex 90 %).
 constexpr int kSegE = 4;
 
+// Warp w streams the nonzeros [w*nnz/NW, (w+1)*nnz/NW) whatever the row
+// boundaries (news20's rows run to 9,100 slots; a row-balanced split left
+// one warp with ~5x the average work). orow[w] = first row starting at or
+// after warp w's first element (orow[NW] = n). A row cut by warp boundaries
+// is finished from the per-warp pieces — pf[w]: the part of a row continued
+// into warp w up to its tail, pl[w]: the part of a row up to warp w's end —
+// by csr_coef_fixup_kernel. Used when one row could outweigh a warp's share
+// (split); otherwise each warp takes whole rows, n / NW of them.
+__host__ __device__ __forceinline__ uint32_t seg_pos(uint64_t nnz, uint32_t w, uint32_t nw) {
+  return static_cast<uint32_t>(nnz * w / nw);
+}
+
 template <int TASK, bool SMEM, int NT>
 __global__ void __launch_bounds__(NT, 1) csr_coef_seg_kernel(
     const float* __restrict__ val, const uint32_t* __restrict__ idx,
     const uint32_t* __restrict__ rowptr, const float* __restrict__ y, uint32_t n,
-    const float* __restrict__ w32, uint32_t d, float* __restrict__ coef) {
+    const float* __restrict__ w32, uint32_t d, float* __restrict__ coef,
+    const uint32_t* __restrict__ orow, float* __restrict__ pf, float* __restrict__ pl, int split) {
   // Dynamic SMEM: [model (SMEM) | per-warp scratch].
   extern __shared__ __align__(16) unsigned char dsm[];
   float* ws = reinterpret_cast<float*>(dsm);
@@ -840,12 +853,27 @@ __global__ void __launch_bounds__(NT, 1) csr_coef_seg_kernel(
   __syncthreads();
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t r0 = static_cast<uint32_t>(uint64_t(n) * gw / nw);
-  const uint32_t r1 = static_cast<uint32_t>(uint64_t(n) * (gw + 1) / nw);
+  const uint64_t nnz = __ldg(rowptr + n);
+  uint32_t P0, P1, g0, g1;
+  bool cont = false;
+  if (split) {
+    P0 = seg_pos(nnz, gw, nw);
+    P1 = seg_pos(nnz, gw + 1, nw);
+    const uint32_t o0 = __ldg(orow + gw), o1 = __ldg(orow + gw + 1);
+    // Continued row: the one before o0, if it runs past P0.
+    cont = o0 > 0 && __ldg(rowptr + o0) > P0 && __ldg(rowptr + o0 - 1) < P0;
+    g0 = cont ? o0 - 1 : o0;
+    g1 = o1;
+  } else {  // whole rows, n / NW per warp
+    g0 = static_cast<uint32_t>(uint64_t(n) * gw / nw);
+    g1 = static_cast<uint32_t>(uint64_t(n) * (gw + 1) / nw);
+    P0 = __ldg(rowptr + g0);
+    P1 = __ldg(rowptr + g1);
+  }
   if (SMEM) mbar_wait(&bar, 0);
   const float* w = SMEM ? ws : w32;
-  segment_stream<float, kSegE, 2, VecGroup>(
-      rowptr, y, r0, r1, [&](uint32_t a, int k) { return vec_group(val, idx, a + 4 * k); },
+  const float open = segment_stream<float, kSegE, 2, VecGroup>(
+      rowptr, y, g0, g1, P0, P1, [&](uint32_t a, int k) { return vec_group(val, idx, a + 4 * k); },
       [&](const VecGroup (&g)[kSegE / 4], float* p) {
 #pragma unroll
         for (int k = 0; k < kSegE / 4; ++k) {
@@ -864,9 +892,61 @@ __global__ void __launch_bounds__(NT, 1) csr_coef_seg_kernel(
       },
       [&](uint32_t r, float z, float yy, bool ok) {
         const float c = coef_fast<TASK>(z, yy);
-        if (ok) coef[r] = c;
+        if (ok) {
+          if (cont && r == g0) pf[gw] = z;
+          else coef[r] = c;
+        }
       },
       scratch[warp]);
+  if (split && lane == 0 && g1 > g0 && __ldg(rowptr + g1) > P1) pl[gw] = open;
+}
+
+// Finishes the rows cut by warp boundaries (split mode): the warp where row
+// r starts adds its pl, every warp lying wholly inside r adds its pl, the
+// warp holding r's tail adds its pf — in warp order — and the coefficient is
+// formed.
+template <int TASK>
+__global__ void csr_coef_fixup_kernel(const uint32_t* __restrict__ rowptr, const float* __restrict__ y,
+                                      uint32_t n, const uint32_t* __restrict__ orow, uint32_t nw,
+                                      const float* __restrict__ pf, const float* __restrict__ pl,
+                                      float* __restrict__ coef) {
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nw) return;
+  const uint64_t nnz = rowptr[n];
+  const uint32_t o0 = orow[w], o1 = orow[w + 1];
+  if (o1 <= o0) return;  // no row starts in this warp
+  const uint32_t r = o1 - 1;
+  if (rowptr[r + 1] <= seg_pos(nnz, w + 1, nw)) return;  // the row ends inside the warp
+  float z = pl[w];
+  for (uint32_t v = w + 1; v < nw; ++v) {
+    if (rowptr[r + 1] > seg_pos(nnz, v + 1, nw)) {
+      z += pl[v];  // warp v lies wholly inside row r
+    } else {
+      z += pf[v];
+      break;
+    }
+  }
+  coef[r] = coef_fast<TASK>(z, y[r]);
+}
+
+// orow[w] = first row whose start is >= warp w's first element (binary
+// search over rowptr); orow[nw] = n.
+__global__ void seg_partition_kernel(const uint32_t* __restrict__ rowptr, uint32_t n, uint32_t nw,
+                                     uint32_t* __restrict__ orow) {
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w > nw) return;
+  if (w == nw) {
+    orow[w] = n;
+    return;
+  }
+  const uint32_t P = seg_pos(rowptr[n], w, nw);
+  uint32_t lo = 0, hi = n;  // first r in [0, n] with rowptr[r] >= P
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    if (rowptr[mid] >= P) hi = mid;
+    else lo = mid + 1;
+  }
+  orow[w] = lo;
 }
 
 // ---------------------------------------------------------------------------
@@ -1103,7 +1183,7 @@ __global__ void __launch_bounds__(NT, 1) csc_seg_kernel(
   double* out = partials + static_cast<uint64_t>(b) * d;
   mbar_wait(&bar, 0);
   segment_stream<double, kSegE, 2, CscWin>(
-      cp, nullptr, c0, c1,
+      cp, nullptr, c0, c1, __ldg(cp + c0), __ldg(cp + c1),
       [&](uint32_t a, int q) {
         CscWin w;
         w.v = __ldg(reinterpret_cast<const float4*>(cval + a + 4 * q));
@@ -1594,11 +1674,38 @@ bool launch_csr_coef_seg_N(Dataset& ds, Model& m) {
   const uint64_t want = std::max<uint64_t>(1, (ds.nnz / 512 + NT / 32 - 1) / (NT / 32));
   const unsigned grid = static_cast<unsigned>(
       std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(per_sm) * c.num_sms)));
+  const uint32_t nw = grid * (NT / 32);
+  // Split rows across warps when one row could outweigh a warp's share
+  // several times over (news20: 9,100-slot rows vs ~1,950 slots per warp);
+  // otherwise whole rows per warp need no fix-up pass.
+  // Also on large inputs, where the balance gain outweighs the fix-up launch
+  // (rcv1: 135 -> 114 + 9 us; w8a / real-sim lose a few us).
+  const char* se = std::getenv("SGDB_SEG_SPLIT");  // 1 / 0 force it (tests, A/B)
+  const bool split = se ? std::atoi(se) != 0
+                        : (ds.max_row > 4 * (ds.nnz / std::max<uint32_t>(1, nw)) || ds.nnz > (16ull << 20));
+  if (split && ds.seg_nw != nw) {  // warp partition of the nonzeros (cached per dataset and warp count)
+    ds.seg_orow.alloc(nw + 1);
+    ds.seg_pf.alloc(nw);
+    ds.seg_pl.alloc(nw);
+    prof_begin(c, "seg_partition_kernel");
+    seg_partition_kernel<<<(nw + 256) / 256, 256, 0, c.stream>>>(ds.rowptr.p, static_cast<uint32_t>(ds.n), nw,
+                                                               ds.seg_orow.p);
+    launched(c, "seg_partition_kernel");
+    ds.seg_nw = nw;
+  }
   prof_begin(c, "csr_coef_kernel");
   kern<<<grid, NT, smem, c.stream>>>(ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p,
                                      static_cast<uint32_t>(ds.n), m.w32.p,
-                                     static_cast<uint32_t>(ds.d), ds.coef.p);
+                                     static_cast<uint32_t>(ds.d), ds.coef.p, ds.seg_orow.p,
+                                     ds.seg_pf.p, ds.seg_pl.p, split ? 1 : 0);
   launched(c, "csr_coef_kernel");
+  if (split) {
+    prof_begin(c, "csr_coef_fixup_kernel");
+    csr_coef_fixup_kernel<TASK><<<(nw + 255) / 256, 256, 0, c.stream>>>(
+        ds.rowptr.p, ds.labels.p, static_cast<uint32_t>(ds.n), ds.seg_orow.p, nw, ds.seg_pf.p,
+        ds.seg_pl.p, ds.coef.p);
+    launched(c, "csr_coef_fixup_kernel");
+  }
   return true;
 }
 

@@ -46,16 +46,23 @@ struct SegScratch {
 // NB = window buffers per lane: 2 keeps the next tile's loads in flight
 // while a tile is scanned (more registers), 1 issues them at the top of the
 // tile (for CTAs with many warps, which supply the memory parallelism).
+//
+// Element range: the warp streams elements [P0, P1). P0 may lie inside
+// segment g0 (a segment continued from the previous warp: its head is not
+// seen, and the sum emitted at its tail covers only [P0, tail]) and P1 may
+// lie inside segment g1-1 (its tail is not reached: nothing is emitted for
+// it). Returns the open segment's sum at P1 (the cut segment's partial).
+// P0 = ptr[g0], P1 = ptr[g1] gives whole segments.
 template <typename T, int E, int NB, class Win, class Load, class Prod, class Emit>
-__device__ __forceinline__ void segment_stream(const uint32_t* __restrict__ ptr,
-                                               const float* __restrict__ aux, uint32_t g0,
-                                               uint32_t g1, Load load, Prod prod, Emit emit,
-                                               SegScratch<T, E>& sc) {
+__device__ __forceinline__ T segment_stream(const uint32_t* __restrict__ ptr,
+                                            const float* __restrict__ aux, uint32_t g0,
+                                            uint32_t g1, uint32_t P0, uint32_t P1, Load load,
+                                            Prod prod, Emit emit, SegScratch<T, E>& sc) {
   constexpr uint32_t TILE = 32 * E;
   constexpr int NW = E / 4;
   const int lane = threadIdx.x & 31;
-  if (g0 >= g1) return;
-  const uint32_t S1 = __ldg(ptr + g1);
+  if (g0 >= g1) return T(0);
+  const uint32_t S1 = P1;
   auto chunk_start = [&](uint32_t g) { return __ldg(ptr + min(g + lane, g1)); };
   auto chunk_end = [&](uint32_t g) { return __ldg(ptr + min(g + 32, g1)); };
   auto chunk_aux = [&](uint32_t g) { return aux && g + lane < g1 ? __ldg(aux + g + lane) : 0.f; };
@@ -83,7 +90,7 @@ __device__ __forceinline__ void segment_stream(const uint32_t* __restrict__ ptr,
     enter();
   };
   enter();
-  uint32_t pos = __shfl_sync(0xffffffffu, rpA, 0);
+  uint32_t pos = P0;
   T carry = T(0);
   uint8_t* f8 = reinterpret_cast<uint8_t*>(sc.flags);
 
@@ -186,6 +193,7 @@ __device__ __forceinline__ void segment_stream(const uint32_t* __restrict__ ptr,
   }
   // Trailing empty segments after the last element.
   while (gA + 32 < g1) advance();
+  return carry;
 }
 
 }  // namespace sgdb::dev

@@ -51,7 +51,11 @@ SHAPES = _shapes()
 
 @pytest.mark.parametrize("name", sorted(SHAPES))
 @pytest.mark.parametrize("d", [600, 100_000])
-def test_full_batch_gradient_segments(sgdb, dev, orc, name, d):
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_full_batch_gradient_segments(sgdb, dev, orc, name, d, split, monkeypatch):
+    """split=1: warps take equal nonzero ranges and rows cut by warp boundaries
+    are finished from per-warp pieces; split=0: whole rows per warp."""
+    monkeypatch.setenv("SGDB_SEG_SPLIT", split)
     S = sgdb
     lengths = [min(ln, d) for ln in SHAPES[name]]
     ds = _csr(S, lengths, d, seed=len(lengths) + d)
