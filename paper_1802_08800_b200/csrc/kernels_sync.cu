@@ -1041,7 +1041,7 @@ struct CscWin {
   uint2 r;
 };
 
-template <int G>
+template <int G, class ACC>
 __global__ void __launch_bounds__(1024, 1) csc_vec_kernel(
     const float* __restrict__ cval, const uint16_t* __restrict__ crow,
     const uint32_t* __restrict__ colptr, const float* __restrict__ coef, uint64_t n, uint32_t d,
@@ -1094,7 +1094,7 @@ __global__ void __launch_bounds__(1024, 1) csc_vec_kernel(
     t = fmaf(x1, cs[w.r.x >> 16], t);
     t = fmaf(x2, cs[w.r.y & 0xffffu], t);
     t = fmaf(x3, cs[w.r.y >> 16], t);
-    return static_cast<double>(t);
+    return static_cast<ACC>(t);
   };
   constexpr bool kThird = SPC < 8;
   RowChunk A = load_chunk(0), B = load_chunk(1), C;
@@ -1121,11 +1121,11 @@ __global__ void __launch_bounds__(1024, 1) csc_vec_kernel(
   };
   auto consume = [&](uint32_t s, const Stage<CscWin>& st) {
     const uint32_t a = (st.b & ~3u) + 4u * lg;
-    double acc = dot(st.g, a, st.b, st.e);
+    ACC acc = dot(st.g, a, st.b, st.e);
     for (uint32_t aa = a + 4 * G; aa < st.e; aa += 4 * G) acc += dot(window(aa), aa, st.b, st.e);
     acc = group_sum<G>(acc);
     const uint32_t j = c0 + s * CW + gi;
-    if (j < c1 && lg == 0) partials[static_cast<uint64_t>(b) * d + j] = acc;
+    if (j < c1 && lg == 0) partials[static_cast<uint64_t>(b) * d + j] = static_cast<double>(acc);
   };
   Stage<CscWin> s0, s1, s2;
   issue(0, s0);
@@ -1147,7 +1147,10 @@ __global__ void __launch_bounds__(1024, 1) csc_vec_kernel(
 // K3t: the gradient pass over the blocked CSC as a segmented warp stream:
 // CTA (block b, column range k) stages c[rows of b] in SMEM by bulk copy;
 // each warp streams the nonzeros of a contiguous column range (columns are
-// segments) in 128-slot tiles; fp32 products, fp64 segment sums.
+// segments) in 128-slot tiles. Used for short columns (a few slots per
+// block): fp32 products and fp32 segment sums (an fp64 scan was bound by
+// the FP64 / conversion pipes, ncu math_pipe_throttle), stored as fp64
+// partials.
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) csc_seg_kernel(
     const float* __restrict__ cval, const uint16_t* __restrict__ crow,
@@ -1156,7 +1159,7 @@ __global__ void __launch_bounds__(NT, 1) csc_seg_kernel(
   // Dynamic SMEM: [coefficient slice | per-warp scratch].
   extern __shared__ __align__(16) unsigned char dsm[];
   float* cs = reinterpret_cast<float*>(dsm);
-  auto* scratch = reinterpret_cast<SegScratch<double, kSegE>*>(dsm + round_up16(uint64_t(rb) * 4));
+  auto* scratch = reinterpret_cast<SegScratch<float, kSegE>*>(dsm + round_up16(uint64_t(rb) * 4));
   __shared__ uint64_t bar;
   const uint32_t b = blockIdx.x / cpb, k = blockIdx.x % cpb;
   if (b >= nblk) return;
@@ -1182,7 +1185,7 @@ __global__ void __launch_bounds__(NT, 1) csc_seg_kernel(
   const uint32_t* cp = colptr + static_cast<uint64_t>(b) * (d + 1);
   double* out = partials + static_cast<uint64_t>(b) * d;
   mbar_wait(&bar, 0);
-  segment_stream<double, kSegE, 2, CscWin>(
+  segment_stream<float, kSegE, 2, CscWin>(
       cp, nullptr, c0, c1, __ldg(cp + c0), __ldg(cp + c1),
       [&](uint32_t a, int q) {
         CscWin w;
@@ -1199,8 +1202,8 @@ __global__ void __launch_bounds__(NT, 1) csc_seg_kernel(
           p[4 * q + 3] = w[q].v.w * cs[w[q].r.y >> 16];
         }
       },
-      [&](uint32_t j, double v, float, bool ok) {
-        if (ok) out[j] = v;
+      [&](uint32_t j, float v, float, bool ok) {
+        if (ok) out[j] = static_cast<double>(v);
       },
       scratch[warp]);
 }
@@ -1643,7 +1646,8 @@ template <int G>
 void launch_csc_vec_G(Dataset& ds, Model& m) {
   Ctx& c = *ds.ctx;
   const size_t smem = round_up16(static_cast<uint64_t>(ds.csc_rb) * sizeof(float));
-  auto kern = csc_vec_kernel<G>;
+  // fp64 per-(block, column) sums (fp32 sums measured no faster: 85 vs 83 us on rcv1).
+  auto kern = csc_vec_kernel<G, double>;
   set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(csc_vec)");
   int per_sm = 0;
   per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), 1024, smem);
@@ -1713,7 +1717,7 @@ template <int NT>
 bool launch_csc_seg_N(Dataset& ds, Model& m) {
   Ctx& c = *ds.ctx;
   const size_t smem = round_up16(static_cast<uint64_t>(ds.csc_rb) * sizeof(float)) +
-                      (NT / 32) * sizeof(SegScratch<double, kSegE>);
+                      (NT / 32) * sizeof(SegScratch<float, kSegE>);
   auto kern = csc_seg_kernel<NT>;
   const size_t static_smem = static_smem_of(reinterpret_cast<const void*>(kern));
   if (static_smem + smem > c.max_smem_optin) return false;
@@ -1766,7 +1770,7 @@ void launch_apply_partials(Dataset& ds, Model& m, const StepArgs& a) {
   Ctx& c = *ds.ctx;
   // One coordinate per thread: each thread's 16-deep load batch is the only
   // memory parallelism this d-sized pass has.
-  const unsigned grid = grid_for(c, 256, ds.d, 16);
+  const unsigned grid = grid_for(c, 256, ds.d, 64);
   prof_begin(c, "apply_partials_kernel");
   apply_partials_kernel<<<grid, 256, 0, c.stream>>>(ds.d, ds.csc_nblk, m.partials.p, a.alpha,
                                                     a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p,

@@ -45,6 +45,8 @@ def main():
         name = target.split("_")[1]
         if name == "covtype":
             host, task = S.fixtures.dense_classification(581012, 54, 20250810), S.Task.LR
+        elif name == "news20":
+            host, task = S.fixtures.sparse_classification(19996, 1355191, 455.0, 20250814), S.Task.SVM
         elif name == "dense1000":
             host, task = S.fixtures.dense_classification(200000, 1000, 7), S.Task.LR
         else:
