@@ -125,12 +125,15 @@ __global__ void __launch_bounds__(32 * (WC + 1), 1) dense_full_kernel(DenseFullP
   }
   __syncthreads();
 
+  // Stage index and phase bit advance as counters (a runtime `i % S` cost a
+  // ~20-instruction division per tile per warp).
   if (warp == 0) {
     if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;  // phase of the ring pass this tile is in
       uint64_t i = 0;
       for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
-        const int s = static_cast<int>(i % p.S);
-        if (i >= (uint64_t)p.S) mbar_wait(&empty[s], static_cast<uint32_t>(((i / p.S) - 1) & 1));
+        if (i >= (uint64_t)p.S) mbar_wait(&empty[s], ph ^ 1u);
         const uint64_t r0 = t * p.R;
         const uint64_t rows = min(static_cast<uint64_t>(p.R), p.n - r0);
         const uint32_t xb = round_up16(rows * d * 4ull), yb = round_up16(rows * 4ull);
@@ -138,6 +141,10 @@ __global__ void __launch_bounds__(32 * (WC + 1), 1) dense_full_kernel(DenseFullP
         mbar_arrive_expect_tx(&full[s], xb + yb);
         bulk_g2s(st, p.x + r0 * d, xb, &full[s]);
         bulk_g2s(st + p.x_floats, p.y + r0, yb, &full[s]);
+        if (++s == p.S) {
+          s = 0;
+          ph ^= 1u;
+        }
       }
     }
   } else {
@@ -150,10 +157,10 @@ __global__ void __launch_bounds__(32 * (WC + 1), 1) dense_full_kernel(DenseFullP
       wr[k] = j < d ? p.w32[j] : 0.f;
       acc[k] = 0.f;
     }
-    uint64_t i = 0;
-    for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++i) {
-      const int s = static_cast<int>(i % p.S);
-      mbar_wait(&full[s], static_cast<uint32_t>((i / p.S) & 1));
+    int s = 0;
+    uint32_t ph = 0;
+    for (uint64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      mbar_wait(&full[s], ph);
       const float* xs = stages + (size_t)s * p.stage_floats;
       const float* ys = xs + p.x_floats;
       const int rows = static_cast<int>(min(static_cast<uint64_t>(p.R), p.n - t * p.R));
@@ -175,6 +182,10 @@ __global__ void __launch_bounds__(32 * (WC + 1), 1) dense_full_kernel(DenseFullP
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == p.S) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
 #pragma unroll
     for (int k = 0; k < F; ++k) acc[k] = cross_group_sum<L>(acc[k]);
