@@ -6,7 +6,7 @@ NCU="ncu --set full --clock-control none --import-source on"
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 5 --warmup 3 --no-cpu --no-convergence --no-extra > gpurun_out/bench_under_ncu.txt 2>&1
 $NCU -k regex:hogwild_kernel -s 3 -c 1 -f -o gpurun_out/ncu_hogwild python scripts/prof_targets.py hogwild_w8a 5 > /dev/null 2>&1
 $NCU -k regex:dense_full_kernel -s 2 -c 1 -f -o gpurun_out/ncu_c5 python scripts/prof_targets.py sync_c5 3 > /dev/null 2>&1
-$NCU -k regex:"csr_coef|csc_|apply_partials" -s 3 -c 3 -f -o gpurun_out/ncu_rcv1 python scripts/prof_targets.py sync_rcv1 3 > /dev/null 2>&1
+$NCU -k regex:"csr_coef|csc_|apply_partials" -s 4 -c 4 -f -o gpurun_out/ncu_rcv1 python scripts/prof_targets.py sync_rcv1 3 > /dev/null 2>&1
 $NCU -k regex:dense_full_kernel -s 2 -c 1 -f -o gpurun_out/ncu_covtype python scripts/prof_targets.py sync_covtype 3 > /dev/null 2>&1
 ls -la gpurun_out/*.ncu-rep
 # Summaries on the box (the raw reports are too large to bring back together).
