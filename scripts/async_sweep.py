@@ -28,7 +28,7 @@ CFG = {
     "realsim": (lambda: S.fixtures.sparse_classification(72309, 20958, 51.3, 20250812), S.Task.SVM, 1e-3,
                 ["row-rr:kernel:10", "row-ch:kernel:0"]),
     "covtype": (lambda: S.fixtures.dense_classification(581012, 54, 20250810), S.Task.LR, 1e-4,
-                ["row-ch:kernel:0", "row-rr:kernel:0"]),
+                ["row-ch:kernel:0", "row-rr:kernel:0", "row-ch:block:0"]),
 }
 
 
