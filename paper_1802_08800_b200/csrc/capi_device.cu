@@ -55,6 +55,10 @@ void csc_blocked_from_csr(uint64_t n, uint64_t d, const std::vector<uint32_t>& r
                           std::vector<uint16_t>& crow, std::vector<float>& cval) {
   const uint64_t nnz = idx.size();
   uint64_t want = std::clamp<uint64_t>((nnz * 2) / ((d + 1) * 4), 1, 16);
+  // A single block whenever its coefficient slice fits SMEM: the gradient
+  // kernels then apply the update straight from the column sums (no
+  // partials pass; news20: 19,996 rows).
+  if (n <= 49152) want = 1;
   want = std::max<uint64_t>(want, (n + 49151) / 49152);  // slice <= 192 KB of SMEM
   // rb % 4 == 0 keeps every block's coefficient slice 16-byte aligned (bulk copies).
   rb = static_cast<uint32_t>(std::max<uint64_t>(4, ((n + want - 1) / want + 3) & ~uint64_t(3)));

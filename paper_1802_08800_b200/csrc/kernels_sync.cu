@@ -1155,6 +1155,19 @@ __global__ void __launch_bounds__(1024, 1) csc_vec_kernel(
   }
 }
 
+// Update applied straight from the column sums when there is a single row
+// block (news20: 19,996 rows): no partials, no apply_partials_kernel.
+struct DirectApply {
+  int on;
+  double alpha;
+  int apply, want_norm;
+  double* w64;
+  float* w32;
+  double* g64;
+  int* finite;
+  double* norm2;
+};
+
 // K3t: the gradient pass over the blocked CSC as a segmented warp stream:
 // CTA (block b, column range k) stages c[rows of b] in SMEM by bulk copy;
 // each warp streams the nonzeros of a contiguous column range (columns are
@@ -1166,7 +1179,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT, 1) csc_seg_kernel(
     const float* __restrict__ cval, const uint16_t* __restrict__ crow,
     const uint32_t* __restrict__ colptr, const float* __restrict__ coef, uint64_t n, uint32_t d,
-    uint32_t rb, uint32_t nblk, uint32_t cpb, double* __restrict__ partials) {
+    uint32_t rb, uint32_t nblk, uint32_t cpb, double* __restrict__ partials, DirectApply da) {
   // Dynamic SMEM: [coefficient slice | per-warp scratch].
   extern __shared__ __align__(16) unsigned char dsm[];
   float* cs = reinterpret_cast<float*>(dsm);
@@ -1196,6 +1209,8 @@ __global__ void __launch_bounds__(NT, 1) csc_seg_kernel(
   const uint32_t* cp = colptr + static_cast<uint64_t>(b) * (d + 1);
   double* out = partials + static_cast<uint64_t>(b) * d;
   mbar_wait(&bar, 0);
+  int bad = 0;
+  double nrm = 0.0;
   segment_stream<float, kSegE, 2, CscWin>(
       cp, nullptr, c0, c1, __ldg(cp + c0), __ldg(cp + c1),
       [&](uint32_t a, int q) {
@@ -1214,9 +1229,32 @@ __global__ void __launch_bounds__(NT, 1) csc_seg_kernel(
         }
       },
       [&](uint32_t j, float v, float, bool ok) {
-        if (ok) out[j] = static_cast<double>(v);
+        if (!ok) return;
+        if (!da.on) {
+          out[j] = static_cast<double>(v);
+          return;
+        }
+        // One row block: this lane's sum IS g_j, so apply it here (K3f's
+        // arithmetic) instead of staging partials for a separate pass.
+        const double g = static_cast<double>(v);
+        if (!isfinite(g)) bad = 1;
+        if (da.apply) {
+          const double w = da.w64[j] - da.alpha * g;
+          da.w64[j] = w;
+          da.w32[j] = static_cast<float>(w);
+        } else {
+          da.g64[j] = g;
+        }
+        nrm += g * g;
       },
       scratch[warp]);
+  if (da.on) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) *da.finite = 0;
+    if (da.want_norm) {
+      nrm = warp_sum_d(nrm);
+      if (lane == 0 && nrm != 0.0) atomicAdd(da.norm2, nrm);
+    }
+  }
 }
 
 // K3f: g_j = sum_b partials[b][j] (fixed order), fused w -= alpha*g_j (one
@@ -1725,7 +1763,7 @@ bool launch_csr_coef_seg_N(Dataset& ds, Model& m) {
 }
 
 template <int NT>
-bool launch_csc_seg_N(Dataset& ds, Model& m) {
+bool launch_csc_seg_N(Dataset& ds, Model& m, const DirectApply& da) {
   Ctx& c = *ds.ctx;
   const size_t smem = round_up16(static_cast<uint64_t>(ds.csc_rb) * sizeof(float)) +
                       (NT / 32) * sizeof(SegScratch<float, kSegE>);
@@ -1742,7 +1780,7 @@ bool launch_csc_seg_N(Dataset& ds, Model& m) {
   prof_begin(c, "csc_grad_kernel");
   kern<<<cpb * ds.csc_nblk, NT, smem, c.stream>>>(ds.cval.p, ds.crow.p, ds.colptr.p, ds.coef.p, ds.n,
                                                   static_cast<uint32_t>(ds.d), ds.csc_rb,
-                                                  ds.csc_nblk, cpb, m.partials.p);
+                                                  ds.csc_nblk, cpb, m.partials.p, da);
   launched(c, "csc_grad_kernel");
   return true;
 }
@@ -1770,11 +1808,17 @@ void launch_csr_coef_seg(Dataset& ds, Model& m, bool smem_model) {
   if (!go.template operator()<false>()) throw CudaError("csr_coef_seg: no launchable configuration");
 }
 
-void launch_csc_seg(Dataset& ds, Model& m) {
+// Returns true when the update was applied in the kernel (one row block).
+bool launch_csc_seg(Dataset& ds, Model& m, const StepArgs& a) {
   const int nt = seg_threads();
-  if (nt >= 1024 && launch_csc_seg_N<1024>(ds, m)) return;
-  if (nt >= 768 && launch_csc_seg_N<768>(ds, m)) return;
-  if (!launch_csc_seg_N<512>(ds, m)) throw CudaError("csc_seg: no launchable configuration");
+  DirectApply da{};
+  if (ds.csc_nblk == 1)
+    da = DirectApply{1, a.alpha, a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p,
+                     m.finite.p, m.scal.p};
+  if (nt >= 1024 && launch_csc_seg_N<1024>(ds, m, da)) return da.on;
+  if (nt >= 768 && launch_csc_seg_N<768>(ds, m, da)) return da.on;
+  if (!launch_csc_seg_N<512>(ds, m, da)) throw CudaError("csc_seg: no launchable configuration");
+  return da.on;
 }
 
 void launch_apply_partials(Dataset& ds, Model& m, const StepArgs& a) {
@@ -1932,8 +1976,9 @@ void csr_full_step(Dataset& ds, Model& m, const StepArgs& a) {
   }();
   const bool aligned = ds.csc_rb % 4 == 0;
   const int mode = !aligned ? 0 : (csc_mode >= 0 ? csc_mode : (per_col < 12.0 ? 2 : 1));
+  bool applied = false;
   if (mode == 2) {
-    launch_csc_seg(ds, m);
+    applied = launch_csc_seg(ds, m, a);
   } else if (mode == 1) {
     // 4-slot windows: one window per lane group covers 4G slots of a column.
     const int gv = per_col <= 24.0 ? 4 : 8;
@@ -1941,7 +1986,7 @@ void csr_full_step(Dataset& ds, Model& m, const StepArgs& a) {
   } else {
     dispatch_G(env_lanes("SGDB_COL_LANES", gc), [&]<int G>() { launch_csc_block_G<G>(ds, m); });
   }
-  launch_apply_partials(ds, m, a);
+  if (!applied) launch_apply_partials(ds, m, a);
 }
 
 void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, const StepArgs& a) {
