@@ -490,29 +490,6 @@ __device__ __forceinline__ float gather_dot(const float* __restrict__ val,
   return z;
 }
 
-// ---------------------------------------------------------------------------
-// K2: sparse margins + coefficients for all local rows. G lanes per row,
-// coalesced val/idx, model gathered from L2 (d <= 1.4M floats stays resident).
-// ---------------------------------------------------------------------------
-template <int G, int TASK>
-__global__ void __launch_bounds__(256) csr_coef_kernel(const float* __restrict__ val,
-                                                       const uint32_t* __restrict__ idx,
-                                                       const uint32_t* __restrict__ rowptr,
-                                                       const float* __restrict__ y, uint64_t n,
-                                                       const float* __restrict__ w32,
-                                                       float* __restrict__ coef) {
-  constexpr int RW = 32 / G;
-  const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t base = gw * RW; base < n; base += tw * RW) {
-    const uint64_t row = base + grp;
-    float z = 0.f;
-    if (row < n) z = gather_dot<G>(val, idx, rowptr[row], rowptr[row + 1], lg, w32);
-    z = group_sum<G>(z);
-    if (row < n && lg == 0) coef[row] = coef_f<TASK>(z, y[row]);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // K2p: K2 with a 2-stage software pipeline across the rows a warp walks:
@@ -687,32 +664,6 @@ __global__ void __launch_bounds__(256) csr_coef_vec_kernel(
   }
 }
 
-// ---------------------------------------------------------------------------
-// K2s: margin pass with the fp32 model staged in shared memory (d <= ~56K
-// floats). Every model gather becomes an LDS — a 32-lane random gather costs
-// a few bank wavefronts — instead of one L1 tag lookup per lane, which is
-// what bounds K2v (l1tex ~79 %, one wavefront per nonzero). The model
-// arrives by bulk copy (1-D TMA) while the first rows' windows are already
-// in flight. Each warp walks a contiguous row range; G lanes per row read
-// aligned float4/uint4 windows of 4G slots; three rows deep (windows of rows
-// i+1, i+2 and the extent of row i+3 are in flight while row i reduces).
-// ---------------------------------------------------------------------------
-// Window dot product without divergence: slots outside [b, e) get x = 0
-// (their indices are still valid model coordinates — a neighbouring row's or
-// the zero slack — so the gathers stay in bounds).
-__device__ __forceinline__ float vec_dot_masked(const VecGroup& g, uint32_t a, uint32_t b, uint32_t e,
-                                                const float* w) {
-  const int lo = static_cast<int>(b - a), hi = static_cast<int>(e - a);
-  const float x0 = (0 >= lo && 0 < hi) ? g.v.x : 0.f;
-  const float x1 = (1 >= lo && 1 < hi) ? g.v.y : 0.f;
-  const float x2 = (2 >= lo && 2 < hi) ? g.v.z : 0.f;
-  const float x3 = (3 >= lo && 3 < hi) ? g.v.w : 0.f;
-  float z = x0 * w[g.j.x];
-  z = fmaf(x1, w[g.j.y], z);
-  z = fmaf(x2, w[g.j.z], z);
-  return fmaf(x3, w[g.j.w], z);
-}
-
 // Extents of a warp's contiguous row (or column) range, cached 32 at a time:
 // lane l holds the pointer (and label) of entry r0 + 32q + l, `end` the
 // pointer after the chunk. Extents are read with shuffles, so the only
@@ -730,90 +681,6 @@ struct Stage {
   W g;
 };
 
-template <int G, int TASK, int NT>
-__global__ void __launch_bounds__(NT, 1) csr_coef_smem_kernel(
-    const float* __restrict__ val, const uint32_t* __restrict__ idx,
-    const uint32_t* __restrict__ rowptr, const float* __restrict__ y, uint32_t n,
-    const float* __restrict__ w32, uint32_t d, float* __restrict__ coef) {
-  extern __shared__ __align__(16) float ws[];
-  __shared__ uint64_t bar;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-    const uint32_t total = round_up16(uint64_t(d) * 4);  // w32 is allocated in 16-byte groups
-    mbar_arrive_expect_tx(&bar, total);
-    for (uint32_t off = 0; off < total; off += 32768)
-      bulk_g2s(reinterpret_cast<char*>(ws) + off, reinterpret_cast<const char*>(w32) + off,
-               min(32768u, total - off), &bar);
-  }
-  constexpr uint32_t RW = 32 / G;   // rows per warp step
-  constexpr uint32_t SPC = 32 / RW;  // steps per 32-row chunk
-  const int lane = threadIdx.x & 31, lg = lane % G, gi = lane / G;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t r0 = static_cast<uint32_t>(uint64_t(n) * gw / nw);
-  const uint32_t r1 = static_cast<uint32_t>(uint64_t(n) * (gw + 1) / nw);
-  const uint32_t nsteps = (r1 - r0 + RW - 1) / RW;
-  auto load_chunk = [&](uint32_t q) {
-    RowChunk ch;
-    const uint32_t row = r0 + 32 * q + lane;
-    ch.rp = rowptr[min(row, r1)];
-    ch.y = row < r1 ? y[row] : 0.f;
-    ch.end = rowptr[min(r0 + 32 * q + 32, r1)];
-    return ch;
-  };
-  // Chunks qa (the issue front) and qa+1 are loaded (and qa+2 when a chunk
-  // is only a few steps long).
-  constexpr bool kThird = SPC < 8;
-  RowChunk A = load_chunk(0), B = load_chunk(1), C;
-  if constexpr (kThird) C = load_chunk(2);
-  uint32_t qa = 0;
-  auto issue = [&](uint32_t s, Stage<VecGroup>& st) {
-    if (s / SPC != qa) {  // warp-uniform; issue steps only move forward by one
-      A = B;
-      ++qa;
-      if constexpr (kThird) {
-        B = C;
-        C = load_chunk(qa + 2);
-      } else {
-        B = load_chunk(qa + 1);
-      }
-    }
-    const uint32_t l = (s % SPC) * RW + gi;
-    st.b = __shfl_sync(0xffffffffu, A.rp, l);
-    const uint32_t nx = __shfl_sync(0xffffffffu, A.rp, (l + 1) & 31);
-    st.y = __shfl_sync(0xffffffffu, A.y, l);
-    st.e = l == 31 ? A.end : nx;
-    if (s >= nsteps) st.e = st.b;
-    const uint32_t a = (st.b & ~3u) + 4u * lg;
-    st.g = vec_group(val, idx, a < st.e ? a : 0u);
-  };
-  auto consume = [&](uint32_t k, const Stage<VecGroup>& st) {
-    const uint32_t a = (st.b & ~3u) + 4u * lg;
-    float z = vec_dot_masked(st.g, a, st.b, st.e, ws);
-    for (uint32_t aa = a + 4 * G; aa < st.e; aa += 4 * G)
-      z += vec_dot_masked(vec_group(val, idx, aa), aa, st.b, st.e, ws);
-    z = group_sum<G>(z);
-    const uint32_t r = r0 + k * RW + gi;
-    if (r < r1 && lg == 0) coef[r] = coef_f<TASK>(z, st.y);
-  };
-  Stage<VecGroup> s0, s1, s2;
-  issue(0, s0);
-  issue(1, s1);
-  __syncthreads();  // barrier initialised before anyone polls it
-  mbar_wait(&bar, 0);
-  // Unrolled by the ring size, so the stages never move between registers.
-  for (uint32_t k = 0; k < nsteps; k += 3) {
-    issue(k + 2, s2);
-    consume(k, s0);
-    if (k + 1 >= nsteps) break;
-    issue(k + 3, s0);
-    consume(k + 1, s1);
-    if (k + 2 >= nsteps) break;
-    issue(k + 4, s1);
-    consume(k + 2, s2);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // K2t: margin pass as a segmented warp stream (segstream.cuh): each warp
@@ -1587,7 +1454,12 @@ void launch_dense_loss_LF(Dataset& ds, Model& m, int task) {
 // (L, F) per d: L lanes per row, F features per lane, L*F >= d.
 template <class Fn>
 void dispatch_dense(uint64_t d, Fn&& fn) {
+  static const bool lf416 = [] {
+    const char* e = std::getenv("SGDB_DENSE_LF416");
+    return e && std::atoi(e) != 0;
+  }();
   if (d <= 32) fn.template operator()<4, 8>();
+  else if (d <= 64 && lf416) fn.template operator()<4, 16>();
   else if (d <= 64) fn.template operator()<8, 8>();
   else if (d <= 128) fn.template operator()<16, 8>();
   else if (d <= 256) fn.template operator()<32, 8>();
@@ -1596,15 +1468,6 @@ void dispatch_dense(uint64_t d, Fn&& fn) {
   else throw Unsupported("dense kernels handle d <= 1024 (wider data is stored as CSR)");
 }
 
-template <int G, int TASK>
-void launch_csr_coef_G(Dataset& ds, Model& m) {
-  Ctx& c = *ds.ctx;
-  const unsigned grid = grid_for(c, 8ull * (32 / G) * 4, ds.n, 8);
-  prof_begin(c, "csr_coef_kernel");
-  csr_coef_kernel<G, TASK><<<grid, 256, 0, c.stream>>>(ds.val.p, ds.idx.p, ds.rowptr.p,
-                                                       ds.labels.p, ds.n, m.w32.p, ds.coef.p);
-  launched(c, "csr_coef_kernel");
-}
 
 template <int G, int TASK, bool SMEM>
 void launch_csr_coef_pipe_G(Dataset& ds, Model& m) {
@@ -1639,38 +1502,6 @@ void launch_csr_coef_vec(Dataset& ds, Model& m) {
   launched(c, "csr_coef_kernel");
 }
 
-template <int G, int TASK, int NT>
-void launch_csr_coef_smem_GN(Dataset& ds, Model& m) {
-  constexpr uint32_t kCoefSmemThreads = NT;
-  Ctx& c = *ds.ctx;
-  const size_t smem = round_up16(ds.d * sizeof(float));
-  auto kern = csr_coef_smem_kernel<G, TASK, NT>;
-  set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(csr_coef_smem)");
-  int per_sm = 0;
-  per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kCoefSmemThreads, smem);
-  const uint64_t want = (ds.n * G + kCoefSmemThreads - 1) / kCoefSmemThreads;
-  const unsigned grid = static_cast<unsigned>(
-      std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(std::max(1, per_sm)) * c.num_sms)));
-  prof_begin(c, "csr_coef_kernel");
-  kern<<<grid, kCoefSmemThreads, smem, c.stream>>>(ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p,
-                                                   static_cast<uint32_t>(ds.n), m.w32.p,
-                                                   static_cast<uint32_t>(ds.d), ds.coef.p);
-  launched(c, "csr_coef_kernel");
-}
-
-// CTA size: the model copy limits SMEM to one CTA per SM for large d, so the
-// thread count trades resident warps against registers per thread
-// (SGDB_COEF_THREADS = 1024 | 768 | 512; measured in scripts/sync_sweep.py).
-template <int G, int TASK>
-void launch_csr_coef_smem_G(Dataset& ds, Model& m) {
-  static const int nt = [] {
-    const char* e = std::getenv("SGDB_COEF_THREADS");
-    return e ? std::atoi(e) : 768;
-  }();
-  if (nt == 1024) launch_csr_coef_smem_GN<G, TASK, 1024>(ds, m);
-  else if (nt == 512) launch_csr_coef_smem_GN<G, TASK, 512>(ds, m);
-  else launch_csr_coef_smem_GN<G, TASK, 768>(ds, m);
-}
 
 template <int G>
 void launch_csc_block_G(Dataset& ds, Model& m) {
@@ -1912,48 +1743,30 @@ void csr_full_step(Dataset& ds, Model& m, const StepArgs& a) {
   build_csc(ds);
   if (ds.n > 0) {
     const int g = env_lanes("SGDB_ROW_LANES", lanes_for(static_cast<double>(ds.nnz) / static_cast<double>(ds.n)));
-    // SMEM staging of the model: opt-in (SGDB_COEF_SMEM=1); measured slower on
-    // rcv1 because one 189 KB CTA per SM halves the resident warps.
-    static const bool smem_pref = [] {
-      const char* e = std::getenv("SGDB_COEF_SMEM");
-      return e && std::atoi(e) == 1;
-    }();
-    const bool smem_model = smem_pref && ds.d * sizeof(float) <= 192 * 1024;
-    static const bool vec_pref = [] {
-      const char* e = std::getenv("SGDB_ROW_VEC");
-      return !e || std::atoi(e) != 0;
-    }();
-    // Model staged in SMEM with vector windows (K2s) whenever it fits
-    // (SGDB_COEF_SMEM=0 disables it for A/B runs).
-    static const int smem_env = [] {
-      const char* e = std::getenv("SGDB_COEF_SMEM");
-      return e ? std::atoi(e) : 2;
-    }();
+    // K2t (segmented warp stream; model in SMEM when it fits, SGDB_SEG_SMEM=0
+    // gathers it through L1 instead). SGDB_SEG=0 selects the lane-group
+    // kernels measured before it (K2v for 32 lanes, else K2p).
     static const bool seg = [] {
       const char* e = std::getenv("SGDB_SEG");
       return !e || std::atoi(e) != 0;
     }();
+    static const bool seg_smem = [] {
+      const char* e = std::getenv("SGDB_SEG_SMEM");
+      return !e || std::atoi(e) != 0;
+    }();
     const bool fits = round_up16(ds.d * sizeof(float)) + 8192 <= ds.ctx->max_smem_optin;
     if (seg) {
-      if (a.task == kTaskLR) launch_csr_coef_seg<kTaskLR>(ds, m, fits && smem_env != 0);
-      else launch_csr_coef_seg<kTaskSVM>(ds, m, fits && smem_env != 0);
-    } else if (smem_env == 2 && fits) {
-      dispatch_G(g, [&]<int G>() {
-        if (a.task == kTaskLR) launch_csr_coef_smem_G<G, kTaskLR>(ds, m);
-        else launch_csr_coef_smem_G<G, kTaskSVM>(ds, m);
-      });
-    } else if (g == 32 && vec_pref && !smem_model) {
+      if (a.task == kTaskLR) launch_csr_coef_seg<kTaskLR>(ds, m, fits && seg_smem);
+      else launch_csr_coef_seg<kTaskSVM>(ds, m, fits && seg_smem);
+    } else if (g == 32) {
       if (a.task == kTaskLR) launch_csr_coef_vec<kTaskLR>(ds, m);
       else launch_csr_coef_vec<kTaskSVM>(ds, m);
-    } else dispatch_G(g, [&]<int G>() {
-      if (smem_model) {
-        if (a.task == kTaskLR) launch_csr_coef_pipe_G<G, kTaskLR, true>(ds, m);
-        else launch_csr_coef_pipe_G<G, kTaskSVM, true>(ds, m);
-      } else {
+    } else {
+      dispatch_G(g, [&]<int G>() {
         if (a.task == kTaskLR) launch_csr_coef_pipe_G<G, kTaskLR, false>(ds, m);
         else launch_csr_coef_pipe_G<G, kTaskSVM, false>(ds, m);
-      }
-    });
+      });
+    }
   }
   const double per_col = static_cast<double>(ds.nnz) /
                          static_cast<double>(std::max<uint64_t>(1, ds.d) * std::max(1u, ds.csc_nblk));
