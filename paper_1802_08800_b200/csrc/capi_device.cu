@@ -328,7 +328,10 @@ sgdb_status sgdb_model_average_ranks(sgdb_ctx* ctx, sgdb_model* m, uint64_t worl
     dense_written(*m);
     call_allreduce(*ctx, m->w64.p, m->d, 1);
     scale_model(*m, 1.0 / static_cast<double>(world));
-    check(cudaStreamSynchronize(ctx->stream), "average_ranks sync");
+    // No host sync: the hook's collective is ordered on the context stream
+    // (NCCL through torch's current stream), so the next epoch's kernels see
+    // the averaged model; a per-average host round trip would stall every
+    // ~25 us epoch of the multi-GPU bench.
   });
 }
 
