@@ -283,7 +283,7 @@ def run_ours(args):
     # whole input from pinned host memory and reads its result back.
     copy_stream = torch.cuda.Stream()
     copy_dev = S.Device(local, stream=copy_stream.cuda_stream)
-    bufs = [dds, S.DeviceDataset(dev, host)]
+    bufs = [S.DeviceDataset(dev, host), S.DeviceDataset(dev, host)]  # dds keeps its CSC copy
     ready = [torch.cuda.Event(), torch.cuda.Event()]
     free = [torch.cuda.Event(), torch.cuda.Event()]
     used = [False, False]

@@ -224,7 +224,10 @@ sgdb_status sgdb_dataset_upload_ex(sgdb_ctx* ctx, const sgdb_dataset_view* view,
 /* Re-copy host arrays of the same shape into an existing device dataset
  * (the e2e leg of bench.py): fp32 values/labels straight from (pinned) host
  * buffers, asynchronously on the context stream. indices/row_offsets may be
- * NULL to keep the device copies. */
+ * NULL to keep the device copies. Refreshing a CSR dataset's values, indices
+ * or row offsets drops its row-blocked CSC copy: Hogwild and mini-batch sync
+ * keep working, full-batch sync then returns SGDB_ERR_UNSUPPORTED (upload
+ * again to rebuild it). */
 sgdb_status sgdb_dataset_refresh_f32(sgdb_ctx* ctx, sgdb_dataset* ds, const float* values,
                                      const float* labels, const uint32_t* indices,
                                      const uint32_t* row_offsets32);

@@ -494,6 +494,14 @@ sgdb_status sgdb_dataset_refresh_f32(sgdb_ctx* ctx, sgdb_dataset* ds, const floa
       if (values) h2d(ds->val.p, values, ds->nnz, s);
       if (indices) h2d(ds->idx.p, indices, ds->nnz, s);
       if (row_offsets32) h2d(ds->rowptr.p, row_offsets32, ds->n + 1, s);
+      if (values || indices || row_offsets32) {
+        // The row-blocked CSC copy (full-batch gradient pass) is built from
+        // the host arrays at upload and is not refreshed here: full-batch
+        // sparse sync on this dataset now fails loudly instead of reading
+        // stale values. The margin pass's warp partition is recomputed.
+        ds->csc_built = false;
+        ds->seg_nw = 0;
+      }
     }
   });
 }
