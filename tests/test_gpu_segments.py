@@ -81,3 +81,24 @@ def test_full_batch_epochs_segments(sgdb, dev, orc, name):
     for e in range(4):
         assert S.sync_epoch(dds, model, S.Task.LR, 0.05, None, ds.n_examples)
         assert rel_l2(model.get(), om[e]) <= 1e-5
+
+
+def test_refresh_drops_csc_copy(sgdb, dev):
+    """sgdb_dataset_refresh_f32 re-copies CSR arrays but not the row-blocked CSC
+    copy built at upload: full-batch sync must fail loudly afterwards (not read
+    stale values), while Hogwild and a fresh upload keep working."""
+    S = sgdb
+    ds = S.fixtures.sparse_classification(500, 80, 6.0, 31).rounded_f32()
+    dds = S.DeviceDataset(dev, ds)
+    model = S.DeviceModel(dev, ds.n_features)
+    assert S.sync_epoch(dds, model, S.Task.LR, 0.1, None, ds.n_examples)
+    new_vals = np.ascontiguousarray(ds.values.astype(np.float32) * 2.0)
+    dds.refresh_f32(new_vals)
+    dev.synchronize()
+    with pytest.raises(S.UnsupportedError):
+        S.sync_epoch(dds, model, S.Task.LR, 0.1, None, ds.n_examples)
+    plan = S.parse_plan("row-ch:kernel:0")
+    plan.workers = 4
+    S.hogwild_epoch(dds, model, S.Task.LR, 0.1, plan)
+    fresh = S.DeviceDataset(dev, ds)
+    assert S.sync_epoch(fresh, model, S.Task.LR, 0.1, None, ds.n_examples)
