@@ -629,7 +629,7 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
           !std::getenv("SGDB_NO_PERSISTENT_EPOCH") &&
           dense_epoch(*ds, *m, task, alpha, batch_b)) {
         // K1c: the whole epoch in one persistent launch
-      } else if (hook || ng / batch_b < 4) {
+      } else if (hook || ng / batch_b < 4 || std::getenv("SGDB_NO_EPOCH_GRAPH")) {
         run_steps(a);
       } else {
         // Launch-bound many-step epoch: replay a captured CUDA graph of the

@@ -1187,13 +1187,15 @@ __global__ void __launch_bounds__(256) csr_batch_kernel(
       valid = row < n_local;
     }
     uint32_t b = 0, e = 0;
-    if (valid) {
+    float yr = 0.f;
+    if (valid) {  // the label is loaded with the extent, off the margin's chain
       b = rowptr[row];
       e = rowptr[row + 1];
+      yr = y[row];
     }
     const float z = group_sum<G>(gather_dot<G>(val, idx, b, e, lg, w32));
     if (!valid) continue;
-    const float c = coef_f<TASK>(z, y[row]);
+    const float c = coef_f<TASK>(z, yr);
     if (c == 0.f) continue;
     for (uint32_t s = b + lg; s < e; s += G)
       atomicAdd(&g64[__ldg(idx + s)], static_cast<double>(c * __ldg(val + s)));
@@ -1667,7 +1669,11 @@ void launch_apply_partials(Dataset& ds, Model& m, const StepArgs& a) {
 template <int G, int TASK>
 void launch_csr_batch_G(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, bool check) {
   Ctx& c = *ds.ctx;
-  const unsigned grid = grid_for(c, 8ull * (32 / G) * 2, nb, 8);
+  // One row group per warp: each row is a chain of dependent loads (id ->
+  // extent -> slots -> model gather), so rows are spread over as many warps
+  // as the batch has, not walked two deep (rcv1 B = 4096: 24.9 -> see
+  // profiles/round1_sync_sweep.jsonl).
+  const unsigned grid = grid_for(c, 8ull * (32 / G), nb, 16);
   prof_begin(c, "csr_batch_kernel");
   csr_batch_kernel<G, TASK><<<grid, 256, 0, c.stream>>>(
       ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p, ds.n, ds.row_base, ids, nb, m.w32.p,
@@ -1813,7 +1819,8 @@ void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, con
 
 void apply_update(Model& m, double alpha, bool want_norm, const double* alpha_dev) {
   Ctx& c = *m.ctx;
-  const unsigned grid = grid_for(c, 256ull * 4, m.d, 8);
+  // One coordinate per thread (each iteration is a dependent load chain).
+  const unsigned grid = grid_for(c, 256, m.d, 64);
   prof_begin(c, "apply_kernel");
   apply_kernel<<<grid, 256, 0, c.stream>>>(m.d, alpha, alpha_dev, m.w64.p, m.w32.p, m.g64.p, m.finite.p,
                                            m.scal.p, want_norm ? 1 : 0);
