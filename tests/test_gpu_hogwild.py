@@ -263,3 +263,21 @@ def test_gpu_scale_workers_converge(sgdb, acceptance5, plan_text, workers, gs):
         if en is not None and (best is None or en < best):
             best = en
     assert best is not None and best <= 60
+
+
+@pytest.mark.parametrize("task", [0, 1])
+def test_long_rows_one_worker_equals_sequential(sgdb, dev, orc, task):
+    """Rows of hundreds of slots select the LONG kernel variant (two slot
+    batches per round trip, K5); one worker is still sequential
+    Alg. 3 (same tolerance as the other one-worker cases)."""
+    S = sgdb
+    ds = S.fixtures.sparse_classification(120, 3000, 400.0, 41).rounded_f32()
+    assert ds.values.size / ds.n_examples >= 256
+    plan = S.parse_plan("row-ch:kernel:0")
+    plan.workers = 1
+    hp = _inc(S, S.Task(task), 0.01, 3)
+    r = S.hogwild.train(S.Task(task), ds, hp, plan, 0, device=dev)
+    om, ol, _ = orc.hogwild_serial(ds, task, 0.01, 3, 0, 0, 0, 1)
+    for e in range(3):
+        assert rel(r.trace.epochs[e].loss, ol[e]) <= LOSS_TOL, (e, r.trace.epochs[e].loss, ol[e])
+    assert rel_l2(r.model, om[-1]) <= MODEL_TOL
