@@ -791,11 +791,15 @@ __global__ void __launch_bounds__(NT, 1) csr_coef_seg_kernel(
     P0 = __ldg(rowptr + g0);
     P1 = __ldg(rowptr + g1);
   }
-  if (SMEM) mbar_wait(&bar, 0);
   const float* w = SMEM ? ws : w32;
+  bool model_ready = !SMEM;  // the first tiles' loads overlap the model's bulk copy
   const float open = segment_stream<float, kSegE, 2, VecGroup>(
       rowptr, y, g0, g1, P0, P1, [&](uint32_t a, int k) { return vec_group(val, idx, a + 4 * k); },
       [&](const VecGroup (&g)[kSegE / 4], float* p) {
+        if (!model_ready) {
+          mbar_wait(&bar, 0);
+          model_ready = true;
+        }
 #pragma unroll
         for (int k = 0; k < kSegE / 4; ++k) {
           if (SMEM) {
