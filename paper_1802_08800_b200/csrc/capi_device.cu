@@ -607,12 +607,17 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
       const uint64_t ng = ds->n_global;
       if (order) {
         h2d(ds->order.p, order, ng, c.stream);
-      } else {
+        ds->order_iota = false;
+      } else if (!ds->order_iota) {  // identity order: uploaded once, kept
         std::vector<uint32_t> iota(ng);
         std::iota(iota.begin(), iota.end(), 0u);
         h2d(ds->order.p, iota.data(), ng, c.stream);
         check(cudaStreamSynchronize(c.stream), "order sync");
+        ds->order_iota = true;
       }
+      // Chunk plan of this epoch's order for the sparse steps (outside any
+      // captured graph: it may allocate; the graph re-reads it every replay).
+      if (ds->kind == Kind::Csr) csr_batch_plan(*ds, ds->order.p, ng, batch_b);
       auto run_steps = [&](const StepArgs& sa) {
         for (uint64_t lo = 0; lo < ng; lo += batch_b) {
           const uint64_t nb = std::min(batch_b, ng - lo);
@@ -704,8 +709,13 @@ sgdb_status sgdb_batch_gradient(sgdb_ctx* ctx, sgdb_dataset* ds, int32_t task,
       DBuf<uint32_t> ids;
       ids.alloc(n_rows);
       h2d(ids.p, rows, n_rows, c.stream);
-      if (ds->kind == Kind::Dense) dense_batch_step(*ds, tmp, ids.p, n_rows, a);
-      else csr_batch_step(*ds, tmp, ids.p, n_rows, a);
+      if (ds->kind == Kind::Dense) {
+        dense_batch_step(*ds, tmp, ids.p, n_rows, a);
+      } else {
+        csr_batch_plan(*ds, ids.p, n_rows, n_rows);
+        csr_batch_step(*ds, tmp, ids.p, n_rows, a);
+        ds->mb_ids = nullptr;  // the plan refers to this call's ids
+      }
       check(cudaStreamSynchronize(c.stream), "batch_gradient sync");
     }
     call_allreduce(c, tmp.g64.p, ds->d, 1);

@@ -149,6 +149,19 @@ struct Dataset {
   // Scratch.
   DBuf<float> coef;        // per local row coefficient (sparse full batch)
   DBuf<uint32_t> order;    // n_global ids of the current epoch
+  bool order_iota = false; // order holds 0..n_global-1 (sync_epoch with no order)
+  // Sparse mini-batch chunk plan (K3c): rows of ids[0..mb_count) cut into
+  // chunks of mb_ch slots; mb_off = exclusive prefix of the chunk counts
+  // (mb_count + 1 entries), mb_z = per-chunk partial margins of one step.
+  const uint32_t* mb_ids = nullptr;
+  uint64_t mb_count = 0;
+  uint32_t mb_ch = 0;
+  DBuf<uint32_t> mb_cnt, mb_off;
+  DBuf<uint4> mb_meta;     // per chunk {slot begin, slot end, position, local row}
+  uint64_t mb_cap = 0;     // chunks mb_meta holds (steps beyond it search mb_off)
+  DBuf<float> mb_z;
+  DBuf<unsigned char> mb_tmp;
+  size_t mb_tmp_bytes = 0;
   // Exact-fp64 mode (SGDB_UPLOAD_EXACT_FP64): fp64 copies of the values and
   // the scratch of the reference-order kernels (kernels_linalg.cu).
   bool exact = false;
@@ -213,7 +226,12 @@ void dense_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb,
                       const StepArgs& a);
 // Sparse, all local rows: margin/coef pass + CSC gradient pass.
 void csr_full_step(Dataset& ds, Model& m, const StepArgs& a);
-// Sparse mini-batch: scatter with fp64 atomics, then apply.
+// Sparse mini-batch: chunk plan of the ids a sequence of steps walks (device
+// ids[0..count), steps of at most max_step positions); steps whose ids lie
+// outside the current plan build their own.
+void csr_batch_plan(Dataset& ds, const uint32_t* ids, uint64_t count, uint64_t max_step);
+// Sparse mini-batch step: chunk margins, then coefficient + scatter with fp64
+// atomics, then apply.
 void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, const StepArgs& a);
 // w -= alpha*g64; w32 = w64; finite; g64 = 0. alpha_dev (if set) overrides alpha.
 void apply_update(Model& m, double alpha, bool want_norm, const double* alpha_dev = nullptr);

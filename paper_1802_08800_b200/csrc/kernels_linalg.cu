@@ -600,6 +600,7 @@ void exact_sync_epoch(Dataset& ds, Model& m, int task, double alpha, const uint3
   check(cudaMemcpyAsync(ds.order.p, ord.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice,
                         c.stream),
         "H2D order");
+  ds.order_iota = false;
   ds.ex_live.alloc(1);
   for (uint64_t lo = 0; lo < n; lo += batch_b) {
     const uint64_t nb = std::min(batch_b, n - lo);

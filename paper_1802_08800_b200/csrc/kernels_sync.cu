@@ -14,6 +14,8 @@
 
 #include "common.cuh"
 #include "segstream.cuh"
+#include <cub/cub.cuh>
+
 #include "device.hpp"
 
 namespace sgdb::dev {
@@ -1244,8 +1246,187 @@ __global__ void __launch_bounds__(256) csr_batch_kernel(
     if (!valid) continue;
     const float c = coef_f<TASK>(z, yr);
     if (c == 0.f) continue;
-    for (uint32_t s = b + lg; s < e; s += G)
-      atomicAdd(&g64[__ldg(idx + s)], static_cast<double>(c * __ldg(val + s)));
+    // Slots in batches of U: the U loads are in flight together instead of
+    // one load -> red round trip per slot (ncu: 79 % long-scoreboard on the
+    // one-deep loop, news20 B = 4096).
+    constexpr int U = 8;
+    for (uint32_t s0 = b + lg; s0 < e; s0 += G * U) {
+      uint32_t jv[U];
+      float xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t s = s0 + u * G;
+        jv[u] = s < e ? __ldg(idx + s) : 0u;
+        xv[u] = s < e ? __ldg(val + s) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (s0 + u * G < e) atomicAdd(&g64[jv[u]], static_cast<double>(c * xv[u]));
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// K3c: sparse mini-batch in row chunks. A batch's rows are heavy-tailed (the
+// longest of 4,096 rcv1 rows is ~18x the mean, news20 ~20x), and with one
+// lane group per row the step lasted as long as its longest row's load chain
+// (news20: 85 us for 1.9M slots). The rows are cut into chunks of CH = G*8
+// slots; the plan (per epoch: chunk counts + exclusive scan over the order)
+// lets every lane group take one chunk:
+//   K3c-m: partial margin of each chunk -> mb_z (one slot per chunk);
+//   K3c-s: the row margin = its chunks' partials summed in chunk order
+//          (deterministic), coefficient, scatter of the chunk's c*x into g64
+//          with fp64 atomics (red.global.add.f64).
+// ---------------------------------------------------------------------------
+__global__ void mb_count_kernel(const uint32_t* __restrict__ ids, uint64_t count,
+                                const uint32_t* __restrict__ rowptr, uint64_t n_local,
+                                uint64_t row_base, uint32_t ch, uint32_t* __restrict__ cnt) {
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p <= count;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t k = 0;
+    if (p < count) {
+      const uint64_t row = static_cast<uint64_t>(ids[p]) - row_base;  // wraps if not local
+      if (row < n_local) k = (rowptr[row + 1] - rowptr[row] + ch - 1) / ch;
+    }
+    cnt[p] = k;
+  }
+}
+
+// Largest p in [lo, hi) with off[p] <= q (off[lo] <= q < off[hi]): the
+// position owning chunk q (positions with no chunk share their successor's
+// offset and are skipped).
+__device__ __forceinline__ uint64_t chunk_owner(const uint32_t* __restrict__ off, uint64_t lo,
+                                                uint64_t hi, uint32_t q) {
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (__ldg(off + mid) <= q) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+struct ChunkRef {
+  uint64_t p = 0, row = 0;
+  uint32_t b = 0, e = 0;
+};
+
+// Chunk q of the plan: one 16-byte load from the per-chunk table when the
+// plan holds it (every permutation order), else the owner search.
+template <int G, int U>
+__device__ __forceinline__ ChunkRef chunk_ref(const uint4* __restrict__ meta, uint64_t cap,
+                                              const uint32_t* __restrict__ off,
+                                              const uint32_t* __restrict__ ids,
+                                              const uint32_t* __restrict__ rowptr, uint64_t row_base,
+                                              uint64_t lo, uint64_t hi, uint32_t q, bool direct) {
+  ChunkRef r;
+  if (direct) {
+    const uint4 m = __ldg(meta + q);
+    r.b = m.x;
+    r.e = m.y;
+    r.p = m.z;
+    r.row = m.w;
+    return r;
+  }
+  r.p = chunk_owner(off, lo, hi, q);
+  const uint32_t sub = q - __ldg(off + r.p);
+  r.row = static_cast<uint64_t>(__ldg(ids + r.p)) - row_base;
+  const uint32_t rb = __ldg(rowptr + r.row), re = __ldg(rowptr + r.row + 1);
+  r.b = rb + sub * static_cast<uint32_t>(G * U);
+  r.e = min(r.b + static_cast<uint32_t>(G * U), re);
+  return r;
+}
+
+__global__ void mb_fill_kernel(const uint32_t* __restrict__ ids, uint64_t count,
+                               const uint32_t* __restrict__ rowptr, uint64_t row_base, uint32_t ch,
+                               const uint32_t* __restrict__ off, uint4* __restrict__ meta,
+                               uint64_t cap) {
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < count;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q0 = off[p], q1 = off[p + 1];
+    if (q0 == q1) continue;
+    const uint32_t row = static_cast<uint32_t>(static_cast<uint64_t>(ids[p]) - row_base);
+    const uint32_t rb = rowptr[row], re = rowptr[row + 1];
+    for (uint32_t q = q0; q < q1 && q < cap; ++q) {
+      const uint32_t b = rb + (q - q0) * ch;
+      meta[q] = make_uint4(b, min(b + ch, re), static_cast<uint32_t>(p), row);
+    }
+  }
+}
+
+template <int G, int U>
+__global__ void __launch_bounds__(256) mb_margin_kernel(
+    const float* __restrict__ val, const uint32_t* __restrict__ idx,
+    const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ ids,
+    const uint32_t* __restrict__ off, const uint4* __restrict__ meta, uint64_t cap, uint64_t lo,
+    uint64_t hi, uint64_t row_base, const float* __restrict__ w32, float* __restrict__ zpart,
+    const int* finite, int check_finite) {
+  if (check_finite && *finite == 0) return;
+  constexpr int RW = 32 / G;
+  const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
+  const uint32_t c0 = __ldg(off + lo), c1 = __ldg(off + hi);
+  const bool direct = c1 <= cap;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t base = c0 + gw * RW; base < c1; base += tw * RW) {
+    const uint64_t q = base + grp;
+    const bool valid = q < c1;
+    uint32_t b = 0, e = 0;
+    if (valid) {
+      const ChunkRef r = chunk_ref<G, U>(meta, cap, off, ids, rowptr, row_base, lo, hi,
+                                         static_cast<uint32_t>(q), direct);
+      b = r.b;
+      e = r.e;
+    }
+    uint32_t jv[U];
+    float xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t s = b + lg + u * G;
+      jv[u] = s < e ? __ldg(idx + s) : 0u;
+      xv[u] = s < e ? __ldg(val + s) : 0.f;
+    }
+    float z = 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) z = fmaf(xv[u], b + lg + u * G < e ? __ldg(w32 + jv[u]) : 0.f, z);
+    z = group_sum<G>(z);
+    if (valid && lg == 0) zpart[q - c0] = z;
+  }
+}
+
+template <int G, int U, int TASK>
+__global__ void __launch_bounds__(256) mb_scatter_kernel(
+    const float* __restrict__ val, const uint32_t* __restrict__ idx,
+    const uint32_t* __restrict__ rowptr, const float* __restrict__ y,
+    const uint32_t* __restrict__ ids, const uint32_t* __restrict__ off,
+    const uint4* __restrict__ meta, uint64_t cap, uint64_t lo, uint64_t hi, uint64_t row_base,
+    const float* __restrict__ zpart, double* g64, const int* finite, int check_finite) {
+  if (check_finite && *finite == 0) return;
+  constexpr int RW = 32 / G;
+  const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
+  const uint32_t c0 = __ldg(off + lo), c1 = __ldg(off + hi);
+  const bool direct = c1 <= cap;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t q = c0 + gw * RW + grp; q < c1; q += tw * RW) {  // no shuffles: per group
+    const ChunkRef r = chunk_ref<G, U>(meta, cap, off, ids, rowptr, row_base, lo, hi,
+                                       static_cast<uint32_t>(q), direct);
+    uint32_t jv[U];
+    float xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // the chunk's slots load while the margin is summed
+      const uint32_t s = r.b + lg + u * G;
+      jv[u] = s < r.e ? __ldg(idx + s) : 0u;
+      xv[u] = s < r.e ? __ldg(val + s) : 0.f;
+    }
+    const uint32_t z0 = __ldg(off + r.p) - c0, z1 = __ldg(off + r.p + 1) - c0;
+    float z = 0.f;
+    for (uint32_t k = z0; k < z1; ++k) z += __ldg(zpart + k);  // chunk order
+    const float c = coef_f<TASK>(z, __ldg(y + r.row));
+    if (c == 0.f) continue;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (r.b + lg + u * G < r.e) atomicAdd(&g64[jv[u]], static_cast<double>(c * xv[u]));
   }
 }
 
@@ -1855,12 +2036,102 @@ void csr_full_step(Dataset& ds, Model& m, const StepArgs& a) {
   if (!applied) launch_apply_partials(ds, m, a);
 }
 
+namespace {
+constexpr int kChunkU = 8;  // slots per lane per chunk (CH = G * kChunkU)
+
+int batch_lanes(const Dataset& ds) {
+  return env_lanes("SGDB_BATCH_LANES",
+                   lanes_for(ds.n ? static_cast<double>(ds.nnz) / static_cast<double>(ds.n) : 1.0));
+}
+
+bool chunked_batches() {
+  static const bool on = [] {
+    const char* e = std::getenv("SGDB_BATCH_CHUNKS");  // 0 = one lane group per row (K3b)
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
+template <int G, int TASK>
+void launch_mb_chunks(Dataset& ds, Model& m, uint64_t lo, uint64_t nb, bool check) {
+  Ctx& c = *ds.ctx;
+  constexpr int RW = 32 / G;
+  // Chunks of one step: the rows plus one per CH slots of their mean length.
+  const double avg = ds.n ? static_cast<double>(ds.nnz) / static_cast<double>(ds.n) : 1.0;
+  const uint64_t est = nb + static_cast<uint64_t>(nb * avg / (G * kChunkU));
+  const unsigned grid = grid_for(c, 8ull * RW, est, 16);
+  const uint64_t hi = lo + nb;
+  prof_begin(c, "mb_margin_kernel");
+  mb_margin_kernel<G, kChunkU><<<grid, 256, 0, c.stream>>>(
+      ds.val.p, ds.idx.p, ds.rowptr.p, ds.mb_ids, ds.mb_off.p, ds.mb_meta.p, ds.mb_cap, lo, hi,
+      ds.row_base, m.w32.p, ds.mb_z.p, m.finite.p, check ? 1 : 0);
+  launched(c, "mb_margin_kernel");
+  prof_begin(c, "mb_scatter_kernel");
+  mb_scatter_kernel<G, kChunkU, TASK><<<grid, 256, 0, c.stream>>>(
+      ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p, ds.mb_ids, ds.mb_off.p, ds.mb_meta.p,
+      ds.mb_cap, lo, hi, ds.row_base, ds.mb_z.p, m.g64.p, m.finite.p, check ? 1 : 0);
+  launched(c, "mb_scatter_kernel");
+}
+}  // namespace
+
+void csr_batch_plan(Dataset& ds, const uint32_t* ids, uint64_t count, uint64_t max_step) {
+  if (!chunked_batches() || count == 0) return;
+  Ctx& c = *ds.ctx;
+  const uint32_t ch = static_cast<uint32_t>(batch_lanes(ds) * kChunkU);
+  const uint64_t per_row = ds.max_row ? (ds.max_row + ch - 1) / ch : 1;
+  const uint64_t zcap = std::min(max_step, count) * per_row;
+  // Chunk table: every chunk of a permutation order (sum over the local rows
+  // of ceil(len / ch) <= nnz / ch + n); larger plans (repeated ids) search.
+  const uint64_t cap = std::min<uint64_t>(count * per_row, ds.nnz / ch + ds.n + 1);
+  const bool grow = !ds.mb_cnt.p || ds.mb_cnt.n < count + 1 || ds.mb_z.n < zcap ||
+                    ds.mb_meta.n < cap;
+  ds.mb_cnt.alloc(count + 1);
+  ds.mb_off.alloc(count + 1);
+  ds.mb_z.alloc(std::max<uint64_t>(1, zcap));
+  ds.mb_meta.alloc(std::max<uint64_t>(1, cap));
+  ds.mb_cap = cap;
+  size_t bytes = 0;
+  check(cub::DeviceScan::ExclusiveSum(nullptr, bytes, ds.mb_cnt.p, ds.mb_off.p,
+                                      static_cast<int64_t>(count + 1), c.stream),
+        "cub scan size");
+  if (bytes > ds.mb_tmp.n) ds.mb_tmp.alloc(bytes);
+  // New buffers invalidate epoch graphs captured against the old ones.
+  if (grow) ds.uid = next_dataset_uid();
+  const unsigned grid = grid_for(c, 256, count + 1, 8);
+  prof_begin(c, "mb_count_kernel");
+  mb_count_kernel<<<grid, 256, 0, c.stream>>>(ids, count, ds.rowptr.p, ds.n, ds.row_base, ch,
+                                              ds.mb_cnt.p);
+  launched(c, "mb_count_kernel");
+  bytes = ds.mb_tmp.n;
+  check(cub::DeviceScan::ExclusiveSum(ds.mb_tmp.p, bytes, ds.mb_cnt.p, ds.mb_off.p,
+                                      static_cast<int64_t>(count + 1), c.stream),
+        "cub scan");
+  prof_begin(c, "mb_fill_kernel");
+  mb_fill_kernel<<<grid, 256, 0, c.stream>>>(ids, count, ds.rowptr.p, ds.row_base, ch, ds.mb_off.p,
+                                             ds.mb_meta.p, cap);
+  launched(c, "mb_fill_kernel");
+  ds.mb_ids = ids;
+  ds.mb_count = count;
+  ds.mb_ch = ch;
+}
+
 void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, const StepArgs& a) {
-  const int g = lanes_for(ds.n ? static_cast<double>(ds.nnz) / static_cast<double>(ds.n) : 1.0);
-  dispatch_G(g, [&]<int G>() {
-    if (a.task == kTaskLR) launch_csr_batch_G<G, kTaskLR>(ds, m, ids, nb, a.apply);
-    else launch_csr_batch_G<G, kTaskSVM>(ds, m, ids, nb, a.apply);
-  });
+  const int g = batch_lanes(ds);
+  if (chunked_batches()) {
+    if (!(ds.mb_ids && ids >= ds.mb_ids && ids + nb <= ds.mb_ids + ds.mb_count &&
+          ds.mb_ch == static_cast<uint32_t>(g * kChunkU)))
+      csr_batch_plan(ds, ids, nb, nb);
+    const uint64_t lo = static_cast<uint64_t>(ids - ds.mb_ids);
+    dispatch_G(g, [&]<int G>() {
+      if (a.task == kTaskLR) launch_mb_chunks<G, kTaskLR>(ds, m, lo, nb, a.apply);
+      else launch_mb_chunks<G, kTaskSVM>(ds, m, lo, nb, a.apply);
+    });
+  } else {
+    dispatch_G(g, [&]<int G>() {
+      if (a.task == kTaskLR) launch_csr_batch_G<G, kTaskLR>(ds, m, ids, nb, a.apply);
+      else launch_csr_batch_G<G, kTaskSVM>(ds, m, ids, nb, a.apply);
+    });
+  }
   if (a.apply) apply_update(m, a.alpha, a.want_norm, a.alpha_dev);
 }
 

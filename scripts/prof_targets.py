@@ -1,6 +1,6 @@
 """Small driver for ncu captures: runs a few epochs of one target op.
 
-    python scripts/prof_targets.py {hogwild_w8a|hogwild_rcv1_block|sync_covtype|sync_rcv1|sync_dense1000|sync_c5} [epochs]
+    python scripts/prof_targets.py {hogwild_w8a|hogwild_rcv1_block|sync_covtype|sync_rcv1|sync_realsim|sync_news20|sync_dense1000|sync_c5} [epochs]
 """
 import os
 import sys
@@ -47,6 +47,8 @@ def main():
             host, task = S.fixtures.dense_classification(581012, 54, 20250810), S.Task.LR
         elif name == "news20":
             host, task = S.fixtures.sparse_classification(19996, 1355191, 455.0, 20250814), S.Task.SVM
+        elif name == "realsim":
+            host, task = S.fixtures.sparse_classification(72309, 20958, 51.3, 20250812), S.Task.SVM
         elif name == "dense1000":
             host, task = S.fixtures.dense_classification(200000, 1000, 7), S.Task.LR
         else:

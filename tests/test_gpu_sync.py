@@ -252,3 +252,52 @@ def test_padded_and_colmajor_inputs(sgdb, dev, orc):
         ra = S.sync.train(S.Task.LR, a, hp, 5, device=dev)
         rb = S.sync.train(S.Task.LR, b, hp, 5, device=dev)
         assert rel_l2(ra.model, rb.model) <= 1e-6
+
+
+def _heavy_tailed(S, n, d, seed):
+    """CSR rows with a heavy tail (a few rows many chunks long) and empty rows:
+    the chunked mini-batch kernels (K3c) cut rows into chunks of G*8 slots."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, 40, n)
+    lens[rng.choice(n, 6, replace=False)] = rng.integers(600, 3000, 6)
+    lens[rng.choice(n, 25, replace=False)] = 0
+    idx, val, offs = [], [], [0]
+    for ln in lens:
+        cols = np.sort(rng.choice(d, int(ln), replace=False))
+        idx.extend(cols.tolist())
+        val.extend(rng.normal(0, 0.5, int(ln)).tolist())
+        offs.append(len(idx))
+    labels = np.where(rng.random(n) < 0.5, 1.0, -1.0)
+    return S.Dataset(n, d, S.Layout.Csr, labels, np.array(val), np.array(idx, np.uint32),
+                     np.array(offs, np.uint64)).rounded_f32()
+
+
+@pytest.mark.parametrize("batch", [37, 256])
+@pytest.mark.parametrize("task", [0, 1])
+def test_minibatch_heavy_tailed_rows(sgdb, dev, orc, batch, task):
+    S = sgdb
+    ds = _heavy_tailed(S, 1500, 5000, 29 + task)
+    alpha = 0.5 / batch
+    gm, gl = _run_epochs(S, dev, ds, S.Task(task), alpha, batch, 4, seed=3)
+    om, ol, div = orc.sync_train(ds, task, alpha, batch, 4, 3)
+    assert not div
+    for e in range(4):
+        assert rel_l2(gm[e], om[e]) <= MODEL_TOL, (e, rel_l2(gm[e], om[e]))
+        assert rel(gl[e], ol[e]) <= LOSS_TOL, (e, gl[e], ol[e])
+
+
+def test_minibatch_heavy_tailed_batch_gradient_repeats(sgdb, dev, orc):
+    """Operator API with repeated and unsorted ids over heavy-tailed rows."""
+    S = sgdb
+    ds = _heavy_tailed(S, 900, 3000, 41)
+    rng = np.random.default_rng(5)
+    w = rng.normal(0, 0.2, ds.n_features)
+    lens = np.diff(ds.row_offsets.astype(np.int64))
+    heavy = np.argsort(lens)[-3:].astype(np.uint32)
+    # random repeats (fits the per-chunk table) and the longest rows repeated
+    # past the table's capacity (the kernels fall back to the owner search)
+    for rows in (rng.integers(0, ds.n_examples, 700).astype(np.uint32), np.tile(heavy, 150)):
+        for task in (0, 1):
+            g = S.sync.batch_gradient(S.Task(task), ds, rows, w, device=dev)
+            og = orc.batch_gradient(ds, task, rows, w)
+            assert rel_l2(g, og) <= 1e-5
