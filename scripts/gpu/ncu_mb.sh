@@ -1,6 +1,8 @@
-# ncu --set full of the sparse mini-batch step kernels (news20 / rcv1 shapes, B = 4096)
+# ncu --set full of the sparse mini-batch step kernels (K3c) on the rcv1 / news20 shapes, B = 4096
 mkdir -p gpurun_out
 NCU="ncu --set full --clock-control none --import-source on"
-$NCU -k regex:"csr_batch|apply_kernel" -s 6 -c 2 -f -o gpurun_out/ncu_mb_news20 python scripts/sync_sweep.py news20 > gpurun_out/ncu_mb.log 2>&1
-python scripts/ncu_summary.py gpurun_out/ncu_mb_news20.ncu-rep > gpurun_out/ncu_mb_news20.txt 2>&1
-ncu -i gpurun_out/ncu_mb_news20.ncu-rep --page source --csv -k regex:csr_batch > gpurun_out/ncu_mb_news20_src.csv 2>&1
+for shape in rcv1 news20; do
+  $NCU -k regex:"mb_margin|mb_scatter|apply_kernel" -s 30 -c 3 -f -o gpurun_out/ncu_mb_$shape python scripts/sync_sweep.py $shape > gpurun_out/ncu_mb_$shape.log 2>&1
+  python scripts/ncu_summary.py gpurun_out/ncu_mb_$shape.ncu-rep > gpurun_out/ncu_mb_$shape.txt 2>&1
+  rm -f gpurun_out/ncu_mb_$shape.ncu-rep
+done
