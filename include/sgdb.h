@@ -231,6 +231,12 @@ sgdb_status sgdb_dataset_upload_ex(sgdb_ctx* ctx, const sgdb_dataset_view* view,
 sgdb_status sgdb_dataset_refresh_f32(sgdb_ctx* ctx, sgdb_dataset* ds, const float* values,
                                      const float* labels, const uint32_t* indices,
                                      const uint32_t* row_offsets32);
+/* Compact transfer of the column ids of a CSR dataset with d <= 65536: nnz
+ * 16-bit ids copied host -> device on ctx's stream and widened there to the
+ * 32-bit ids the kernels read (half the index bytes over PCIe). Same
+ * invalidation as sgdb_dataset_refresh_f32. Not in the reference API (its
+ * datasets live in host memory); it serves hosts that stream inputs. */
+sgdb_status sgdb_dataset_refresh_idx16(sgdb_ctx* ctx, sgdb_dataset* ds, const uint16_t* indices16);
 sgdb_status sgdb_dataset_free(sgdb_dataset* ds);
 /* K9: generate a dense synthetic classification shard on the device (rows
  * [row_base, row_base + n_local) of an n_global x d dataset) — the

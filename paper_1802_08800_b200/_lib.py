@@ -80,6 +80,7 @@ PROTOTYPES = {
     "sgdb_dataset_upload": (_S, [vp, P(DatasetView), u64, u64, P(vp)]),
     "sgdb_dataset_upload_ex": (_S, [vp, P(DatasetView), u64, u64, u32, P(vp)]),
     "sgdb_dataset_refresh_f32": (_S, [vp, vp, vp, vp, vp, vp]),
+    "sgdb_dataset_refresh_idx16": (_S, [vp, vp, vp]),
     "sgdb_dataset_free": (_S, [vp]),
     "sgdb_dataset_generate_dense": (_S, [vp, u64, u64, u64, u64, u64, dbl, P(vp)]),
     "sgdb_generate_hidden_model": (_S, [u64, u64, P(dbl)]),

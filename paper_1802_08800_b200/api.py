@@ -507,6 +507,12 @@ class DeviceDataset:
         check(_lib().sgdb_dataset_refresh_f32(ctx, self._h, p(values), p(labels), p(indices),
                                               p(row_offsets32)))
 
+    def refresh_idx16(self, indices16, device: Optional[Device] = None):
+        """Async H2D copy of 16-bit column ids (d <= 65536), widened on the device
+        (sgdb_dataset_refresh_idx16); same stream rules as refresh_f32."""
+        ptr = indices16.data_ptr() if hasattr(indices16, "data_ptr") else indices16.ctypes.data
+        check(_lib().sgdb_dataset_refresh_idx16((device or self.dev).handle, self._h, ptr))
+
     def close(self):
         if getattr(self, "_h", None):
             _lib().sgdb_dataset_free(self._h)

@@ -506,6 +506,20 @@ sgdb_status sgdb_dataset_refresh_f32(sgdb_ctx* ctx, sgdb_dataset* ds, const floa
   });
 }
 
+sgdb_status sgdb_dataset_refresh_idx16(sgdb_ctx* ctx, sgdb_dataset* ds, const uint16_t* indices16) {
+  return sgdb_guard([&] {
+    require(ctx && ds && indices16, "null argument");
+    require(ds->kind == Kind::Csr, "refresh_idx16: the dataset is not stored as CSR");
+    require(ds->d <= 65536, "refresh_idx16: column ids need d <= 65536");
+    cudaStream_t s = ctx->stream;
+    ds->idx16.alloc(ds->nnz + 8);
+    h2d(ds->idx16.p, indices16, ds->nnz, s);
+    widen_u16(*ctx, ds->idx16.p, ds->idx.p, ds->nnz);
+    ds->csc_built = false;  // as sgdb_dataset_refresh_f32
+    ds->seg_nw = 0;
+  });
+}
+
 sgdb_status sgdb_dataset_free(sgdb_dataset* ds) {
   return sgdb_guard([&] {
     if (!ds) return;

@@ -114,6 +114,7 @@ struct Dataset {
   DBuf<float> val;
   DBuf<uint32_t> idx;
   DBuf<uint32_t> rowptr;
+  DBuf<uint16_t> idx16;  // staging for sgdb_dataset_refresh_idx16
   // Row-blocked CSC of the local rows (full-batch sparse gradients): rows are
   // split into csc_nblk blocks of csc_rb (< 2^16) rows; block b holds its
   // columns back to back, colptr[b*(d+1) + j] are global offsets, row ids
@@ -235,6 +236,8 @@ void csr_batch_plan(Dataset& ds, const uint32_t* ids, uint64_t count, uint64_t m
 void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, const StepArgs& a);
 // w -= alpha*g64; w32 = w64; finite; g64 = 0. alpha_dev (if set) overrides alpha.
 void apply_update(Model& m, double alpha, bool want_norm, const double* alpha_dev = nullptr);
+// dst[i] = src[i] (u16 -> u32) on c's stream; src 16-byte aligned.
+void widen_u16(Ctx& c, const uint16_t* src, uint32_t* dst, uint64_t n);
 // fp64 loss over all local rows; result left in ctx.loss_out[0] (device).
 void loss_launch(Dataset& ds, Model& m, int task);
 // w64 = (double) w32[0..d)

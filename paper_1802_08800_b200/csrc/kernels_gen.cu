@@ -83,6 +83,30 @@ std::vector<double> gen_hidden_model(uint64_t seed, uint64_t d) {
   return w;
 }
 
+// Widen 16-bit CSR column ids (host transfer format when d <= 65536) into the
+// 32-bit ids the kernels read: 8 ids per thread, 16-byte loads.
+__global__ void __launch_bounds__(256) widen_u16_kernel(const uint16_t* __restrict__ src,
+                                                        uint32_t* __restrict__ dst, uint64_t n) {
+  const uint64_t groups = n / 8;
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(src)[g];
+    uint4* o = reinterpret_cast<uint4*>(dst + g * 8);
+    o[0] = make_uint4(v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16);
+    o[1] = make_uint4(v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < n % 8) dst[groups * 8 + threadIdx.x] = src[groups * 8 + threadIdx.x];
+}
+
+void widen_u16(Ctx& c, const uint16_t* src, uint32_t* dst, uint64_t n) {
+  if (n == 0) return;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
+      std::max<uint64_t>(1, (n / 8 + 255) / 256), static_cast<uint64_t>(c.num_sms) * 8));
+  prof_begin(c, "widen_u16_kernel");
+  widen_u16_kernel<<<grid, 256, 0, c.stream>>>(src, dst, n);
+  launched(c, "widen_u16_kernel");
+}
+
 void gen_dense(Dataset& ds, uint64_t seed, double noise) {
   Ctx& c = *ds.ctx;
   const std::vector<double> w = gen_hidden_model(seed, ds.d);

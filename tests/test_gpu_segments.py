@@ -102,3 +102,38 @@ def test_refresh_drops_csc_copy(sgdb, dev):
     S.hogwild_epoch(dds, model, S.Task.LR, 0.1, plan)
     fresh = S.DeviceDataset(dev, ds)
     assert S.sync_epoch(fresh, model, S.Task.LR, 0.1, None, ds.n_examples)
+
+
+@pytest.mark.parametrize("nnz_tail", [0, 3])
+def test_refresh_idx16_matches_idx32(sgdb, dev, nnz_tail):
+    """sgdb_dataset_refresh_idx16 (16-bit ids widened on the device) leaves the
+    dataset identical to a 32-bit refresh: one-worker Hogwild epochs and the
+    mini-batch sync epochs give bit-identical models."""
+    S = sgdb
+    ds = S.fixtures.sparse_classification(997 + nnz_tail, 300, 11.65, 57).rounded_f32()
+    vals = np.ascontiguousarray(ds.values.astype(np.float32)[::-1].copy())
+    idx = np.ascontiguousarray(ds.indices[::-1].astype(np.uint32))
+    idx = np.minimum(idx, ds.n_features - 1).astype(np.uint32)
+    a, b = S.DeviceDataset(dev, ds), S.DeviceDataset(dev, ds)
+    a.refresh_f32(vals, None, idx)
+    b.refresh_f32(vals)
+    b.refresh_idx16(np.ascontiguousarray(idx.astype(np.uint16)))
+    dev.synchronize()
+    plan = S.parse_plan("row-ch:kernel:0")
+    plan.workers = 1
+    ma, mb = S.DeviceModel(dev, ds.n_features), S.DeviceModel(dev, ds.n_features)
+    for _ in range(2):
+        S.hogwild_epoch(a, ma, S.Task.SVM, 0.01, plan)
+        S.hogwild_epoch(b, mb, S.Task.SVM, 0.01, plan)
+    np.testing.assert_array_equal(ma.get(), mb.get())
+    assert S.sync_epoch(a, ma, S.Task.LR, 0.01, None, 64)
+    assert S.sync_epoch(b, mb, S.Task.LR, 0.01, None, 64)
+    np.testing.assert_allclose(ma.get(), mb.get(), rtol=1e-12, atol=1e-14)
+
+
+def test_refresh_idx16_rejects_wide_models(sgdb, dev):
+    S = sgdb
+    ds = S.fixtures.sparse_classification(50, 70000, 5.0, 3).rounded_f32()
+    dds = S.DeviceDataset(dev, ds)
+    with pytest.raises(Exception):
+        dds.refresh_idx16(np.zeros(ds.nnz, np.uint16))
