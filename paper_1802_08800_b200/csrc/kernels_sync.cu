@@ -968,11 +968,73 @@ struct CscWin {
   uint2 r;
 };
 
+// Update applied straight from the column sums when there is a single row
+// block (news20: 19,996 rows): no partials, no apply_partials_kernel.
+struct DirectApply {
+  int on;
+  double alpha;
+  int apply, want_norm;
+  double* w64;
+  float* w32;
+  double* g64;
+  int* finite;
+  double* norm2;
+  // Several row blocks, cooperative launch: after a grid barrier the CTAs
+  // sum the partials and apply (K3f's arithmetic) instead of a second launch.
+  unsigned* gbar;  // non-null: grid-apply mode (on == 0)
+};
+
+// K3f's per-coordinate work, shared by apply_partials_kernel and the
+// grid-apply tail of K3t: g_j = sum_b partials[b][j] in block order.
+template <bool CG>
+__device__ __forceinline__ void apply_partials_range(uint64_t j0, uint64_t stride, uint64_t d,
+                                                     uint32_t nblk, const double* partials,
+                                                     double alpha, int apply, int want_norm,
+                                                     double* w64, float* w32, double* g64,
+                                                     int* finite, double* norm2) {
+  double nrm = 0.0;
+  int bad = 0;
+  for (uint64_t j = j0; j < d; j += stride) {
+    // Sum over blocks in block order; 16 loads in flight per thread (only
+    // ~d threads exist, so memory parallelism has to come from each one).
+    double g = 0.0;
+    uint32_t b = 0;
+    for (; b + 16 <= nblk; b += 16) {
+      double v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const double* q = partials + static_cast<uint64_t>(b + k) * d + j;
+        v[k] = CG ? __ldcg(q) : *q;
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) g += v[k];
+    }
+    for (; b < nblk; ++b) {
+      const double* q = partials + static_cast<uint64_t>(b) * d + j;
+      g += CG ? __ldcg(q) : *q;
+    }
+    if (!isfinite(g)) bad = 1;
+    if (apply) {
+      const double w = w64[j] - alpha * g;
+      w64[j] = w;
+      w32[j] = static_cast<float>(w);
+    } else {
+      g64[j] = g;
+    }
+    nrm += g * g;
+  }
+  if (bad) *finite = 0;
+  if (want_norm) {
+    nrm = warp_sum_d(nrm);
+    if ((threadIdx.x & 31) == 0 && nrm != 0.0) atomicAdd(norm2, nrm);
+  }
+}
+
 template <int G, class ACC>
 __global__ void __launch_bounds__(1024, 1) csc_vec_kernel(
     const float* __restrict__ cval, const uint16_t* __restrict__ crow,
     const uint32_t* __restrict__ colptr, const float* __restrict__ coef, uint64_t n, uint32_t d,
-    uint32_t rb, uint32_t nblk, uint32_t cpb, double* __restrict__ partials) {
+    uint32_t rb, uint32_t nblk, uint32_t cpb, double* __restrict__ partials, DirectApply da) {
   extern __shared__ __align__(16) float cs[];
   __shared__ uint64_t bar;
   const uint32_t b = blockIdx.x / cpb, k = blockIdx.x % cpb;
@@ -1069,20 +1131,14 @@ __global__ void __launch_bounds__(1024, 1) csc_vec_kernel(
     issue(s + 4, s1);
     consume(s + 2, s2);
   }
+  if (da.gbar) {  // grid-apply tail (cooperative launch), as in K3t
+    grid_sync(da.gbar, gridDim.x);
+    apply_partials_range<true>(static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+                               static_cast<uint64_t>(gridDim.x) * blockDim.x, d, nblk, partials,
+                               da.alpha, da.apply, da.want_norm, da.w64, da.w32, da.g64,
+                               da.finite, da.norm2);
+  }
 }
-
-// Update applied straight from the column sums when there is a single row
-// block (news20: 19,996 rows): no partials, no apply_partials_kernel.
-struct DirectApply {
-  int on;
-  double alpha;
-  int apply, want_norm;
-  double* w64;
-  float* w32;
-  double* g64;
-  int* finite;
-  double* norm2;
-};
 
 // K3t: the gradient pass over the blocked CSC as a segmented warp stream:
 // CTA (block b, column range k) stages c[rows of b] in SMEM by bulk copy;
@@ -1170,6 +1226,12 @@ __global__ void __launch_bounds__(NT, 1) csc_seg_kernel(
       nrm = warp_sum_d(nrm);
       if (lane == 0 && nrm != 0.0) atomicAdd(da.norm2, nrm);
     }
+  } else if (da.gbar) {
+    grid_sync(da.gbar, gridDim.x);  // every block's partials are written
+    apply_partials_range<true>(static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+                               static_cast<uint64_t>(gridDim.x) * blockDim.x, d, nblk, partials,
+                               da.alpha, da.apply, da.want_norm, da.w64, da.w32, da.g64,
+                               da.finite, da.norm2);
   }
 }
 
@@ -1178,37 +1240,9 @@ __global__ void __launch_bounds__(NT, 1) csc_seg_kernel(
 __global__ void apply_partials_kernel(uint64_t d, uint32_t nblk, const double* __restrict__ partials,
                                       double alpha, int apply, int want_norm, double* w64,
                                       float* w32, double* g64, int* finite, double* norm2) {
-  double nrm = 0.0;
-  int bad = 0;
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
-       j += (uint64_t)gridDim.x * blockDim.x) {
-    // Sum over blocks in block order; 16 loads in flight per thread (only
-    // ~d threads exist, so memory parallelism has to come from each one).
-    double g = 0.0;
-    uint32_t b = 0;
-    for (; b + 16 <= nblk; b += 16) {
-      double v[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = partials[static_cast<uint64_t>(b + k) * d + j];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) g += v[k];
-    }
-    for (; b < nblk; ++b) g += partials[static_cast<uint64_t>(b) * d + j];
-    if (!isfinite(g)) bad = 1;
-    if (apply) {
-      const double w = w64[j] - alpha * g;
-      w64[j] = w;
-      w32[j] = static_cast<float>(w);
-    } else {
-      g64[j] = g;
-    }
-    nrm += g * g;
-  }
-  if (bad) *finite = 0;
-  if (want_norm) {
-    nrm = warp_sum_d(nrm);
-    if ((threadIdx.x & 31) == 0 && nrm != 0.0) atomicAdd(norm2, nrm);
-  }
+  apply_partials_range<false>((uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                              (uint64_t)gridDim.x * blockDim.x, d, nblk, partials, alpha, apply,
+                              want_norm, w64, w32, g64, finite, norm2);
 }
 
 // ---------------------------------------------------------------------------
@@ -1753,7 +1787,7 @@ void launch_csc_block_G(Dataset& ds, Model& m) {
 }
 
 template <int G>
-void launch_csc_vec_G(Dataset& ds, Model& m) {
+void launch_csc_vec_G(Dataset& ds, Model& m, const DirectApply& da) {
   Ctx& c = *ds.ctx;
   const size_t smem = round_up16(static_cast<uint64_t>(ds.csc_rb) * sizeof(float));
   // fp64 per-(block, column) sums (fp32 sums measured no faster: 85 vs 83 us on rcv1).
@@ -1765,9 +1799,25 @@ void launch_csc_vec_G(Dataset& ds, Model& m) {
   const uint32_t cpb = std::max<uint32_t>(1, slots / ds.csc_nblk);
   m.partials.alloc(static_cast<uint64_t>(ds.csc_nblk) * ds.d);
   prof_begin(c, "csc_grad_kernel");
-  kern<<<cpb * ds.csc_nblk, 1024, smem, c.stream>>>(ds.cval.p, ds.crow.p, ds.colptr.p, ds.coef.p, ds.n,
-                                                    static_cast<uint32_t>(ds.d), ds.csc_rb,
-                                                    ds.csc_nblk, cpb, m.partials.p);
+  if (da.gbar) {
+    check(cudaMemsetAsync(da.gbar, 0, sizeof(unsigned), c.stream), "memset barrier");
+    const float* cval = ds.cval.p;
+    const uint16_t* crow = ds.crow.p;
+    const uint32_t* colptr = ds.colptr.p;
+    const float* coef = ds.coef.p;
+    uint64_t n = ds.n;
+    uint32_t d = static_cast<uint32_t>(ds.d), rb = ds.csc_rb, nblk = ds.csc_nblk, cpb_ = cpb;
+    double* partials = m.partials.p;
+    DirectApply dav = da;
+    void* args[] = {&cval, &crow, &colptr, &coef, &n, &d, &rb, &nblk, &cpb_, &partials, &dav};
+    check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(cpb * ds.csc_nblk),
+                                      dim3(1024), args, smem, c.stream),
+          "cudaLaunchCooperativeKernel(csc_vec)");
+  } else {
+    kern<<<cpb * ds.csc_nblk, 1024, smem, c.stream>>>(ds.cval.p, ds.crow.p, ds.colptr.p, ds.coef.p,
+                                                      ds.n, static_cast<uint32_t>(ds.d), ds.csc_rb,
+                                                      ds.csc_nblk, cpb, m.partials.p, da);
+  }
   launched(c, "csc_grad_kernel");
 }
 
@@ -1839,9 +1889,25 @@ bool launch_csc_seg_N(Dataset& ds, Model& m, const DirectApply& da) {
   const uint32_t cpb = std::max<uint32_t>(1, slots / ds.csc_nblk);
   m.partials.alloc(static_cast<uint64_t>(ds.csc_nblk) * ds.d);
   prof_begin(c, "csc_grad_kernel");
-  kern<<<cpb * ds.csc_nblk, NT, smem, c.stream>>>(ds.cval.p, ds.crow.p, ds.colptr.p, ds.coef.p, ds.n,
-                                                  static_cast<uint32_t>(ds.d), ds.csc_rb,
-                                                  ds.csc_nblk, cpb, m.partials.p, da);
+  if (da.gbar) {  // grid-apply tail: co-residency guaranteed by the cooperative launch
+    check(cudaMemsetAsync(da.gbar, 0, sizeof(unsigned), c.stream), "memset barrier");
+    const float* cval = ds.cval.p;
+    const uint16_t* crow = ds.crow.p;
+    const uint32_t* colptr = ds.colptr.p;
+    const float* coef = ds.coef.p;
+    uint64_t n = ds.n;
+    uint32_t d = static_cast<uint32_t>(ds.d), rb = ds.csc_rb, nblk = ds.csc_nblk, cpb_ = cpb;
+    double* partials = m.partials.p;
+    DirectApply dav = da;
+    void* args[] = {&cval, &crow, &colptr, &coef, &n, &d, &rb, &nblk, &cpb_, &partials, &dav};
+    check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(cpb * ds.csc_nblk),
+                                      dim3(NT), args, smem, c.stream),
+          "cudaLaunchCooperativeKernel(csc_seg)");
+  } else {
+    kern<<<cpb * ds.csc_nblk, NT, smem, c.stream>>>(ds.cval.p, ds.crow.p, ds.colptr.p, ds.coef.p,
+                                                    ds.n, static_cast<uint32_t>(ds.d), ds.csc_rb,
+                                                    ds.csc_nblk, cpb, m.partials.p, da);
+  }
   launched(c, "csc_grad_kernel");
   return true;
 }
@@ -1869,17 +1935,34 @@ void launch_csr_coef_seg(Dataset& ds, Model& m, bool smem_model) {
   if (!go.template operator()<false>()) throw CudaError("csr_coef_seg: no launchable configuration");
 }
 
+// Grid-apply tail (several row blocks): the gradient kernel sums the partials
+// and applies after a grid barrier. SGDB_CSC_GRID_APPLY=0 keeps the separate
+// K3f launch (A/B).
+DirectApply grid_apply_args(Model& m, const StepArgs& a) {
+  static const bool on = [] {
+    const char* e = std::getenv("SGDB_CSC_GRID_APPLY");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (!on) return DirectApply{};
+  m.gbar.alloc(2);
+  return DirectApply{0, a.alpha, a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p,
+                     m.finite.p, m.scal.p, m.gbar.p};
+}
+
 // Returns true when the update was applied in the kernel (one row block).
 bool launch_csc_seg(Dataset& ds, Model& m, const StepArgs& a) {
   const int nt = seg_threads();
   DirectApply da{};
   if (ds.csc_nblk == 1)
     da = DirectApply{1, a.alpha, a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p,
-                     m.finite.p, m.scal.p};
-  if (nt >= 1024 && launch_csc_seg_N<1024>(ds, m, da)) return da.on;
-  if (nt >= 768 && launch_csc_seg_N<768>(ds, m, da)) return da.on;
+                     m.finite.p, m.scal.p, nullptr};
+  else
+    da = grid_apply_args(m, a);
+  const bool applied = da.on || da.gbar;
+  if (nt >= 1024 && launch_csc_seg_N<1024>(ds, m, da)) return applied;
+  if (nt >= 768 && launch_csc_seg_N<768>(ds, m, da)) return applied;
   if (!launch_csc_seg_N<512>(ds, m, da)) throw CudaError("csc_seg: no launchable configuration");
-  return da.on;
+  return applied;
 }
 
 void launch_apply_partials(Dataset& ds, Model& m, const StepArgs& a) {
@@ -2029,7 +2112,9 @@ void csr_full_step(Dataset& ds, Model& m, const StepArgs& a) {
   } else if (mode == 1) {
     // 4-slot windows: one window per lane group covers 4G slots of a column.
     const int gv = per_col <= 24.0 ? 4 : 8;
-    dispatch_G(env_lanes("SGDB_COL_LANES", gv), [&]<int G>() { launch_csc_vec_G<G>(ds, m); });
+    const DirectApply da = grid_apply_args(m, a);
+    dispatch_G(env_lanes("SGDB_COL_LANES", gv), [&]<int G>() { launch_csc_vec_G<G>(ds, m, da); });
+    applied = da.gbar != nullptr;
   } else {
     dispatch_G(env_lanes("SGDB_COL_LANES", gc), [&]<int G>() { launch_csc_block_G<G>(ds, m); });
   }
