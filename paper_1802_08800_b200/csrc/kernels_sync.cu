@@ -1434,12 +1434,14 @@ __global__ void __launch_bounds__(256) mb_scatter_kernel(
     const uint32_t* __restrict__ rowptr, const float* __restrict__ y,
     const uint32_t* __restrict__ ids, const uint32_t* __restrict__ off,
     const uint4* __restrict__ meta, uint64_t cap, uint64_t lo, uint64_t hi, uint64_t row_base,
-    const float* __restrict__ zpart, double* g64, const int* finite, int check_finite) {
+    const float* __restrict__ zpart, double* g64, const int* finite, int check_finite,
+    int prefetch_next, uint64_t count) {
   if (check_finite && *finite == 0) return;
   constexpr int RW = 32 / G;
   const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
   const uint32_t c0 = __ldg(off + lo), c1 = __ldg(off + hi);
   const bool direct = c1 <= cap;
+  const uint64_t total = prefetch_next ? __ldg(off + count) : 0;  // chunks of the whole plan
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t q = c0 + gw * RW + grp; q < c1; q += tw * RW) {  // no shuffles: per group
@@ -1457,10 +1459,24 @@ __global__ void __launch_bounds__(256) mb_scatter_kernel(
     float z = 0.f;
     for (uint32_t k = z0; k < z1; ++k) z += __ldg(zpart + k);  // chunk order
     const float c = coef_f<TASK>(z, __ldg(y + r.row));
-    if (c == 0.f) continue;
+    if (c != 0.f) {
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (r.b + lg + u * G < r.e) atomicAdd(&g64[jv[u]], static_cast<double>(c * xv[u]));
+      for (int u = 0; u < U; ++u)
+        if (r.b + lg + u * G < r.e) atomicAdd(&g64[jv[u]], static_cast<double>(c * xv[u]));
+    }
+    if (prefetch_next && total <= cap) {
+      // Pull the slots of the chunk at the same position of the next step
+      // into L2, so that step's margin pass reads them from L2, not HBM.
+      const uint64_t qn = q + (c1 - c0);
+      if (qn < total && lg < 16) {  // total <= cap: table entries below it are written
+        const uint4 mn = __ldg(meta + qn);
+        const uint32_t lines = min((mn.y - mn.x + 31) / 32, U * G / 32u);  // 128-byte lines
+        const char* base = lg < 8 ? reinterpret_cast<const char*>(idx + mn.x)
+                                  : reinterpret_cast<const char*>(val + mn.x);
+        for (uint32_t l = lg & 7; l < lines; l += 8)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128ull * l));
+      }
+    }
   }
 }
 
@@ -2137,6 +2153,14 @@ bool chunked_batches() {
   return on;
 }
 
+bool mb_prefetch() {
+  static const bool on = [] {  // SGDB_BATCH_PREFETCH=0: no L2 prefetch of the next step
+    const char* e = std::getenv("SGDB_BATCH_PREFETCH");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 template <int G, int TASK>
 void launch_mb_chunks(Dataset& ds, Model& m, uint64_t lo, uint64_t nb, bool check) {
   Ctx& c = *ds.ctx;
@@ -2154,7 +2178,8 @@ void launch_mb_chunks(Dataset& ds, Model& m, uint64_t lo, uint64_t nb, bool chec
   prof_begin(c, "mb_scatter_kernel");
   mb_scatter_kernel<G, kChunkU, TASK><<<grid, 256, 0, c.stream>>>(
       ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p, ds.mb_ids, ds.mb_off.p, ds.mb_meta.p,
-      ds.mb_cap, lo, hi, ds.row_base, ds.mb_z.p, m.g64.p, m.finite.p, check ? 1 : 0);
+      ds.mb_cap, lo, hi, ds.row_base, ds.mb_z.p, m.g64.p, m.finite.p, check ? 1 : 0,
+      mb_prefetch() && hi < ds.mb_count ? 1 : 0, ds.mb_count);
   launched(c, "mb_scatter_kernel");
 }
 }  // namespace
