@@ -283,23 +283,34 @@ def run_ours(args):
     # Double-buffered: step k+1's inputs are copied into the other device buffer
     # on a copy stream while step k's epoch runs; every step still copies its
     # whole input from pinned host memory and reads its result back.
-    copy_stream = torch.cuda.Stream()
-    copy_dev = S.Device(local, stream=copy_stream.cuda_stream)
+    # Two copy streams: the values on one, ids / labels / offsets on the other
+    # (B200 has several copy engines; SGDB_E2E_STREAMS=1 uses one).
+    n_copy = 1 if os.environ.get("SGDB_E2E_STREAMS") == "1" else 2
+    copy_streams = [torch.cuda.Stream() for _ in range(n_copy)]
+    copy_devs = [S.Device(local, stream=cs.cuda_stream) for cs in copy_streams]
+    cA, cB = copy_devs[0], copy_devs[-1]
     bufs = [S.DeviceDataset(dev, host), S.DeviceDataset(dev, host)]  # dds keeps its CSC copy
-    ready = [torch.cuda.Event(), torch.cuda.Event()]
+    ready = [[torch.cuda.Event() for _ in range(n_copy)] for _ in range(2)]
     free = [torch.cuda.Event(), torch.cuda.Event()]
     used = [False, False]
+
+    def refresh(b):
+        bufs[b].refresh_f32(vals, None, None, None, device=cA)
+        bufs[b].refresh_f32(None, labs, None, rp, device=cB)
+        bufs[b].refresh_idx16(idx, device=cB)
+        for ev, cs in zip(ready[b], copy_streams):
+            ev.record(cs)
 
     def e2e_step(k):
         b = k % 2
         if k + 1 < e2e_steps:
             nb = 1 - b
             if used[nb]:
-                copy_stream.wait_event(free[nb])
-            bufs[nb].refresh_f32(vals, labs, None, rp, device=copy_dev)
-            bufs[nb].refresh_idx16(idx, device=copy_dev)
-            ready[nb].record(copy_stream)
-        stream.wait_event(ready[b])
+                for cs in copy_streams:
+                    cs.wait_event(free[nb])
+            refresh(nb)
+        for ev in ready[b]:
+            stream.wait_event(ev)
         SD.hogwild_epoch_ranks(dev, bufs[b], model, task, alpha, plan, world, args.segments)
         free[b].record(stream)
         used[b] = True
@@ -307,9 +318,7 @@ def run_ours(args):
 
     def e2e_run():
         used[0] = used[1] = False
-        bufs[0].refresh_f32(vals, labs, None, rp, device=copy_dev)  # step 0's inputs
-        bufs[0].refresh_idx16(idx, device=copy_dev)
-        ready[0].record(copy_stream)
+        refresh(0)  # step 0's inputs
         for k in range(e2e_steps):
             e2e_step(k)
 
@@ -344,7 +353,8 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": sweep, "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-                "pipeline": "double-buffered: step k+1's H2D (copy stream) overlaps step k's "
+                "copy_streams": n_copy,
+                "pipeline": "double-buffered: step k+1's H2D (copy streams) overlaps step k's "
                             "epoch; every step copies its inputs (column ids as 16 bits, widened "
                             "on the device) and reads the model back"},
         "gpu_launches": launches,
