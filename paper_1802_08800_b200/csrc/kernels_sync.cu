@@ -1470,7 +1470,7 @@ __global__ void __launch_bounds__(256) mb_scatter_kernel(
       const uint64_t qn = q + (c1 - c0);
       if (qn < total && lg < 16) {  // total <= cap: table entries below it are written
         const uint4 mn = __ldg(meta + qn);
-        const uint32_t lines = min((mn.y - mn.x + 31) / 32, U * G / 32u);  // 128-byte lines
+        const uint32_t lines = min((mn.y - mn.x + 31) / 32, (U * G + 31) / 32u);  // 128-byte lines
         const char* base = lg < 8 ? reinterpret_cast<const char*>(idx + mn.x)
                                   : reinterpret_cast<const char*>(val + mn.x);
         for (uint32_t l = lg & 7; l < lines; l += 8)
@@ -2138,7 +2138,16 @@ void csr_full_step(Dataset& ds, Model& m, const StepArgs& a) {
 }
 
 namespace {
-constexpr int kChunkU = 8;  // slots per lane per chunk (CH = G * kChunkU)
+// Slots per lane per chunk (CH = G * U): 4 by default (measured against 2 / 8
+// / 16, profiles/round1_minibatch_chunk_u_ab.jsonl); SGDB_BATCH_CHUNK_U selects.
+int chunk_u() {
+  static const int u = [] {
+    const char* e = std::getenv("SGDB_BATCH_CHUNK_U");
+    const int v = e ? std::atoi(e) : 4;
+    return v == 2 || v == 8 || v == 16 ? v : 4;
+  }();
+  return u;
+}
 
 int batch_lanes(const Dataset& ds) {
   return env_lanes("SGDB_BATCH_LANES",
@@ -2161,33 +2170,43 @@ bool mb_prefetch() {
   return on;
 }
 
-template <int G, int TASK>
-void launch_mb_chunks(Dataset& ds, Model& m, uint64_t lo, uint64_t nb, bool check) {
+template <int G, int TASK, int U>
+void launch_mb_chunks_U(Dataset& ds, Model& m, uint64_t lo, uint64_t nb, bool check) {
   Ctx& c = *ds.ctx;
   constexpr int RW = 32 / G;
   // Chunks of one step: the rows plus one per CH slots of their mean length.
   const double avg = ds.n ? static_cast<double>(ds.nnz) / static_cast<double>(ds.n) : 1.0;
-  const uint64_t est = nb + static_cast<uint64_t>(nb * avg / (G * kChunkU));
+  const uint64_t est = nb + static_cast<uint64_t>(nb * avg / (G * U));
   const unsigned grid = grid_for(c, 8ull * RW, est, 16);
   const uint64_t hi = lo + nb;
   prof_begin(c, "mb_margin_kernel");
-  mb_margin_kernel<G, kChunkU><<<grid, 256, 0, c.stream>>>(
+  mb_margin_kernel<G, U><<<grid, 256, 0, c.stream>>>(
       ds.val.p, ds.idx.p, ds.rowptr.p, ds.mb_ids, ds.mb_off.p, ds.mb_meta.p, ds.mb_cap, lo, hi,
       ds.row_base, m.w32.p, ds.mb_z.p, m.finite.p, check ? 1 : 0);
   launched(c, "mb_margin_kernel");
   prof_begin(c, "mb_scatter_kernel");
-  mb_scatter_kernel<G, kChunkU, TASK><<<grid, 256, 0, c.stream>>>(
+  mb_scatter_kernel<G, U, TASK><<<grid, 256, 0, c.stream>>>(
       ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p, ds.mb_ids, ds.mb_off.p, ds.mb_meta.p,
       ds.mb_cap, lo, hi, ds.row_base, ds.mb_z.p, m.g64.p, m.finite.p, check ? 1 : 0,
       mb_prefetch() && hi < ds.mb_count ? 1 : 0, ds.mb_count);
   launched(c, "mb_scatter_kernel");
+}
+
+template <int G, int TASK>
+void launch_mb_chunks(Dataset& ds, Model& m, uint64_t lo, uint64_t nb, bool check) {
+  switch (chunk_u()) {
+    case 2: launch_mb_chunks_U<G, TASK, 2>(ds, m, lo, nb, check); break;
+    case 8: launch_mb_chunks_U<G, TASK, 8>(ds, m, lo, nb, check); break;
+    case 16: launch_mb_chunks_U<G, TASK, 16>(ds, m, lo, nb, check); break;
+    default: launch_mb_chunks_U<G, TASK, 4>(ds, m, lo, nb, check); break;
+  }
 }
 }  // namespace
 
 void csr_batch_plan(Dataset& ds, const uint32_t* ids, uint64_t count, uint64_t max_step) {
   if (!chunked_batches() || count == 0) return;
   Ctx& c = *ds.ctx;
-  const uint32_t ch = static_cast<uint32_t>(batch_lanes(ds) * kChunkU);
+  const uint32_t ch = static_cast<uint32_t>(batch_lanes(ds) * chunk_u());
   const uint64_t per_row = ds.max_row ? (ds.max_row + ch - 1) / ch : 1;
   const uint64_t zcap = std::min(max_step, count) * per_row;
   // Chunk table: every chunk of a permutation order (sum over the local rows
@@ -2229,7 +2248,7 @@ void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, con
   const int g = batch_lanes(ds);
   if (chunked_batches()) {
     if (!(ds.mb_ids && ids >= ds.mb_ids && ids + nb <= ds.mb_ids + ds.mb_count &&
-          ds.mb_ch == static_cast<uint32_t>(g * kChunkU)))
+          ds.mb_ch == static_cast<uint32_t>(g * chunk_u())))
       csr_batch_plan(ds, ids, nb, nb);
     const uint64_t lo = static_cast<uint64_t>(ids - ds.mb_ids);
     dispatch_G(g, [&]<int G>() {
