@@ -256,7 +256,7 @@ def test_padded_and_colmajor_inputs(sgdb, dev, orc):
 
 def _heavy_tailed(S, n, d, seed):
     """CSR rows with a heavy tail (a few rows many chunks long) and empty rows:
-    the chunked mini-batch kernels (K3c) cut rows into chunks of G*8 slots."""
+    the chunked mini-batch kernels (K3c) cut rows into chunks of G*4 slots."""
     rng = np.random.default_rng(seed)
     lens = rng.integers(0, 40, n)
     lens[rng.choice(n, 6, replace=False)] = rng.integers(600, 3000, 6)
