@@ -176,6 +176,8 @@ class Oracle(_Lib):
         L.orc_merge_models.argtypes = [_P(_dbl), _u64, _u64, _P(_dbl), _P(_dbl)]
         L.orc_philox_hidden_model.argtypes = [_u64, _u64, _P(_dbl)]
         L.orc_philox_dense.argtypes = [_u64, _u64, _u64, _u64, _dbl, _P(_dbl), _P(_dbl)]
+        L.orc_philox_dense_gradient.argtypes = [_u64, _u64, _u64, _u64, _dbl, _int, _P(_dbl),
+                                                C.c_uint32, _P(_dbl), _P(_dbl)]
 
     def round_f32(self, ds: HostData) -> HostData:
         out = HostData(**ds.__dict__)
@@ -252,6 +254,17 @@ class Oracle(_Lib):
         labels = np.zeros(n, np.float64)
         self.lib.orc_philox_dense(n, d, row_base, seed, noise, _ptr(values, _dbl), _ptr(labels, _dbl))
         return HostData(n, d, DENSE_ROW, labels, values)
+
+    def philox_dense_gradient(self, n, d, seed, task, w, row_base=0, noise=0.1, threads=None):
+        """Full-batch gradient and loss at w over rows [row_base, row_base+n) of the
+        device generator's dataset, streamed (rows regenerated, never stored)."""
+        threads = threads or max(1, os.cpu_count() or 1)
+        w = np.ascontiguousarray(w, np.float64)
+        g = np.zeros(d, np.float64)
+        loss = _dbl(0.0)
+        self.lib.orc_philox_dense_gradient(n, d, row_base, seed, noise, task, _ptr(w, _dbl),
+                                           threads, _ptr(g, _dbl), C.byref(loss))
+        return g, float(loss.value)
 
     def merge_models(self, replicas: np.ndarray, weights=None) -> np.ndarray:
         reps = np.ascontiguousarray(replicas, np.float64)

@@ -21,6 +21,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
@@ -705,4 +706,76 @@ void orc_philox_dense(uint64_t n, uint64_t d, uint64_t row_base, uint64_t seed, 
   }
 }
 
+// Streaming full-batch gradient over rows [row_base, row_base + n) of the
+// generated dataset at model w, without materialising it (the 25M x 1000
+// shard of C5 is 100 GB in fp32): every row is regenerated from its Philox
+// counters (exactly the values orc_philox_dense produces), its margin is the
+// fp64 dot in ascending feature order (src/linalg.cpp:30-44), the coefficient
+// is src/glm.cpp:30-34, and g = sum_e c_e x_e (src/linalg.cpp:58-76) is
+// accumulated in fp64. Rows are split into `threads` contiguous ranges, each
+// accumulated in row order, and the per-thread partials added in thread order
+// (deterministic for a fixed thread count). loss_out (may be NULL) receives
+// dataset_loss at w (src/glm.cpp:85-94).
+void orc_philox_dense_gradient(uint64_t n, uint64_t d, uint64_t row_base, uint64_t seed,
+                               double noise, int task, const double* w, uint32_t threads,
+                               double* g_out, double* loss_out) {
+  if (threads == 0) threads = 1;
+  std::vector<double> wt(d);
+  orc_philox_hidden_model(seed, d, wt.data());
+  std::vector<std::vector<double>> part(threads, std::vector<double>(d, 0.0));
+  std::vector<double> lpart(threads, 0.0);
+  auto work = [&](uint32_t t) {
+    const uint64_t r0 = n * t / threads, r1 = n * (t + 1) / threads;
+    std::vector<double> x(d);
+    std::vector<double>& g = part[t];
+    double lsum = 0.0;
+    const uint64_t nq = (d + 3) / 4;
+    for (uint64_t r = r0; r < r1; ++r) {
+      const uint64_t e = row_base + r;
+      double lane[32] = {0.0};
+      for (uint64_t q = 0; q < nq; ++q) {
+        P4 u = philox10(P4{{static_cast<uint32_t>(e), static_cast<uint32_t>(e >> 32),
+                            static_cast<uint32_t>(q), 0x5EED0001u}},
+                        static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t j = 4 * q + k;
+          if (j >= d) continue;
+          x[j] = static_cast<double>(unit_val(u.v[k]));
+          lane[q % 32] = lane[q % 32] + x[j] * wt[j];
+        }
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        double nx[32];
+        for (int l = 0; l < 32; ++l) nx[l] = lane[l] + lane[l ^ off];
+        for (int l = 0; l < 32; ++l) lane[l] = nx[l];
+      }
+      double y = lane[0] >= 0.0 ? 1.0 : -1.0;
+      if (noise > 0.0) {
+        P4 f = philox10(P4{{static_cast<uint32_t>(e), static_cast<uint32_t>(e >> 32), 0u, 0x5EED0002u}},
+                        static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+        const float uf = static_cast<float>(f.v[0] >> 8) * (1.0f / 16777216.0f);
+        if (static_cast<double>(uf) < noise) y = -y;
+      }
+      double z = 0.0;
+      for (uint64_t j = 0; j < d; ++j) z = z + x[j] * w[j];
+      lsum = lsum + loss_from_margin(task, z, y);
+      const double c = coefficient(task, z, y);
+      if (c != 0.0)
+        for (uint64_t j = 0; j < d; ++j) g[j] = g[j] + c * x[j];
+    }
+    lpart[t] = lsum;
+  };
+  std::vector<std::thread> pool;
+  for (uint32_t t = 0; t < threads; ++t) pool.emplace_back(work, t);
+  for (auto& th : pool) th.join();
+  double l = 0.0;
+  for (uint64_t j = 0; j < d; ++j) g_out[j] = 0.0;
+  for (uint32_t t = 0; t < threads; ++t) {
+    for (uint64_t j = 0; j < d; ++j) g_out[j] = g_out[j] + part[t][j];
+    l = l + lpart[t];
+  }
+  if (loss_out) *loss_out = l;
+}
+
 }  // extern "C"
+
