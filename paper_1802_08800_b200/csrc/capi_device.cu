@@ -46,48 +46,6 @@ void h2d(T* dst, const T* src, uint64_t count, cudaStream_t s) {
   if (count) check(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
 }
 
-// Row-blocked CSC of a CSR matrix (counting sort per row block; rows stay
-// ascending inside a column). Block count: enough blocks to feed every SM,
-// few enough that the per-block column pointers stay small next to the data.
-void csc_blocked_from_csr(uint64_t n, uint64_t d, const std::vector<uint32_t>& rowptr,
-                          const std::vector<uint32_t>& idx, const std::vector<float>& val,
-                          uint32_t& rb, uint32_t& nblk, std::vector<uint32_t>& colptr,
-                          std::vector<uint16_t>& crow, std::vector<float>& cval) {
-  const uint64_t nnz = idx.size();
-  uint64_t want = std::clamp<uint64_t>((nnz * 2) / ((d + 1) * 4), 1, 16);
-  // A single block whenever its coefficient slice fits SMEM: the gradient
-  // kernels then apply the update straight from the column sums (no
-  // partials pass; news20: 19,996 rows).
-  if (n <= 49152) want = 1;
-  want = std::max<uint64_t>(want, (n + 49151) / 49152);  // slice <= 192 KB of SMEM
-  // rb % 4 == 0 keeps every block's coefficient slice 16-byte aligned (bulk copies).
-  rb = static_cast<uint32_t>(std::max<uint64_t>(4, ((n + want - 1) / want + 3) & ~uint64_t(3)));
-  nblk = static_cast<uint32_t>(std::max<uint64_t>(1, (n + rb - 1) / rb));
-  colptr.assign(static_cast<uint64_t>(nblk) * (d + 1), 0);
-  crow.resize(nnz);
-  cval.resize(nnz);
-  std::vector<uint32_t> next(d);
-  uint32_t pos = 0;
-  for (uint32_t bk = 0; bk < nblk; ++bk) {
-    const uint64_t r0 = static_cast<uint64_t>(bk) * rb, r1 = std::min<uint64_t>(n, r0 + rb);
-    uint32_t* cp = colptr.data() + static_cast<uint64_t>(bk) * (d + 1);
-    std::fill(next.begin(), next.end(), 0u);
-    for (uint32_t s = rowptr[r0]; s < rowptr[r1]; ++s) ++next[idx[s]];
-    cp[0] = pos;
-    for (uint64_t j = 0; j < d; ++j) {
-      cp[j + 1] = cp[j] + next[j];
-      next[j] = cp[j];
-    }
-    for (uint64_t r = r0; r < r1; ++r)
-      for (uint32_t s = rowptr[r]; s < rowptr[r + 1]; ++s) {
-        const uint32_t q = next[idx[s]]++;
-        crow[q] = static_cast<uint16_t>(r - r0);
-        cval[q] = val[s];
-      }
-    pos = cp[d];
-  }
-}
-
 void upload_csr(sgdb_dataset* ds, std::vector<uint32_t>& rowptr, std::vector<uint32_t>& idx,
                 std::vector<float>& val) {
   cudaStream_t s = ds->ctx->stream;
@@ -105,22 +63,9 @@ void upload_csr(sgdb_dataset* ds, std::vector<uint32_t>& rowptr, std::vector<uin
   h2d(ds->val.p, val.data(), ds->nnz, s);
   h2d(ds->idx.p, idx.data(), ds->nnz, s);
   h2d(ds->rowptr.p, rowptr.data(), ds->n + 1, s);
-  std::vector<uint32_t> colptr;
-  std::vector<uint16_t> crow;
-  std::vector<float> cval;
-  csc_blocked_from_csr(ds->n, ds->d, rowptr, idx, val, ds->csc_rb, ds->csc_nblk, colptr, crow, cval);
-  // +8 zeroed slack: K3v reads whole aligned 4-slot windows around a column.
-  ds->cval.alloc(ds->nnz + 8);
-  ds->crow.alloc(ds->nnz + 8);
-  ds->cval.zero(s);
-  ds->crow.zero(s);
-  ds->colptr.alloc(colptr.size());
-  h2d(ds->cval.p, cval.data(), ds->nnz, s);
-  h2d(ds->crow.p, crow.data(), ds->nnz, s);
-  h2d(ds->colptr.p, colptr.data(), colptr.size(), s);
-  ds->csc_built = true;
-  ds->coef.alloc(ds->n + 8);  // 16-byte slack: K3v bulk-copies whole slices
-  ds->coef.zero(s);
+  // The full-batch structures (head bitmaps, blocked CSC) are built on the
+  // device on first use (sparse_prep).
+  ds->sparse_ready = false;
   check(cudaStreamSynchronize(s), "upload sync");  // host vectors die with the caller
 }
 
@@ -211,7 +156,7 @@ void model_set(sgdb_model* m, const double* w) {
 
 void full_step(sgdb_dataset* ds, sgdb_model* m, const StepArgs& a) {
   if (ds->kind == Kind::Dense) dense_full_step(*ds, *m, a);
-  else csr_full_step(*ds, *m, a);
+  else sparse_full_step(*ds, *m, a);
 }
 
 }  // namespace
@@ -486,23 +431,37 @@ sgdb_status sgdb_dataset_refresh_f32(sgdb_ctx* ctx, sgdb_dataset* ds, const floa
                                      const float* labels, const uint32_t* indices,
                                      const uint32_t* row_offsets32) {
   return sgdb_guard([&] {
+    require(ctx && ds, "null argument");
+    if (ds->exact || ds->layout_in == SGDB_LAYOUT_PADDED)
+      throw Unsupported("refresh: exact-fp64 and padded-layout datasets keep derived copies; upload again");
     cudaStream_t s = ctx->stream;
     if (labels) h2d(ds->labels.p, labels, ds->n, s);
     if (ds->kind == Kind::Dense) {
-      if (values) h2d(ds->x.p, values, ds->n * ds->d, s);
-    } else {
-      if (values) h2d(ds->val.p, values, ds->nnz, s);
-      if (indices) h2d(ds->idx.p, indices, ds->nnz, s);
-      if (row_offsets32) h2d(ds->rowptr.p, row_offsets32, ds->n + 1, s);
-      if (values || indices || row_offsets32) {
-        // The row-blocked CSC copy (full-batch gradient pass) is built from
-        // the host arrays at upload and is not refreshed here: full-batch
-        // sparse sync on this dataset now fails loudly instead of reading
-        // stale values. The margin pass's warp partition is recomputed.
-        ds->csc_built = false;
-        ds->seg_nw = 0;
+      if (values) {
+        h2d(ds->x.p, values, ds->n * ds->d, s);
+        ds->col_built = false;  // the column-major copy is rebuilt on next use
       }
+      return;
     }
+    if (row_offsets32) {
+      // Row offsets size the mini-batch chunk plans (max_row): validate and
+      // recompute from the host array before it is copied.
+      require(row_offsets32[0] == 0 && row_offsets32[ds->n] == ds->nnz,
+              "refresh: row offsets must start at 0 and end at nnz");
+      uint64_t mr = 0;
+      for (uint64_t r = 0; r < ds->n; ++r) {
+        require(row_offsets32[r + 1] >= row_offsets32[r], "refresh: row offsets must be non-decreasing");
+        mr = std::max<uint64_t>(mr, row_offsets32[r + 1] - row_offsets32[r]);
+      }
+      ds->max_row = mr;
+      ds->mb_ids = nullptr;  // chunk plans refer to the old row extents
+      h2d(ds->rowptr.p, row_offsets32, ds->n + 1, s);
+    }
+    if (values) h2d(ds->val.p, values, ds->nnz, s);
+    if (indices) h2d(ds->idx.p, indices, ds->nnz, s);
+    // The full-batch structures (bitmaps, 16-bit ids, blocked CSC) are
+    // rebuilt on the device at the next full-batch step.
+    if (values || indices || row_offsets32) ds->sparse_ready = false;
   });
 }
 
@@ -511,12 +470,13 @@ sgdb_status sgdb_dataset_refresh_idx16(sgdb_ctx* ctx, sgdb_dataset* ds, const ui
     require(ctx && ds && indices16, "null argument");
     require(ds->kind == Kind::Csr, "refresh_idx16: the dataset is not stored as CSR");
     require(ds->d <= 65536, "refresh_idx16: column ids need d <= 65536");
+    if (ds->exact || ds->layout_in == SGDB_LAYOUT_PADDED)
+      throw Unsupported("refresh: exact-fp64 and padded-layout datasets keep derived copies; upload again");
     cudaStream_t s = ctx->stream;
     ds->idx16.alloc(ds->nnz + 8);
     h2d(ds->idx16.p, indices16, ds->nnz, s);
     widen_u16(*ctx, ds->idx16.p, ds->idx.p, ds->nnz);
-    ds->csc_built = false;  // as sgdb_dataset_refresh_f32
-    ds->seg_nw = 0;
+    ds->sparse_ready = false;  // as sgdb_dataset_refresh_f32
   });
 }
 
@@ -645,10 +605,9 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
         }
       };
       if (!hook && ds->kind == Kind::Dense && ng > batch_b &&
-          !std::getenv("SGDB_NO_PERSISTENT_EPOCH") &&
           dense_epoch(*ds, *m, task, alpha, batch_b)) {
         // K1c: the whole epoch in one persistent launch
-      } else if (hook || ng / batch_b < 4 || std::getenv("SGDB_NO_EPOCH_GRAPH")) {
+      } else if (hook || ng / batch_b < 4) {
         run_steps(a);
       } else {
         // Launch-bound many-step epoch: replay a captured CUDA graph of the
@@ -909,7 +868,4 @@ uint64_t next_dataset_uid() {
   return counter.fetch_add(1);
 }
 
-void build_csc(Dataset& ds) {
-  if (!ds.csc_built) throw Unsupported("CSC copy missing (dataset was not uploaded as CSR)");
-}
 }  // namespace sgdb::dev

@@ -115,15 +115,31 @@ struct Dataset {
   DBuf<uint32_t> idx;
   DBuf<uint32_t> rowptr;
   DBuf<uint16_t> idx16;  // staging for sgdb_dataset_refresh_idx16
-  // Row-blocked CSC of the local rows (full-batch sparse gradients): rows are
-  // split into csc_nblk blocks of csc_rb (< 2^16) rows; block b holds its
-  // columns back to back, colptr[b*(d+1) + j] are global offsets, row ids
-  // are 16-bit block-local.
-  bool csc_built = false;
-  uint32_t csc_rb = 0, csc_nblk = 0;
+  // Full-batch sparse step (kernels_sparse.cu), built on the device by
+  // sparse_prep at upload and again after a refresh (sparse_ready = false):
+  //  * row-head bitmap rbm (bit s = slot s starts a non-empty row) and the
+  //    exclusive popcount prefix of its words (rbm_pre); row_of_ord maps a
+  //    non-empty row's ordinal to its row id when some rows are empty;
+  //  * 16-bit column ids (d <= 65536) for the margin pass;
+  //  * margin-pass CTA ranges (cta_n CTAs, each starting at a row start);
+  //  * the row-blocked CSC: rows split into csc_nblk blocks of csc_rb
+  //    (< 2^16, % 4 == 0) rows, segment (b, j) = block b's entries of column
+  //    j at segptr[b*d + j] .. segptr[b*d + j + 1], 16-bit block-local rows;
+  //    its head bitmap / prefix (cbm, cbm_pre), seg_of_ord when some segments
+  //    are empty, csc_cpb nnz-balanced column ranges (cta_col) shared by all
+  //    blocks, and their arrival tickets.
+  bool sparse_ready = false;
+  DBuf<uint32_t> rbm, rbm_pre, row_of_ord;
+  bool rows_empty = false;
+  DBuf<uint16_t> cidx16;
+  uint32_t cta_n = 0;
+  DBuf<uint32_t> cta_slot;
+  uint32_t csc_rb = 0, csc_nblk = 0, csc_cpb = 0;
   DBuf<float> cval;
   DBuf<uint16_t> crow;
-  DBuf<uint32_t> colptr;
+  DBuf<uint32_t> segptr, cbm, cbm_pre, seg_of_ord, cta_col;
+  bool segs_empty = false;
+  DBuf<unsigned> sparse_tickets;
   // Column-major copies for the col-* access paths (built lazily).
   bool col_built = false;
   DBuf<float> xcol;    // dense: d*n
@@ -142,11 +158,6 @@ struct Dataset {
   DBuf<double> ex_rep64;  // exact-fp64 mode
   DBuf<unsigned> ex_claim, ex_ready;
   unsigned ex_epoch = 0;
-  // Warp partition of the nonzeros for the segmented margin pass (K2t):
-  // first owned row per warp, and the partial sums of rows cut by warps.
-  DBuf<uint32_t> seg_orow;
-  DBuf<float> seg_pf, seg_pl;
-  uint32_t seg_nw = 0;
   // Scratch.
   DBuf<float> coef;        // per local row coefficient (sparse full batch)
   DBuf<uint32_t> order;    // n_global ids of the current epoch
@@ -179,6 +190,7 @@ struct Model {
   DBuf<double> w64;      // d, master
   DBuf<double> g64;      // d, gradient accumulator (kept zeroed between steps)
   DBuf<double> partials; // per-block gradient partials, deterministic full batch
+  DBuf<float> part32;    // per-(row block, column) sums of the full-batch sparse step
   DBuf<unsigned> ticket; // [0] grad ticket
   DBuf<double> g3;       // 3*d rotating gradient buffers of the persistent epoch (K1c)
   DBuf<unsigned> gbar;   // grid barrier words (K1c), zero between uses
@@ -225,8 +237,10 @@ void dense_full_step(Dataset& ds, Model& m, const StepArgs& a);
 bool dense_epoch(Dataset& ds, Model& m, int task, double alpha, uint64_t B);
 void dense_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb,
                       const StepArgs& a);
-// Sparse, all local rows: margin/coef pass + CSC gradient pass.
-void csr_full_step(Dataset& ds, Model& m, const StepArgs& a);
+// Sparse, all local rows: margin/coef pass + CSC gradient pass
+// (kernels_sparse.cu); sparse_prep builds the device structures it reads.
+void sparse_prep(Dataset& ds);
+void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a);
 // Sparse mini-batch: chunk plan of the ids a sequence of steps walks (device
 // ids[0..count), steps of at most max_step positions); steps whose ids lie
 // outside the current plan build their own.
@@ -290,7 +304,6 @@ void exact_sync_epoch(Dataset& ds, Model& m, int task, double alpha, const uint3
 void exact_epoch_batch(Dataset& ds, Model& m, int task, double alpha);
 void exact_loss(Dataset& ds, Model& m, int task);
 void exact_hogwild(Dataset& ds, Model& m, const HogwildArgs& a);
-void build_csc(Dataset& ds);
 void build_col(Dataset& ds);
 
 }  // namespace sgdb::dev

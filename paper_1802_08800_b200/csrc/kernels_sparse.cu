@@ -1,0 +1,818 @@
+// Full-batch sparse step (B = N) over CSR data — the hot path of sync::train
+// at B = N on rcv1 / real-sim / news20 / w8a-shaped inputs
+// (proj/src/sync_engine.cpp:22-42 -> linalg::matvec, the LR/SVM coefficient,
+// linalg::matvec_transposed; proj/src/linalg.cpp:30-109, glm.cpp:30-34).
+//
+//   K2s  margin pass   z = X w                                (CSR stream)
+//   K3s  gradient pass c = coef(z, y), g = X^T c, w -= alpha g (row-blocked CSC stream)
+//
+// Both passes are one segmented stream over a CTA's contiguous range of
+// nonzeros: each warp walks its share in 128-slot tiles (lane l holds slots
+// 4l..4l+3 of a tile: one float4 of values + 4 ids), multiplies with the
+// staged operand (the model, or the row block's coefficient slice, in SMEM),
+// and recovers the per-segment sums (rows, or (block, column) segments) with
+// a segmented warp scan. Segment boundaries come from a HEAD BITMAP (bit s =
+// slot s starts a non-empty segment) built once per upload, so a lane finds
+// its boundaries with one 32-bit load and a shift — no row-pointer walking,
+// no per-slot masks on full tiles. A segment's identity is its ordinal among
+// the heads (the prefix popcount of the bitmap words, also built once); the
+// ordinal maps to a row / (block, column) directly unless the data has empty
+// segments, in which case a compaction map translates it.
+//
+// CTA ranges start at segment starts, so a segment is only ever cut between
+// warps of the same CTA; those pieces are combined in SMEM after the stream,
+// in slot order. The gradient pass writes fp32 per-(block, column) sums; the
+// last CTA of each column range (arrival ticket) sums them over the row
+// blocks in block order and applies the update: deterministic, no atomics on
+// data, no grid barrier, any grid size.
+//
+// The row-blocked CSC (16-bit block-local row ids) is built on the device by a
+// stable radix sort of (block, column) keys, at upload and after a refresh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "device.hpp"
+
+namespace sgdb::dev {
+namespace {
+
+constexpr int kNT = 1024;  // threads per CTA of both passes
+constexpr int kNW = kNT / 32;
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr uint32_t kMaxRowBlock = 49152;  // coefficient slice <= 192 KB of SMEM
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Number of heads in slots [0, P): word prefix + partial word.
+__device__ __forceinline__ int32_t heads_before(const uint32_t* __restrict__ bm,
+                                                const uint32_t* __restrict__ pre, uint32_t P) {
+  const uint32_t wd = P >> 5, sh = P & 31u;
+  uint32_t c = __ldg(pre + wd);
+  if (sh) c += __popc(__ldg(bm + wd) & ((1u << sh) - 1u));
+  return static_cast<int32_t>(c);
+}
+
+// One warp's segmented stream over slots [P, Q), in tiles of 32*E slots
+// (lane l holds slots E*l .. E*l+E-1 of a tile).
+//   ld(s) -> the lane's E-slot window at s (s % E == 0)
+//   prod(win, p[E]) -> the E products
+//   close(X, z, first) -> segment ordinal X ends with sum z (the warp's first
+//                          closing is flagged: its segment began before P)
+// ord: ordinal of the segment holding slot P-1 on entry, of the segment open
+// at Q on exit; carry: the open segment's sum over [.., Q); had: a head was seen.
+// NB window buffers rotate through registers (static indices), so NB-1 tiles
+// of loads stay in flight while one is reduced.
+template <int E, int NB, class Win, class Ld, class Prod, class Close>
+__device__ __forceinline__ void seg_stream(uint32_t P, uint32_t Q, const uint32_t* __restrict__ bm,
+                                           int32_t& ord, float& carry, bool& had, Ld ld,
+                                           Prod prod, Close close) {
+  static_assert(E == 4 || E == 8, "4 or 8 slots per lane");
+  constexpr uint32_t TILE = 32 * E;
+  constexpr uint32_t EM = (1u << E) - 1u;
+  if (P >= Q) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  const uint32_t base = P & ~uint32_t(E - 1);
+  auto fetch = [&](uint32_t t, Win& w, uint32_t& m) {
+    uint32_t s = t + E * lane;
+    s = s < Q ? s : base;  // past the range: re-read a live line (no new traffic)
+    w = ld(s);
+    m = __ldg(bm + (s >> 5));
+  };
+  auto tile = [&](uint32_t t, Win& w, uint32_t& m) {
+    float p[E];
+    prod(w, p);
+    const uint32_t s0 = t + E * lane;
+    uint32_t hd = (m >> (s0 & 31u)) & EM;  // head bits of the lane's slots
+    fetch(t + TILE * NB, w, m);
+    if (!(t >= P && t + TILE <= Q)) {  // warp-uniform: first / last tile only
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        const bool in = s0 + u >= P && s0 + u < Q;
+        p[u] = in ? p[u] : 0.f;
+        hd = in ? hd : (hd & ~(1u << u));
+      }
+    }
+    const uint32_t H = __ballot_sync(kFull, hd != 0u);
+    const bool multi = __any_sync(kFull, (hd & (hd - 1u)) != 0u);
+    float pre = 0.f, post = 0.f;
+    int32_t hb;
+    int32_t heads;
+    if (!multi) {  // at most one head per lane (segments of >= E slots)
+      const int u0 = hd ? __ffs(hd) - 1 : E;
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        if (u < u0) pre += p[u];
+        else post += p[u];
+      }
+      hb = __popc(H & lt);
+      heads = __popc(H);
+    } else {  // short segments: several heads in a lane
+      hb = 0;
+      heads = 0;
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        const uint32_t B = __ballot_sync(kFull, (hd >> u) & 1u);
+        hb += __popc(B & lt);
+        heads += __popc(B);
+      }
+      float run = 0.f;
+      int seen = 0;
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        if ((hd >> u) & 1u) {
+          if (seen) close(ord + hb + seen, run, false);  // began at this lane's previous head
+          else pre = run;
+          run = 0.f;
+          ++seen;
+        }
+        run += p[u];
+      }
+      if (seen) post = run;
+      else pre = run;
+    }
+    // Segmented inclusive scan of the lanes' open sums; a lane with a head
+    // starts a new segment, the carried sum enters at lane 0.
+    float v = hd ? post : pre;
+    if (lane == 0 && !hd) v += carry;
+    const uint32_t Hle = H & (lt | (1u << lane));
+    const int src = Hle ? 31 - __clz(Hle) : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float o = __shfl_up_sync(kFull, v, off);
+      if (lane - off >= src) v += o;
+    }
+    float excl = __shfl_up_sync(kFull, v, 1);
+    if (lane == 0) excl = carry;
+    if (hd) close(ord + hb, excl + pre, !had && lane == __ffs(H) - 1);
+    carry = __shfl_sync(kFull, v, 31);
+    had = had || H != 0u;
+    ord += heads;
+  };
+  uint32_t t = base;
+  Win wb[NB];
+  uint32_t mb[NB];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) fetch(t + TILE * k, wb[k], mb[k]);
+  while (true) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      tile(t, wb[k], mb[k]);
+      t += TILE;
+      if (t >= Q) return;
+    }
+  }
+}
+
+struct CtaScratch {
+  float pl[kNW], pf[kNW];
+  int32_t pf_ord[kNW];
+  int32_t had[kNW], has_pf[kNW];
+  int32_t last;
+};
+
+// The CTA's slots [S0, S1) (S0 a segment start, S1 the next CTA's start):
+// split evenly over the warps (4-slot aligned), streamed, and the segments
+// cut between warps finished in slot order. emit(X, z) receives every
+// complete segment once.
+template <int E, int NB, class Win, class Ld, class Prod, class Emit>
+__device__ __forceinline__ void cta_segments(uint32_t S0, uint32_t S1, const uint32_t* __restrict__ bm,
+                                             const uint32_t* __restrict__ bpre, Ld ld, Prod prod,
+                                             Emit emit, CtaScratch& sc) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  auto split = [&](int k) -> uint32_t {
+    if (k <= 0) return S0;
+    if (k >= kNW) return S1;
+    const uint32_t s = static_cast<uint32_t>(S0 + (uint64_t(S1 - S0) * k) / kNW) & ~uint32_t(E - 1);
+    return max(s, S0);
+  };
+  const uint32_t P = split(w), Q = split(w + 1);
+  if (lane == 0) sc.has_pf[w] = 0;
+  __syncwarp();
+  // Ordinal of the CTA's first segment: closings of lower ordinals (the
+  // segment ending at S0 - 1) belong to the previous CTA and are dropped.
+  const int32_t xmin = S1 > S0 ? heads_before(bm, bpre, S0) : 0;
+  int32_t ord = S1 > S0 ? heads_before(bm, bpre, P) - 1 : 0;
+  float carry = 0.f;
+  bool had = false;
+  seg_stream<E, NB, Win>(P, Q, bm, ord, carry, had, ld, prod, [&](int32_t X, float z, bool first) {
+    if (X < xmin) return;
+    if (!first) {
+      emit(X, z);
+    } else {
+      sc.pf[w] = z;
+      sc.pf_ord[w] = X;
+      sc.has_pf[w] = 1;
+    }
+  });
+  __syncwarp();
+  if (lane == 0) {
+    sc.pl[w] = carry;
+    sc.had[w] = had;
+    if (w == kNW - 1 && S1 > S0) {  // the CTA end closes the open segment
+      if (had) {
+        emit(ord, carry);
+      } else {
+        sc.pf[w] = carry;
+        sc.pf_ord[w] = ord;
+        sc.has_pf[w] = 1;
+      }
+    }
+  }
+  __syncthreads();
+  // Segments cut between warps: the pieces in slot order — from the last
+  // warp before t that saw a head (its piece starts there), through the
+  // head-free warps, to warp t's piece up to its first closing.
+  if (threadIdx.x > 0 && threadIdx.x < kNW && sc.has_pf[threadIdx.x]) {
+    const int t = threadIdx.x;
+    int v0 = t - 1;
+    while (v0 > 0 && !sc.had[v0]) --v0;
+    float z = 0.f;
+    for (int v = v0; v < t; ++v) z += sc.pl[v];
+    emit(sc.pf_ord[t], z + sc.pf[t]);
+  }
+}
+
+// E = 8 slots per lane: two float4 of values + eight ids.
+struct WinR32 {
+  float4 v0, v1;
+  uint4 j0, j1;
+};
+struct WinR16 {
+  float4 v0, v1;
+  uint4 j;  // eight u16
+};
+struct WinC {
+  float4 v0, v1;
+  uint4 r;  // eight u16 block-local rows
+};
+constexpr int kE = 8;
+
+// K2s: margins and coefficients c = coef(z, y) of all local rows
+// (glm.cpp:30-34). The stream emits each row's margin z in place; once the
+// CTA's rows are all complete, the CTA turns its (contiguous) rows' margins
+// into coefficients with coalesced label loads — no label load on the
+// stream's emission path. One CTA per SM; the fp32 model is bulk-copied (1-D
+// TMA) into SMEM when it fits (SMEMW), else gathered through L1/L2. I16:
+// 16-bit column ids (d <= 65536).
+template <int TASK, bool SMEMW, bool I16>
+__global__ void __launch_bounds__(kNT, 1)
+    k2s_margin_kernel(const float* __restrict__ val, const void* __restrict__ idx,
+                      const uint32_t* __restrict__ bm, const uint32_t* __restrict__ bpre,
+                      const uint32_t* __restrict__ cta_slot, const uint32_t* __restrict__ row_of_ord,
+                      const float* __restrict__ y, uint32_t n, const float* __restrict__ w32, uint32_t d,
+                      float* __restrict__ coef) {
+  extern __shared__ __align__(16) float ws[];
+  __shared__ CtaScratch sc;
+  __shared__ uint64_t bar;
+  if (SMEMW && threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    const uint32_t total = round_up16(uint64_t(d + 1) * 4);  // w32 holds whole 16-byte groups
+    mbar_arrive_expect_tx(&bar, total);
+    for (uint32_t off = 0; off < total; off += 32768)
+      bulk_g2s(reinterpret_cast<char*>(ws) + off, reinterpret_cast<const char*>(w32) + off,
+               min(32768u, total - off), &bar);
+  }
+  __syncthreads();
+  const uint32_t S0 = __ldg(cta_slot + blockIdx.x), S1 = __ldg(cta_slot + blockIdx.x + 1);
+  const float* w = SMEMW ? ws : w32;
+  bool ready = !SMEMW;  // the first tiles' loads overlap the model's bulk copy
+  using Win = std::conditional_t<I16, WinR16, WinR32>;
+  cta_segments<kE, 2, Win>(
+      S0, S1, bm, bpre,
+      [&](uint32_t s) {
+        Win q;
+        q.v0 = __ldg(reinterpret_cast<const float4*>(val + s));
+        q.v1 = __ldg(reinterpret_cast<const float4*>(val + s + 4));
+        if constexpr (I16) {
+          q.j = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(idx) + s));
+        } else {
+          q.j0 = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(idx) + s));
+          q.j1 = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(idx) + s + 4));
+        }
+        return q;
+      },
+      [&](const Win& q, float* p) {
+        if (SMEMW && !ready) {
+          mbar_wait(&bar, 0);
+          ready = true;
+        }
+        uint32_t j[8];
+        if constexpr (I16) {
+          j[0] = q.j.x & 0xffffu, j[1] = q.j.x >> 16, j[2] = q.j.y & 0xffffu, j[3] = q.j.y >> 16;
+          j[4] = q.j.z & 0xffffu, j[5] = q.j.z >> 16, j[6] = q.j.w & 0xffffu, j[7] = q.j.w >> 16;
+        } else {
+          j[0] = q.j0.x, j[1] = q.j0.y, j[2] = q.j0.z, j[3] = q.j0.w;
+          j[4] = q.j1.x, j[5] = q.j1.y, j[6] = q.j1.z, j[7] = q.j1.w;
+        }
+        const float x[8] = {q.v0.x, q.v0.y, q.v0.z, q.v0.w, q.v1.x, q.v1.y, q.v1.z, q.v1.w};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) p[u] = x[u] * (SMEMW ? w[j[u]] : __ldg(w + j[u]));
+      },
+      [&](int32_t X, float z) { coef[row_of_ord ? __ldg(row_of_ord + X) : static_cast<uint32_t>(X)] = z; },
+      sc);
+  if (SMEMW && !ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
+  // cta_segments ends with the cut-segment fix-ups: wait for them, then the
+  // CTA's ordinals [xmin, xend) hold margins.
+  __syncthreads();
+  if (S1 <= S0) return;
+  const int32_t xmin = heads_before(bm, bpre, S0), xend = heads_before(bm, bpre, S1);
+  constexpr int KU = 8;  // rows per thread per round, all loads in flight together
+  for (int32_t o0 = xmin + threadIdx.x; o0 < xend; o0 += KU * kNT) {
+    uint32_t r[KU];
+    float z[KU], yy[KU];
+#pragma unroll
+    for (int i = 0; i < KU; ++i) {
+      const int32_t o = o0 + i * kNT;
+      r[i] = o < xend ? (row_of_ord ? __ldg(row_of_ord + o) : static_cast<uint32_t>(o)) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < KU; ++i) {
+      z[i] = __ldcg(coef + r[i]);
+      yy[i] = __ldg(y + r[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < KU; ++i)
+      if (o0 + i * kNT < xend) coef[r[i]] = coef_fast<TASK>(z[i], yy[i]);
+  }
+}
+
+struct ApplyArgs {
+  double alpha;
+  int apply, want_norm;
+  double* w64;
+  float* w32;
+  double* g64;
+  int* finite;
+  double* norm2;
+};
+
+// K3s: CTA (row block b, column range k) bulk-copies the block's coefficient
+// slice into SMEM, streams the block's segments of columns
+// [cta_col[k], cta_col[k+1]) against it, writing fp32 per-(block, column)
+// sums; the last CTA of column range k sums them over the blocks (fixed block
+// order, fp64) and applies w -= a g.
+__global__ void __launch_bounds__(kNT, 1)
+    k3s_grad_kernel(const float* __restrict__ cval, const uint16_t* __restrict__ crow,
+                    const uint32_t* __restrict__ bm, const uint32_t* __restrict__ bpre,
+                    const uint32_t* __restrict__ segptr, const uint32_t* __restrict__ cta_col,
+                    uint32_t cpb, uint32_t nblk, uint32_t d, uint32_t rb, uint32_t n,
+                    const float* __restrict__ coef, const uint32_t* __restrict__ seg_of_ord,
+                    float* __restrict__ part, unsigned* __restrict__ tickets, ApplyArgs aa) {
+  extern __shared__ __align__(16) float cs[];
+  __shared__ CtaScratch sc;
+  __shared__ uint64_t bar;
+  const uint32_t b = blockIdx.x / cpb, k = blockIdx.x % cpb;
+  const uint32_t r0 = b * rb, rows = min(rb, n - r0);  // rb % 4 == 0: 16-byte aligned slice
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    const uint32_t total = round_up16(uint64_t(rows) * 4);  // coef carries 16-byte slack
+    mbar_arrive_expect_tx(&bar, total);
+    for (uint32_t off = 0; off < total; off += 32768)
+      bulk_g2s(reinterpret_cast<char*>(cs) + off, reinterpret_cast<const char*>(coef + r0) + off,
+               min(32768u, total - off), &bar);
+  }
+  const uint32_t j0 = __ldg(cta_col + k), j1 = __ldg(cta_col + k + 1);
+  const uint64_t q0 = uint64_t(b) * d;
+  if (seg_of_ord)  // empty (block, column) segments are never emitted: zero them first
+    for (uint32_t j = j0 + threadIdx.x; j < j1; j += kNT) part[q0 + j] = 0.f;
+  __syncthreads();  // the barrier init is visible to every waiter
+  const uint32_t S0 = __ldg(segptr + q0 + j0), S1 = __ldg(segptr + q0 + j1);
+  bool ready = false;  // the first tiles' loads overlap the slice's bulk copy
+  cta_segments<kE, 2, WinC>(
+      S0, S1, bm, bpre,
+      [&](uint32_t s) {
+        WinC q;
+        q.v0 = __ldg(reinterpret_cast<const float4*>(cval + s));
+        q.v1 = __ldg(reinterpret_cast<const float4*>(cval + s + 4));
+        q.r = __ldg(reinterpret_cast<const uint4*>(crow + s));
+        return q;
+      },
+      [&](const WinC& q, float* p) {
+        if (!ready) {
+          mbar_wait(&bar, 0);
+          ready = true;
+        }
+        p[0] = q.v0.x * cs[q.r.x & 0xffffu], p[1] = q.v0.y * cs[q.r.x >> 16];
+        p[2] = q.v0.z * cs[q.r.y & 0xffffu], p[3] = q.v0.w * cs[q.r.y >> 16];
+        p[4] = q.v1.x * cs[q.r.z & 0xffffu], p[5] = q.v1.y * cs[q.r.z >> 16];
+        p[6] = q.v1.z * cs[q.r.w & 0xffffu], p[7] = q.v1.w * cs[q.r.w >> 16];
+      },
+      [&](int32_t X, float z) {
+        const uint32_t q = seg_of_ord ? __ldg(seg_of_ord + X) : static_cast<uint32_t>(X);
+        part[q] = z;
+      },
+      sc);
+  if (!ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(tickets + k, 1u);
+    sc.last = t == nblk - 1;
+    if (sc.last) tickets[k] = 0u;  // re-armed for the next launch
+  }
+  __syncthreads();
+  if (!sc.last) return;
+  __threadfence();
+  double nrm = 0.0;
+  int bad = 0;
+  for (uint32_t j = j0 + threadIdx.x; j < j1; j += kNT) {
+    // Block order; 8 loads in flight per thread (only d/cpb threads work here).
+    double g = 0.0;
+    uint32_t bb = 0;
+    for (; bb + 8 <= nblk; bb += 8) {
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __ldcg(part + uint64_t(bb + i) * d + j);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) g += static_cast<double>(v[i]);
+    }
+    for (; bb < nblk; ++bb) g += static_cast<double>(__ldcg(part + uint64_t(bb) * d + j));
+    if (!isfinite(g)) bad = 1;
+    if (aa.apply) {
+      const double wn = aa.w64[j] - aa.alpha * g;
+      aa.w64[j] = wn;
+      aa.w32[j] = static_cast<float>(wn);
+    } else {
+      aa.g64[j] = g;
+    }
+    nrm += g * g;
+  }
+  if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) *aa.finite = 0;
+  if (aa.want_norm) {
+    nrm = warp_sum_d(nrm);
+    if ((threadIdx.x & 31) == 0 && nrm != 0.0) atomicAdd(aa.norm2, nrm);
+  }
+}
+
+// ---- preparation (once per upload / refresh) ---------------------------------
+
+__global__ void row_heads_kernel(const uint32_t* __restrict__ rowptr, uint32_t n, uint32_t* bm,
+                                 uint32_t* nonempty, unsigned* n_empty) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const uint32_t s = rowptr[r], e = rowptr[r + 1];
+  const bool ne = e > s;
+  nonempty[r] = ne ? 1u : 0u;
+  if (ne) atomicOr(bm + (s >> 5), 1u << (s & 31u));
+  else atomicAdd(n_empty, 1u);
+}
+
+__global__ void popc_kernel(const uint32_t* __restrict__ bm, uint64_t nwords, uint32_t* out) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nwords) out[i] = __popc(bm[i]);
+  else if (i == nwords) out[i] = 0u;
+}
+
+// dst[pos[i]] = i where flag[i] (pos = exclusive prefix of flag).
+__global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                               uint64_t count, uint32_t* dst) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count && flag[i]) dst[pos[i]] = static_cast<uint32_t>(i);
+}
+
+// CTA k of the margin pass starts at the first row starting at or after
+// k*nnz/nc (a slot position).
+__global__ void cta_slot_kernel(const uint32_t* __restrict__ rowptr, uint32_t n, uint32_t nc,
+                                uint32_t* cta_slot) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > nc) return;
+  const uint64_t nnz = rowptr[n];
+  if (k == nc) {
+    cta_slot[k] = static_cast<uint32_t>(nnz);
+    return;
+  }
+  const uint32_t target = static_cast<uint32_t>(nnz * k / nc);
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    if (rowptr[mid] >= target) hi = mid;
+    else lo = mid + 1;
+  }
+  cta_slot[k] = rowptr[lo];
+}
+
+__global__ void narrow_u16_kernel(const uint32_t* __restrict__ src, uint64_t n, uint16_t* dst) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<uint16_t>(src[i]);
+}
+
+// Sort keys (block*d + column) and payloads (value bits << 16 | block-local
+// row) of every nonzero, warp per row.
+__global__ void csc_keys_kernel(const float* __restrict__ val, const uint32_t* __restrict__ idx,
+                                const uint32_t* __restrict__ rowptr, uint32_t n, uint32_t d,
+                                uint32_t rb, uint32_t* keys, uint64_t* pay) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t r = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const uint32_t b = static_cast<uint32_t>(r / rb), lr = static_cast<uint32_t>(r - uint64_t(b) * rb);
+    const uint32_t s1 = rowptr[r + 1];
+    for (uint32_t s = rowptr[r] + lane; s < s1; s += 32) {
+      keys[s] = b * d + idx[s];
+      pay[s] = (uint64_t(__float_as_uint(val[s])) << 16) | lr;
+    }
+  }
+}
+
+// Unpack the sorted payloads, write the CSC head bitmap (one ballot per 32
+// slots) and the segment pointers (segptr[q] = first slot of key >= q).
+__global__ void csc_unpack_kernel(const uint32_t* __restrict__ keys, const uint64_t* __restrict__ pay,
+                                  uint32_t nnz, uint32_t nseg, float* cval, uint16_t* crow,
+                                  uint32_t* bm, uint32_t* segptr) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t total = (uint64_t(nnz) + 32) & ~uint64_t(31);  // whole warps, one past the end
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    bool head = false;
+    if (i < nnz) {
+      const uint64_t p = pay[i];
+      cval[i] = __uint_as_float(static_cast<uint32_t>(p >> 16));
+      crow[i] = static_cast<uint16_t>(p & 0xffffu);
+      const uint32_t key = keys[i];
+      const uint32_t prev = i ? keys[i - 1] : 0u;
+      head = i == 0 || key != prev;
+      if (head)
+        for (uint32_t q = i ? prev + 1 : 0u; q <= key; ++q) segptr[q] = static_cast<uint32_t>(i);
+    } else if (i == nnz) {
+      for (uint32_t q = nnz ? keys[nnz - 1] + 1 : 0u; q <= nseg; ++q) segptr[q] = nnz;
+    }
+    const uint32_t word = __ballot_sync(kFull, head);
+    if ((threadIdx.x & 31) == 0) bm[i >> 5] = word;
+  }
+}
+
+__global__ void seg_nonempty_kernel(const uint32_t* __restrict__ segptr, uint32_t nseg, uint32_t* flag,
+                                    unsigned* n_empty) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nseg) return;
+  const bool ne = segptr[q + 1] > segptr[q];
+  flag[q] = ne ? 1u : 0u;
+  if (!ne) atomicAdd(n_empty, 1u);
+}
+
+// Column totals over the row blocks (for nnz-balanced column ranges).
+__global__ void col_count_kernel(const uint32_t* __restrict__ segptr, uint32_t d, uint32_t nblk,
+                                 uint32_t* cnt) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d) return;
+  uint32_t c = 0;
+  for (uint32_t b = 0; b < nblk; ++b) c += segptr[uint64_t(b) * d + j + 1] - segptr[uint64_t(b) * d + j];
+  cnt[j] = c;
+}
+
+// cta_col[k] = first column whose inclusive column prefix exceeds k*nnz/cpb.
+__global__ void cta_col_kernel(const uint32_t* __restrict__ incl, uint32_t d, uint32_t cpb,
+                               uint64_t nnz, uint32_t* cta_col) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > cpb) return;
+  if (k == 0 || k == cpb) {
+    cta_col[k] = k == 0 ? 0u : d;
+    return;
+  }
+  const uint64_t target = nnz * k / cpb;
+  uint32_t lo = 0, hi = d;  // first j with incl[j] > target
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    if (incl[mid] > target) hi = mid;
+    else lo = mid + 1;
+  }
+  cta_col[k] = lo;
+}
+
+unsigned grid_1d(uint64_t n, unsigned threads = 256) {
+  return static_cast<unsigned>(std::max<uint64_t>(1, (n + threads - 1) / threads));
+}
+
+template <class T>
+void d2h_sync(T* dst, const T* src, cudaStream_t s) {
+  check(cudaMemcpyAsync(dst, src, sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+  check(cudaStreamSynchronize(s), "prep sync");
+}
+
+// Exclusive prefix (nwords + 1 entries) of the popcounts of bitmap words.
+void word_prefix(Ctx& c, const uint32_t* bm, uint64_t nwords, DBuf<uint32_t>& pre, DBuf<unsigned char>& tmp) {
+  DBuf<uint32_t> cnt;
+  cnt.alloc(nwords + 1);
+  pre.alloc(nwords + 1);
+  prof_begin(c, "sparse_prep_kernel");
+  popc_kernel<<<grid_1d(nwords + 1), 256, 0, c.stream>>>(bm, nwords, cnt.p);
+  launched(c, "sparse_prep_kernel");
+  size_t bytes = 0;
+  check(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, pre.p, static_cast<int64_t>(nwords + 1), c.stream),
+        "cub scan size");
+  tmp.alloc(bytes);
+  check(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, pre.p, static_cast<int64_t>(nwords + 1), c.stream),
+        "cub scan");
+  check(cudaStreamSynchronize(c.stream), "prep sync");
+}
+
+// Compaction map of the set flags (count entries), exclusive-scan based.
+void compaction(Ctx& c, const uint32_t* flag, uint64_t count, DBuf<uint32_t>& map, DBuf<unsigned char>& tmp) {
+  DBuf<uint32_t> pos;
+  pos.alloc(count + 1);
+  size_t bytes = 0;
+  check(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag, pos.p, static_cast<int64_t>(count), c.stream),
+        "cub scan size");
+  tmp.alloc(bytes);
+  check(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, flag, pos.p, static_cast<int64_t>(count), c.stream),
+        "cub scan");
+  map.alloc(std::max<uint64_t>(1, count));
+  prof_begin(c, "sparse_prep_kernel");
+  compact_kernel<<<grid_1d(count), 256, 0, c.stream>>>(flag, pos.p, count, map.p);
+  launched(c, "sparse_prep_kernel");
+  check(cudaStreamSynchronize(c.stream), "prep sync");
+}
+
+// Row-block geometry: blocks of at most 49,152 rows (u16 ids, <= 192 KB
+// slice), and as many CTAs (blocks x column ranges) as SMs, one per SM.
+void choose_blocks(const Ctx& c, uint64_t n, uint32_t& rb, uint32_t& nblk, uint32_t& cpb) {
+  // Fewest row blocks: the apply tail reads nblk partials per coordinate.
+  const uint64_t nb = std::max<uint64_t>(1, (n + kMaxRowBlock - 1) / kMaxRowBlock);
+  const uint64_t sms = static_cast<uint64_t>(std::max(1, c.num_sms));
+  // rb % 8 == 0 keeps every coefficient slice 32-byte aligned (bulk copies, float4 groups).
+  rb = static_cast<uint32_t>(std::max<uint64_t>(8, ((n + nb - 1) / nb + 7) & ~uint64_t(7)));
+  nblk = static_cast<uint32_t>(std::max<uint64_t>(1, (n + rb - 1) / rb));
+  cpb = static_cast<uint32_t>(std::max<uint64_t>(1, sms / nblk));
+}
+
+}  // namespace
+
+void sparse_prep(Dataset& ds) {
+  if (ds.sparse_ready) return;
+  Ctx& c = *ds.ctx;
+  cudaStream_t s = c.stream;
+  const uint64_t n = ds.n, d = ds.d, nnz = ds.nnz;
+  if (d * std::max<uint64_t>(1, (n + kMaxRowBlock - 1) / kMaxRowBlock) * 4 >= (uint64_t(1) << 31) ||
+      n >= (uint64_t(1) << 31))
+    throw Unsupported("full-batch sparse step: rows and (row blocks x d) segments must fit 31 bits");
+  DBuf<unsigned char> tmp;
+  DBuf<unsigned> cnt;
+  cnt.alloc(2);
+  cnt.zero(s);
+  // Row heads, 16-bit ids, margin CTA partition.
+  const uint64_t nwords = (nnz + 256) / 32 + 2;
+  ds.rbm.alloc(nwords);
+  ds.rbm.zero(s);
+  {
+    DBuf<uint32_t> nonempty;
+    nonempty.alloc(std::max<uint64_t>(1, n));
+    prof_begin(c, "sparse_prep_kernel");
+    row_heads_kernel<<<grid_1d(n), 256, 0, s>>>(ds.rowptr.p, static_cast<uint32_t>(n), ds.rbm.p,
+                                                nonempty.p, cnt.p);
+    launched(c, "sparse_prep_kernel");
+    unsigned empty = 0;
+    d2h_sync(&empty, cnt.p, s);
+    ds.rows_empty = empty != 0;
+    if (ds.rows_empty) compaction(c, nonempty.p, n, ds.row_of_ord, tmp);
+  }
+  word_prefix(c, ds.rbm.p, nwords, ds.rbm_pre, tmp);
+  if (d <= 65536) {
+    ds.cidx16.alloc(nnz + 1024);
+    ds.cidx16.zero(s);
+    prof_begin(c, "sparse_prep_kernel");
+    narrow_u16_kernel<<<c.num_sms * 8, 256, 0, s>>>(ds.idx.p, nnz, ds.cidx16.p);
+    launched(c, "sparse_prep_kernel");
+  }
+  ds.cta_n = static_cast<uint32_t>(std::max(1, c.num_sms));
+  ds.cta_slot.alloc(ds.cta_n + 1);
+  prof_begin(c, "sparse_prep_kernel");
+  cta_slot_kernel<<<grid_1d(ds.cta_n + 1), 256, 0, s>>>(ds.rowptr.p, static_cast<uint32_t>(n), ds.cta_n,
+                                                         ds.cta_slot.p);
+  launched(c, "sparse_prep_kernel");
+
+  // Row-blocked CSC by a stable radix sort of (block, column) keys.
+  choose_blocks(c, n, ds.csc_rb, ds.csc_nblk, ds.csc_cpb);
+  const uint64_t nseg = uint64_t(ds.csc_nblk) * d;
+  ds.cval.alloc(nnz + 1024);
+  ds.crow.alloc(nnz + 1024);
+  ds.cval.zero(s);
+  ds.crow.zero(s);
+  ds.segptr.alloc(nseg + 1);
+  ds.cbm.alloc(nwords);
+  ds.cbm.zero(s);
+  if (nnz > 0) {
+    DBuf<uint32_t> k_in, k_out;
+    DBuf<uint64_t> p_in, p_out;
+    k_in.alloc(nnz);
+    k_out.alloc(nnz);
+    p_in.alloc(nnz);
+    p_out.alloc(nnz);
+    prof_begin(c, "sparse_prep_kernel");
+    csc_keys_kernel<<<c.num_sms * 8, 256, 0, s>>>(ds.val.p, ds.idx.p, ds.rowptr.p, static_cast<uint32_t>(n),
+                                                  static_cast<uint32_t>(d), ds.csc_rb, k_in.p, p_in.p);
+    launched(c, "sparse_prep_kernel");
+    int end_bit = 1;
+    while (end_bit < 32 && (uint64_t(1) << end_bit) < nseg) ++end_bit;
+    size_t bytes = 0;
+    check(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k_in.p, k_out.p, p_in.p, p_out.p,
+                                          static_cast<int64_t>(nnz), 0, end_bit, s),
+          "cub sort size");
+    tmp.alloc(bytes);
+    check(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k_in.p, k_out.p, p_in.p, p_out.p,
+                                          static_cast<int64_t>(nnz), 0, end_bit, s),
+          "cub sort");
+    prof_begin(c, "sparse_prep_kernel");
+    csc_unpack_kernel<<<c.num_sms * 8, 256, 0, s>>>(k_out.p, p_out.p, static_cast<uint32_t>(nnz),
+                                                    static_cast<uint32_t>(nseg), ds.cval.p, ds.crow.p,
+                                                    ds.cbm.p, ds.segptr.p);
+    launched(c, "sparse_prep_kernel");
+    check(cudaStreamSynchronize(s), "prep sync");
+  } else {
+    ds.segptr.zero(s);
+  }
+  word_prefix(c, ds.cbm.p, nwords, ds.cbm_pre, tmp);
+  {
+    DBuf<uint32_t> flag;
+    flag.alloc(std::max<uint64_t>(1, nseg));
+    prof_begin(c, "sparse_prep_kernel");
+    seg_nonempty_kernel<<<grid_1d(nseg), 256, 0, s>>>(ds.segptr.p, static_cast<uint32_t>(nseg), flag.p,
+                                                       cnt.p + 1);
+    launched(c, "sparse_prep_kernel");
+    unsigned empty = 0;
+    d2h_sync(&empty, cnt.p + 1, s);
+    ds.segs_empty = empty != 0;
+    if (ds.segs_empty) compaction(c, flag.p, nseg, ds.seg_of_ord, tmp);
+  }
+  {  // nnz-balanced column ranges, shared by every row block
+    DBuf<uint32_t> colc, incl;
+    colc.alloc(std::max<uint64_t>(1, d));
+    incl.alloc(std::max<uint64_t>(1, d));
+    prof_begin(c, "sparse_prep_kernel");
+    col_count_kernel<<<grid_1d(d), 256, 0, s>>>(ds.segptr.p, static_cast<uint32_t>(d), ds.csc_nblk, colc.p);
+    launched(c, "sparse_prep_kernel");
+    size_t bytes = 0;
+    check(cub::DeviceScan::InclusiveSum(nullptr, bytes, colc.p, incl.p, static_cast<int64_t>(d), s),
+          "cub scan size");
+    tmp.alloc(bytes);
+    check(cub::DeviceScan::InclusiveSum(tmp.p, bytes, colc.p, incl.p, static_cast<int64_t>(d), s), "cub scan");
+    ds.cta_col.alloc(ds.csc_cpb + 1);
+    prof_begin(c, "sparse_prep_kernel");
+    cta_col_kernel<<<grid_1d(ds.csc_cpb + 1), 256, 0, s>>>(incl.p, static_cast<uint32_t>(d), ds.csc_cpb, nnz,
+                                                            ds.cta_col.p);
+    launched(c, "sparse_prep_kernel");
+    check(cudaStreamSynchronize(s), "prep sync");
+  }
+  ds.coef.alloc(n + 8);
+  ds.coef.zero(s);
+  ds.sparse_tickets.alloc(ds.csc_cpb);
+  ds.sparse_tickets.zero(s);
+  check(cudaStreamSynchronize(s), "prep sync");
+  ds.sparse_ready = true;
+}
+
+void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a) {
+  sparse_prep(ds);
+  Ctx& c = *ds.ctx;
+  if (ds.n == 0) return;
+  const uint32_t d = static_cast<uint32_t>(ds.d);
+  // K2s
+  {
+    const size_t model_bytes = round_up16(uint64_t(d + 1) * 4);
+    const bool smemw = model_bytes + sizeof(CtaScratch) + 64 <= c.max_smem_optin;
+    const bool i16 = ds.cidx16.p != nullptr;
+    auto go = [&]<bool SW, bool I16>() {
+      auto kern = a.task == kTaskLR ? k2s_margin_kernel<kTaskLR, SW, I16> : k2s_margin_kernel<kTaskSVM, SW, I16>;
+      const size_t smem = SW ? model_bytes : 0;
+      set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(k2s)");
+      prof_begin(c, "k2s_margin_kernel");
+      kern<<<ds.cta_n, kNT, smem, c.stream>>>(ds.val.p, I16 ? static_cast<const void*>(ds.cidx16.p)
+                                                            : static_cast<const void*>(ds.idx.p),
+                                              ds.rbm.p, ds.rbm_pre.p, ds.cta_slot.p,
+                                              ds.rows_empty ? ds.row_of_ord.p : nullptr, ds.labels.p,
+                                              static_cast<uint32_t>(ds.n), m.w32.p, d, ds.coef.p);
+      launched(c, "k2s_margin_kernel");
+    };
+    if (smemw && i16) go.template operator()<true, true>();
+    else if (smemw) go.template operator()<true, false>();
+    else if (i16) go.template operator()<false, true>();
+    else go.template operator()<false, false>();
+  }
+  // K3s
+  {
+    m.part32.alloc(uint64_t(ds.csc_nblk) * d + 1);
+    const size_t smem = round_up16(uint64_t(ds.csc_rb) * 4);
+    auto kern = k3s_grad_kernel;
+    set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(k3s)");
+    ApplyArgs aa{a.alpha, a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p, m.finite.p, m.scal.p};
+    prof_begin(c, "k3s_grad_kernel");
+    kern<<<ds.csc_nblk * ds.csc_cpb, kNT, smem, c.stream>>>(
+        ds.cval.p, ds.crow.p, ds.cbm.p, ds.cbm_pre.p, ds.segptr.p, ds.cta_col.p, ds.csc_cpb, ds.csc_nblk, d,
+        ds.csc_rb, static_cast<uint32_t>(ds.n), ds.coef.p,
+        ds.segs_empty ? ds.seg_of_ord.p : nullptr, m.part32.p, ds.sparse_tickets.p, aa);
+    launched(c, "k3s_grad_kernel");
+  }
+}
+
+}  // namespace sgdb::dev

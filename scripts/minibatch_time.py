@@ -46,7 +46,6 @@ def main():
             ms = float(np.median(times[2:]))
             print(json.dumps({"data": name, "B": B, "steps": steps, "epoch_ms": ms,
                               "us_per_step": ms * 1e3 / steps,
-                              "persistent": not os.environ.get("SGDB_NO_PERSISTENT_EPOCH"),
                               "loss": S.device_loss(dds, model, task)}), flush=True)
 
 

@@ -1,14 +1,16 @@
-"""Edge cases of the full-batch sparse passes (segmented warp stream, K2t/K3t).
+"""Edge cases of the full-batch sparse passes (K2s / K3s, kernels_sparse.cu).
 
 The margin pass and the blocked-CSC gradient pass walk each warp's nonzeros
-in 128-slot tiles and recover per-row / per-column sums with a segmented warp
-scan (paper_1802_08800_b200/csrc/segstream.cuh). These inputs put segment
-boundaries where that bookkeeping can go wrong: empty rows (single, in runs
-longer than the 32-entry pointer chunk, leading and trailing), one-slot rows,
-more rows in one tile than a chunk holds, rows spanning many tiles, and a
-model too wide to stage in shared memory. Full-batch gradients are compared
-with the CPU oracle (proj/src/sync_engine.cpp:22-42 restated) at the sync
-tolerance of DESIGN.md §Numerics.
+in 128-slot tiles, find segment boundaries in a head bitmap and recover
+per-row / per-(block, column) sums with a segmented warp scan; segments cut
+between warps are finished in SMEM, empty segments go through ordinal maps.
+These inputs put boundaries where that bookkeeping can go wrong: empty rows
+(single, in long runs, leading and trailing), one-slot rows (several heads
+per lane), rows spanning many tiles and warps, tiny inputs (most warps
+empty), a model too wide to stage in shared memory, 32-bit column ids, and
+more row blocks than SMs. Full-batch gradients are compared with the CPU
+oracle (proj/src/sync_engine.cpp:22-42 restated) at the sync tolerance of
+DESIGN.md §Numerics.
 """
 import numpy as np
 import pytest
@@ -51,11 +53,9 @@ SHAPES = _shapes()
 
 @pytest.mark.parametrize("name", sorted(SHAPES))
 @pytest.mark.parametrize("d", [600, 100_000])
-@pytest.mark.parametrize("split", ["0", "1"])
-def test_full_batch_gradient_segments(sgdb, dev, orc, name, d, split, monkeypatch):
-    """split=1: warps take equal nonzero ranges and rows cut by warp boundaries
-    are finished from per-warp pieces; split=0: whole rows per warp."""
-    monkeypatch.setenv("SGDB_SEG_SPLIT", split)
+def test_full_batch_gradient_segments(sgdb, dev, orc, name, d):
+    """d = 600: model in SMEM, 16-bit ids; d = 100,000: model gathered from
+    L2, 32-bit ids."""
     S = sgdb
     lengths = [min(ln, d) for ln in SHAPES[name]]
     ds = _csr(S, lengths, d, seed=len(lengths) + d)
@@ -83,25 +83,83 @@ def test_full_batch_epochs_segments(sgdb, dev, orc, name):
         assert rel_l2(model.get(), om[e]) <= 1e-5
 
 
-def test_refresh_drops_csc_copy(sgdb, dev):
-    """sgdb_dataset_refresh_f32 re-copies CSR arrays but not the row-blocked CSC
-    copy built at upload: full-batch sync must fail loudly afterwards (not read
-    stale values), while Hogwild and a fresh upload keep working."""
+def test_refresh_rebuilds_full_batch_structures(sgdb, dev, orc):
+    """sgdb_dataset_refresh_f32 with new values, column ids and row offsets
+    (same n, nnz): the head bitmaps, 16-bit ids and the blocked CSC are
+    rebuilt on the device, so full-batch gradients, the mini-batch chunk plan
+    (longest row recomputed) and Hogwild all see the new data."""
     S = sgdb
-    ds = S.fixtures.sparse_classification(500, 80, 6.0, 31).rounded_f32()
-    dds = S.DeviceDataset(dev, ds)
-    model = S.DeviceModel(dev, ds.n_features)
-    assert S.sync_epoch(dds, model, S.Task.LR, 0.1, None, ds.n_examples)
-    new_vals = np.ascontiguousarray(ds.values.astype(np.float32) * 2.0)
-    dds.refresh_f32(new_vals)
+    a = S.fixtures.sparse_classification(3000, 500, 12.0, 31).rounded_f32()
+    dds = S.DeviceDataset(dev, a)
+    model = S.DeviceModel(dev, a.n_features)
+    assert S.sync_epoch(dds, model, S.Task.LR, 0.1, None, a.n_examples)
+    # Same nnz, different rows: rotate the slots by one row's worth so every
+    # row boundary moves, and make one row much longer than any before.
+    rng = np.random.default_rng(4)
+    nnz = a.values.size
+    lens = np.diff(a.row_offsets.astype(np.int64))
+    lens = np.roll(lens, 7)
+    lens[0] += 200
+    lens[1:201] -= np.minimum(lens[1:201] - 1, 1)
+    lens[-1] += nnz - lens.sum()
+    assert lens.min() >= 0 and lens.sum() == nnz
+    rows = np.zeros(a.n_examples + 1, np.uint64)
+    np.cumsum(lens, out=rows[1:])
+    idx = np.empty(nnz, np.uint32)
+    for r in range(a.n_examples):
+        lo, hi = int(rows[r]), int(rows[r + 1])
+        idx[lo:hi] = np.sort(rng.choice(a.n_features, hi - lo, replace=False))
+    vals = rng.uniform(-1, 1, nnz).astype(np.float32)
+    labs = np.where(rng.random(a.n_examples) < 0.5, -1.0, 1.0).astype(np.float32)
+    b = S.Dataset(a.n_examples, a.n_features, S.Layout.Csr, labels=labs.astype(np.float64),
+                  values=vals.astype(np.float64), indices=idx, row_offsets=rows)
+    dds.refresh_f32(vals, labs, idx, rows.astype(np.uint32))
     dev.synchronize()
+    w = rng.normal(0, 0.3, a.n_features)
+    for task in (0, 1):
+        g = S.sync.batch_gradient(S.Task(task), dds, None, w, device=dev)
+        assert rel_l2(g, orc.batch_gradient(b, task, None, w)) <= 1e-5
+        rows_b = np.sort(rng.choice(a.n_examples, 400, replace=False)).astype(np.uint32)
+        g = S.sync.batch_gradient(S.Task(task), dds, rows_b, w, device=dev)
+        assert rel_l2(g, orc.batch_gradient(b, task, rows_b, w)) <= 1e-5
+    m2 = S.DeviceModel(dev, a.n_features)
+    sched = S.Schedule(3, a.n_examples)
+    om, ol, _ = orc.sync_train(b, 1, 0.05, 256, 2, 3)
+    for e in range(2):
+        assert S.sync_epoch(dds, m2, S.Task.SVM, 0.05, sched.next(), 256)
+        assert rel_l2(m2.get(), om[e]) <= 1e-5
+
+
+def test_refresh_dense_rebuilds_column_copy(sgdb, dev, orc):
+    """Dense refresh invalidates the column-major copy the col-* Hogwild paths
+    read: a one-worker col-rr epoch after the refresh trains on
+    the new values."""
+    S = sgdb
+    a = S.fixtures.dense_classification(400, 16, 8).rounded_f32()
+    b = S.fixtures.dense_classification(400, 16, 9).rounded_f32()
+    col_a = S.convert_layout(a, S.Layout.DenseColMajor)
+    dds = S.DeviceDataset(dev, col_a)
+    plan = S.parse_plan("col-rr:kernel:0")
+    plan.workers = 1
+    m = S.DeviceModel(dev, a.n_features)
+    S.hogwild_epoch(dds, m, S.Task.LR, 0.05, plan)  # builds the column copy from a
+    dds.refresh_f32(np.ascontiguousarray(b.values.astype(np.float32)),
+                    np.ascontiguousarray(b.labels.astype(np.float32)))
+    m.set(np.zeros(a.n_features))
+    S.hogwild_epoch(dds, m, S.Task.LR, 0.05, plan)
+    om, _, _ = orc.hogwild_serial(S.convert_layout(b, S.Layout.DenseColMajor), 0, 0.05, 1, 1, 0, 0, 1)
+    assert rel_l2(m.get(), om[-1]) <= 1e-4
+
+
+def test_refresh_rejects_exact_and_padded(sgdb, dev):
+    S = sgdb
+    a = S.fixtures.sparse_classification(200, 50, 5.0, 2).rounded_f32()
+    exact = S.DeviceDataset(dev, a, exact=True)
     with pytest.raises(S.UnsupportedError):
-        S.sync_epoch(dds, model, S.Task.LR, 0.1, None, ds.n_examples)
-    plan = S.parse_plan("row-ch:kernel:0")
-    plan.workers = 4
-    S.hogwild_epoch(dds, model, S.Task.LR, 0.1, plan)
-    fresh = S.DeviceDataset(dev, ds)
-    assert S.sync_epoch(fresh, model, S.Task.LR, 0.1, None, ds.n_examples)
+        exact.refresh_f32(np.ascontiguousarray(a.values.astype(np.float32)))
+    padded = S.DeviceDataset(dev, S.convert_layout(a, S.Layout.PaddedDense))
+    with pytest.raises(S.UnsupportedError):
+        padded.refresh_f32(np.ascontiguousarray(a.values.astype(np.float32)))
 
 
 @pytest.mark.parametrize("nnz_tail", [0, 3])
@@ -137,3 +195,27 @@ def test_refresh_idx16_rejects_wide_models(sgdb, dev):
     dds = S.DeviceDataset(dev, ds)
     with pytest.raises(Exception):
         dds.refresh_idx16(np.zeros(ds.nnz, np.uint16))
+
+
+def test_more_row_blocks_than_sms(sgdb, dev, orc):
+    """7.5M rows: more row blocks of the CSC (<= 49,152 rows each) than SMs, so
+    the gradient pass runs several waves of CTAs (no co-residency assumed)."""
+    S = sgdb
+    rng = np.random.default_rng(9)
+    n, d = 7_500_000, 40
+    lens = rng.integers(1, 4, n)
+    rows = np.zeros(n + 1, np.uint64)
+    np.cumsum(lens, out=rows[1:])
+    nnz = int(rows[-1])
+    idx = rng.integers(0, d, nnz).astype(np.uint32)
+    # column ids must be unique within a row: take distinct offsets per slot
+    pos = np.arange(nnz) - np.repeat(rows[:-1].astype(np.int64), lens)
+    idx = ((np.repeat(rng.integers(0, d, n), lens) + pos * 7) % d).astype(np.uint32)
+    val = rng.uniform(-1, 1, nnz).astype(np.float32).astype(np.float64)
+    y = np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    ds = S.Dataset(n, d, S.Layout.Csr, labels=y, values=val, indices=idx, row_offsets=rows)
+    w = rng.normal(0, 0.5, d)
+    for task in (0, 1):
+        g = S.sync.batch_gradient(S.Task(task), ds, None, w, device=dev)
+        og = orc.batch_gradient(ds, task, None, w)
+        assert rel_l2(g, og) <= 1e-5, (task, rel_l2(g, og))
