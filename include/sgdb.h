@@ -164,8 +164,9 @@ typedef struct sgdb_train_options {
 
 /* Collective hook for multi-GPU runs: called by the engine at each exchange
  * step with a device buffer to SUM-reduce in place across ranks on `stream`
- * (dtype 0 = float32, 1 = float64). Provided by the host's process group
- * (torch.distributed / NCCL); the engine never owns a communicator. */
+ * (dtype 0 = float32, 1 = float64), for hosts that bring their own process
+ * group. The engine can also own an NCCL communicator (sgdb_ctx_init_nccl),
+ * which takes precedence. */
 typedef int32_t (*sgdb_allreduce_fn)(void* user, void* device_buffer, uint64_t count,
                                      int32_t dtype, void* stream);
 
@@ -192,6 +193,16 @@ sgdb_status sgdb_ctx_synchronize(sgdb_ctx* ctx);
 /* Number of this library's kernels launched on the context so far. */
 sgdb_status sgdb_ctx_launch_count(sgdb_ctx* ctx, uint64_t* out);
 sgdb_status sgdb_ctx_set_allreduce(sgdb_ctx* ctx, sgdb_allreduce_fn fn, void* user);
+/* In-library NCCL communicator (multi-GPU without a host collective
+ * provider; generalises numa_dual_train's replica exchange,
+ * proj/src/async_engine.cpp:462-520, to G GPUs). Rank 0 creates the 128-byte
+ * id, the host distributes it (any channel), every rank attaches its context.
+ * The engine then SUM-reduces gradients / models / losses with ncclAllReduce
+ * on the context stream — mini-batch steps stay CUDA-graph-replayed. NCCL is
+ * resolved at run time (libnccl.so.2); absent -> SGDB_ERR_RUNTIME. */
+sgdb_status sgdb_nccl_get_unique_id(uint8_t* id_out /* 128 bytes */);
+sgdb_status sgdb_ctx_init_nccl(sgdb_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t* id);
+sgdb_status sgdb_ctx_world(sgdb_ctx* ctx, int32_t* rank, int32_t* nranks);
 /* Per-launch CUDA-event timing of this library's kernels on the context
  * stream (off by default; enabling clears earlier records). Entry i of the
  * per-kernel aggregate: name, launches, total milliseconds; *n_entries is the

@@ -73,6 +73,9 @@ PROTOTYPES = {
     "sgdb_ctx_synchronize": (_S, [vp]),
     "sgdb_ctx_launch_count": (_S, [vp, P(u64)]),
     "sgdb_ctx_set_allreduce": (_S, [vp, ALLREDUCE_FN, vp]),
+    "sgdb_nccl_get_unique_id": (_S, [C.c_char_p]),
+    "sgdb_ctx_init_nccl": (_S, [vp, i32, i32, C.c_char_p]),
+    "sgdb_ctx_world": (_S, [vp, C.POINTER(i32), C.POINTER(i32)]),
     "sgdb_ctx_resident_workers": (_S, [vp, vp, i32, P(u64)]),
     "sgdb_ctx_set_profiling": (_S, [vp, i32]),
     "sgdb_ctx_kernel_stats": (_S, [vp, u64, C.c_char_p, u64, P(u64), P(dbl), P(u64)]),

@@ -409,6 +409,27 @@ class Device:
         self._allreduce_cb = L.ALLREDUCE_FN(tramp)
         check(_lib().sgdb_ctx_set_allreduce(self._h, self._allreduce_cb, None))
 
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        """A fresh 128-byte NCCL id (rank 0 creates it, the host distributes it)."""
+        buf = C.create_string_buffer(128)
+        check(_lib().sgdb_nccl_get_unique_id(buf))
+        return buf.raw
+
+    def init_nccl(self, nranks: int, rank: int, uid: bytes) -> None:
+        """Attach an in-library NCCL communicator (sgdb_ctx_init_nccl): the
+        engine's gradient / model / loss reductions run as ncclAllReduce on
+        this context's stream."""
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        check(_lib().sgdb_ctx_init_nccl(self._h, nranks, rank, uid))
+
+    def world(self) -> tuple[int, int]:
+        """(rank, nranks) of the attached communicator ((0, 1) without one)."""
+        r, n = L.i32(0), L.i32(0)
+        check(_lib().sgdb_ctx_world(self._h, C.byref(r), C.byref(n)))
+        return int(r.value), int(n.value)
+
     def close(self):
         if getattr(self, "_h", None):
             _lib().sgdb_ctx_destroy(self._h)

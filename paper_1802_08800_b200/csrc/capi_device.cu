@@ -3,6 +3,7 @@
 // epoch, replica averaging, loss). Host code only; kernels live in
 // kernels_sync.cu / kernels_hogwild.cu.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <map>
 #include <mutex>
@@ -116,7 +117,57 @@ int read_finite(sgdb_model* m) {
   return *c.pinned_flag != 0 ? 1 : 0;
 }
 
+// NCCL, resolved at run time (dlopen "libnccl.so.2": the copy already in the
+// process when a host framework loaded one, else the system library), so the
+// engine carries no link dependency and single-GPU use never needs NCCL.
+// Types and entry points follow nccl.h (NCCL 2.x ABI).
+struct NcclUid {
+  char internal[128];
+};
+struct NcclApi {
+  using GetUid = int (*)(NcclUid*);
+  using InitRank = int (*)(void**, int, NcclUid, int);
+  using AllReduce = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+  using Destroy = int (*)(void*);
+  using ErrStr = const char* (*)(int);
+  GetUid get_uid = nullptr;
+  InitRank init_rank = nullptr;
+  AllReduce all_reduce = nullptr;
+  Destroy destroy = nullptr;
+  ErrStr err = nullptr;
+};
+constexpr int kNcclSum = 0, kNcclFloat32 = 7, kNcclFloat64 = 8;
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_uid = reinterpret_cast<NcclApi::GetUid>(dlsym(h, "ncclGetUniqueId"));
+    a.init_rank = reinterpret_cast<NcclApi::InitRank>(dlsym(h, "ncclCommInitRank"));
+    a.all_reduce = reinterpret_cast<NcclApi::AllReduce>(dlsym(h, "ncclAllReduce"));
+    a.destroy = reinterpret_cast<NcclApi::Destroy>(dlsym(h, "ncclCommDestroy"));
+    a.err = reinterpret_cast<NcclApi::ErrStr>(dlsym(h, "ncclGetErrorString"));
+    return a;
+  }();
+  if (!api.get_uid || !api.init_rank || !api.all_reduce || !api.destroy)
+    throw std::runtime_error("NCCL (libnccl.so.2) is not available");
+  return api;
+}
+
+void nccl_check(int r, const char* what) {
+  if (r != 0)
+    throw std::runtime_error(std::string(what) + ": " + (nccl().err ? nccl().err(r) : "NCCL error"));
+}
+
 void call_allreduce(Ctx& c, void* ptr, uint64_t count, int dtype) {
+  if (c.nccl_comm) {
+    nccl_check(nccl().all_reduce(ptr, ptr, count, dtype == 0 ? kNcclFloat32 : kNcclFloat64, kNcclSum,
+                                 c.nccl_comm, c.stream),
+               "ncclAllReduce");
+    return;
+  }
   if (!c.allreduce) return;
   if (c.allreduce(c.allreduce_user, ptr, count, dtype, c.stream) != 0)
     throw std::runtime_error("allreduce hook failed");
@@ -201,6 +252,7 @@ sgdb_status sgdb_ctx_destroy(sgdb_ctx* ctx) {
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->pinned_flag) cudaFreeHost(ctx->pinned_flag);
     if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
+    if (ctx->nccl_comm) nccl().destroy(ctx->nccl_comm);
     delete ctx;
   });
 }
@@ -264,11 +316,45 @@ sgdb_status sgdb_ctx_kernel_stats(sgdb_ctx* ctx, uint64_t i, char* name, uint64_
   });
 }
 
+sgdb_status sgdb_nccl_get_unique_id(uint8_t* id_out) {
+  return sgdb_guard([&] {
+    require(id_out != nullptr, "null argument");
+    NcclUid uid{};
+    nccl_check(nccl().get_uid(&uid), "ncclGetUniqueId");
+    std::memcpy(id_out, uid.internal, sizeof(uid.internal));
+  });
+}
+
+sgdb_status sgdb_ctx_init_nccl(sgdb_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t* id) {
+  return sgdb_guard([&] {
+    require(ctx && id, "null argument");
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "rank out of range");
+    require(ctx->nccl_comm == nullptr, "the context already has a communicator");
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    NcclUid uid{};
+    std::memcpy(uid.internal, id, sizeof(uid.internal));
+    void* comm = nullptr;
+    nccl_check(nccl().init_rank(&comm, nranks, uid, rank), "ncclCommInitRank");
+    ctx->nccl_comm = comm;
+    ctx->nccl_rank = rank;
+    ctx->nccl_nranks = nranks;
+  });
+}
+
+sgdb_status sgdb_ctx_world(sgdb_ctx* ctx, int32_t* rank, int32_t* nranks) {
+  return sgdb_guard([&] {
+    require(ctx != nullptr, "null argument");
+    if (rank) *rank = ctx->nccl_rank;
+    if (nranks) *nranks = ctx->nccl_nranks;
+  });
+}
+
 sgdb_status sgdb_model_average_ranks(sgdb_ctx* ctx, sgdb_model* m, uint64_t world) {
   return sgdb_guard([&] {
     require(world >= 1, "world size must be >= 1");
-    if (world == 1) return;
-    if (!ctx->allreduce) throw std::invalid_argument("no allreduce hook set on the context");
+    if (world == 1 && !has_collective(*ctx)) return;
+    if (!has_collective(*ctx))
+      throw std::invalid_argument("no collective on the context (sgdb_ctx_init_nccl or an allreduce hook)");
     materialize(*m);
     dense_written(*m);
     call_allreduce(*ctx, m->w64.p, m->d, 1);
@@ -566,7 +652,9 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
       if (finite_out) *finite_out = read_finite(m);
       return;
     }
-    const bool hook = c.allreduce != nullptr;
+    // With a cross-rank collective every step's gradient is SUM-reduced
+    // before the identical update on every rank.
+    const bool hook = has_collective(c);
     StepArgs a;
     a.task = task;
     a.alpha = alpha;
@@ -600,21 +688,22 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
           else csr_batch_step(*ds, *m, ids, nb, sa);
           if (hook) {
             call_allreduce(c, m->g64.p, m->d, 1);
-            apply_update(*m, alpha, false);
+            apply_update(*m, alpha, false, sa.alpha_dev);
           }
         }
       };
       if (!hook && ds->kind == Kind::Dense && ng > batch_b &&
           dense_epoch(*ds, *m, task, alpha, batch_b)) {
         // K1c: the whole epoch in one persistent launch
-      } else if (hook || ng / batch_b < 4) {
+      } else if (c.allreduce || ng / batch_b < 4) {
+        // (a host hook cannot be captured; NCCL steps are graph-replayed)
         run_steps(a);
       } else {
         // Launch-bound many-step epoch: replay a captured CUDA graph of the
         // whole step sequence (captured once per dataset / batch size / task;
         // the step size is read from device memory).
         if (!(m->epoch_graph && m->graph_ds == ds->uid && m->graph_b == batch_b &&
-              m->graph_task == task)) {
+              m->graph_task == task && m->graph_comm == c.nccl_comm)) {
           if (m->epoch_graph) cudaGraphExecDestroy(m->epoch_graph);
           m->epoch_graph = nullptr;
           m->alpha_dev.alloc(1);
@@ -647,6 +736,7 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
           m->graph_ds = ds->uid;
           m->graph_b = batch_b;
           m->graph_task = task;
+          m->graph_comm = c.nccl_comm;
         }
         h2d(m->alpha_dev.p, &alpha, 1, c.stream);  // pageable source: staged before return
         prof_begin(c, "sync_epoch_graph");
@@ -720,11 +810,11 @@ sgdb_status sgdb_epoch_batch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int
     StepArgs a;
     a.task = task;
     a.alpha = alpha;
-    a.apply = c.allreduce == nullptr;
+    a.apply = !has_collective(c);
     a.want_norm = true;
     set_finite(m);
     full_step(ds, m, a);
-    if (c.allreduce) {
+    if (has_collective(c)) {
       call_allreduce(c, m->g64.p, m->d, 1);
       apply_update(*m, alpha, true);
     }

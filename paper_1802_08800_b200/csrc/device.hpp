@@ -57,6 +57,10 @@ struct Ctx {
   uint64_t launches = 0;
   sgdb_allreduce_fn allreduce = nullptr;
   void* allreduce_user = nullptr;
+  // In-library NCCL communicator (sgdb_ctx_init_nccl): SUM all-reduces are
+  // issued on the context stream (CUDA-graph capturable, no host hop).
+  void* nccl_comm = nullptr;
+  int nccl_rank = 0, nccl_nranks = 1;
   DBuf<double> loss_partials;  // per-block loss sums
   DBuf<double> loss_out;       // [0] loss, [1] scratch
   DBuf<unsigned> tickets;      // [0] loss ticket
@@ -140,6 +144,14 @@ struct Dataset {
   DBuf<uint32_t> segptr, cbm, cbm_pre, seg_of_ord, cta_col;
   bool segs_empty = false;
   DBuf<unsigned> sparse_tickets;
+  // sparse_prep's scratch, kept so a rebuild after every refresh (bench
+  // e2e) neither allocates nor frees (cudaFree synchronises the device).
+  struct {
+    DBuf<uint32_t> k_in, k_out, a, b, c;
+    DBuf<uint64_t> p_in, p_out;
+    DBuf<unsigned char> tmp;
+    DBuf<unsigned> cnt;
+  } prep;
   // Column-major copies for the col-* access paths (built lazily).
   bool col_built = false;
   DBuf<float> xcol;    // dense: d*n
@@ -209,6 +221,7 @@ struct Model {
   cudaGraphExec_t epoch_graph = nullptr;
   uint64_t graph_ds = 0, graph_b = 0, graph_nodes = 0;
   int graph_task = -1;
+  void* graph_comm = nullptr;  // the NCCL communicator captured into the graph
   DBuf<double> alpha_dev;
   Model() = default;
   Model(const Model&) = delete;
@@ -217,6 +230,9 @@ struct Model {
     if (epoch_graph) cudaGraphExecDestroy(epoch_graph);
   }
 };
+
+// A cross-rank collective is attached (NCCL communicator or host hook).
+inline bool has_collective(const Ctx& c) { return c.nccl_comm != nullptr || c.allreduce != nullptr; }
 
 // ---- launchers (kernels_*.cu) -------------------------------------------------
 

@@ -595,15 +595,9 @@ unsigned grid_1d(uint64_t n, unsigned threads = 256) {
   return static_cast<unsigned>(std::max<uint64_t>(1, (n + threads - 1) / threads));
 }
 
-template <class T>
-void d2h_sync(T* dst, const T* src, cudaStream_t s) {
-  check(cudaMemcpyAsync(dst, src, sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
-  check(cudaStreamSynchronize(s), "prep sync");
-}
-
 // Exclusive prefix (nwords + 1 entries) of the popcounts of bitmap words.
-void word_prefix(Ctx& c, const uint32_t* bm, uint64_t nwords, DBuf<uint32_t>& pre, DBuf<unsigned char>& tmp) {
-  DBuf<uint32_t> cnt;
+void word_prefix(Ctx& c, const uint32_t* bm, uint64_t nwords, DBuf<uint32_t>& pre, DBuf<unsigned char>& tmp,
+                 DBuf<uint32_t>& cnt) {
   cnt.alloc(nwords + 1);
   pre.alloc(nwords + 1);
   prof_begin(c, "sparse_prep_kernel");
@@ -613,26 +607,26 @@ void word_prefix(Ctx& c, const uint32_t* bm, uint64_t nwords, DBuf<uint32_t>& pr
   check(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, pre.p, static_cast<int64_t>(nwords + 1), c.stream),
         "cub scan size");
   tmp.alloc(bytes);
+  bytes = tmp.n;
   check(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, pre.p, static_cast<int64_t>(nwords + 1), c.stream),
         "cub scan");
-  check(cudaStreamSynchronize(c.stream), "prep sync");
 }
 
 // Compaction map of the set flags (count entries), exclusive-scan based.
-void compaction(Ctx& c, const uint32_t* flag, uint64_t count, DBuf<uint32_t>& map, DBuf<unsigned char>& tmp) {
-  DBuf<uint32_t> pos;
+void compaction(Ctx& c, const uint32_t* flag, uint64_t count, DBuf<uint32_t>& map, DBuf<unsigned char>& tmp,
+                DBuf<uint32_t>& pos) {
   pos.alloc(count + 1);
   size_t bytes = 0;
   check(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flag, pos.p, static_cast<int64_t>(count), c.stream),
         "cub scan size");
   tmp.alloc(bytes);
+  bytes = tmp.n;
   check(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, flag, pos.p, static_cast<int64_t>(count), c.stream),
         "cub scan");
   map.alloc(std::max<uint64_t>(1, count));
   prof_begin(c, "sparse_prep_kernel");
   compact_kernel<<<grid_1d(count), 256, 0, c.stream>>>(flag, pos.p, count, map.p);
   launched(c, "sparse_prep_kernel");
-  check(cudaStreamSynchronize(c.stream), "prep sync");
 }
 
 // Row-block geometry: blocks of at most 49,152 rows (u16 ids, <= 192 KB
@@ -654,33 +648,24 @@ void sparse_prep(Dataset& ds) {
   Ctx& c = *ds.ctx;
   cudaStream_t s = c.stream;
   const uint64_t n = ds.n, d = ds.d, nnz = ds.nnz;
-  if (d * std::max<uint64_t>(1, (n + kMaxRowBlock - 1) / kMaxRowBlock) * 4 >= (uint64_t(1) << 31) ||
+  if (d * std::max<uint64_t>(1, (n + kMaxRowBlock - 1) / kMaxRowBlock) >= (uint64_t(1) << 31) ||
       n >= (uint64_t(1) << 31))
     throw Unsupported("full-batch sparse step: rows and (row blocks x d) segments must fit 31 bits");
-  DBuf<unsigned char> tmp;
-  DBuf<unsigned> cnt;
-  cnt.alloc(2);
-  cnt.zero(s);
+  auto& sp = ds.prep;
+  sp.cnt.alloc(2);
+  check(cudaMemsetAsync(sp.cnt.p, 0, 2 * sizeof(unsigned), s), "memset");
   // Row heads, 16-bit ids, margin CTA partition.
   const uint64_t nwords = (nnz + 256) / 32 + 2;
   ds.rbm.alloc(nwords);
   ds.rbm.zero(s);
-  {
-    DBuf<uint32_t> nonempty;
-    nonempty.alloc(std::max<uint64_t>(1, n));
-    prof_begin(c, "sparse_prep_kernel");
-    row_heads_kernel<<<grid_1d(n), 256, 0, s>>>(ds.rowptr.p, static_cast<uint32_t>(n), ds.rbm.p,
-                                                nonempty.p, cnt.p);
-    launched(c, "sparse_prep_kernel");
-    unsigned empty = 0;
-    d2h_sync(&empty, cnt.p, s);
-    ds.rows_empty = empty != 0;
-    if (ds.rows_empty) compaction(c, nonempty.p, n, ds.row_of_ord, tmp);
-  }
-  word_prefix(c, ds.rbm.p, nwords, ds.rbm_pre, tmp);
+  sp.a.alloc(std::max<uint64_t>(1, n));  // non-empty row flags
+  prof_begin(c, "sparse_prep_kernel");
+  row_heads_kernel<<<grid_1d(n), 256, 0, s>>>(ds.rowptr.p, static_cast<uint32_t>(n), ds.rbm.p, sp.a.p, sp.cnt.p);
+  launched(c, "sparse_prep_kernel");
+  word_prefix(c, ds.rbm.p, nwords, ds.rbm_pre, sp.tmp, sp.b);
   if (d <= 65536) {
     ds.cidx16.alloc(nnz + 1024);
-    ds.cidx16.zero(s);
+    check(cudaMemsetAsync(ds.cidx16.p + nnz, 0, 1024 * sizeof(uint16_t), s), "memset");
     prof_begin(c, "sparse_prep_kernel");
     narrow_u16_kernel<<<c.num_sms * 8, 256, 0, s>>>(ds.idx.p, nnz, ds.cidx16.p);
     launched(c, "sparse_prep_kernel");
@@ -697,78 +682,80 @@ void sparse_prep(Dataset& ds) {
   const uint64_t nseg = uint64_t(ds.csc_nblk) * d;
   ds.cval.alloc(nnz + 1024);
   ds.crow.alloc(nnz + 1024);
-  ds.cval.zero(s);
-  ds.crow.zero(s);
+  check(cudaMemsetAsync(ds.cval.p + nnz, 0, 1024 * sizeof(float), s), "memset");
+  check(cudaMemsetAsync(ds.crow.p + nnz, 0, 1024 * sizeof(uint16_t), s), "memset");
   ds.segptr.alloc(nseg + 1);
   ds.cbm.alloc(nwords);
   ds.cbm.zero(s);
   if (nnz > 0) {
-    DBuf<uint32_t> k_in, k_out;
-    DBuf<uint64_t> p_in, p_out;
-    k_in.alloc(nnz);
-    k_out.alloc(nnz);
-    p_in.alloc(nnz);
-    p_out.alloc(nnz);
+    sp.k_in.alloc(nnz);
+    sp.k_out.alloc(nnz);
+    sp.p_in.alloc(nnz);
+    sp.p_out.alloc(nnz);
     prof_begin(c, "sparse_prep_kernel");
     csc_keys_kernel<<<c.num_sms * 8, 256, 0, s>>>(ds.val.p, ds.idx.p, ds.rowptr.p, static_cast<uint32_t>(n),
-                                                  static_cast<uint32_t>(d), ds.csc_rb, k_in.p, p_in.p);
+                                                  static_cast<uint32_t>(d), ds.csc_rb, sp.k_in.p, sp.p_in.p);
     launched(c, "sparse_prep_kernel");
     int end_bit = 1;
     while (end_bit < 32 && (uint64_t(1) << end_bit) < nseg) ++end_bit;
     size_t bytes = 0;
-    check(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k_in.p, k_out.p, p_in.p, p_out.p,
+    check(cub::DeviceRadixSort::SortPairs(nullptr, bytes, sp.k_in.p, sp.k_out.p, sp.p_in.p, sp.p_out.p,
                                           static_cast<int64_t>(nnz), 0, end_bit, s),
           "cub sort size");
-    tmp.alloc(bytes);
-    check(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k_in.p, k_out.p, p_in.p, p_out.p,
+    sp.tmp.alloc(bytes);
+    bytes = sp.tmp.n;
+    check(cub::DeviceRadixSort::SortPairs(sp.tmp.p, bytes, sp.k_in.p, sp.k_out.p, sp.p_in.p, sp.p_out.p,
                                           static_cast<int64_t>(nnz), 0, end_bit, s),
           "cub sort");
     prof_begin(c, "sparse_prep_kernel");
-    csc_unpack_kernel<<<c.num_sms * 8, 256, 0, s>>>(k_out.p, p_out.p, static_cast<uint32_t>(nnz),
+    csc_unpack_kernel<<<c.num_sms * 8, 256, 0, s>>>(sp.k_out.p, sp.p_out.p, static_cast<uint32_t>(nnz),
                                                     static_cast<uint32_t>(nseg), ds.cval.p, ds.crow.p,
                                                     ds.cbm.p, ds.segptr.p);
     launched(c, "sparse_prep_kernel");
-    check(cudaStreamSynchronize(s), "prep sync");
   } else {
     ds.segptr.zero(s);
   }
-  word_prefix(c, ds.cbm.p, nwords, ds.cbm_pre, tmp);
-  {
-    DBuf<uint32_t> flag;
-    flag.alloc(std::max<uint64_t>(1, nseg));
-    prof_begin(c, "sparse_prep_kernel");
-    seg_nonempty_kernel<<<grid_1d(nseg), 256, 0, s>>>(ds.segptr.p, static_cast<uint32_t>(nseg), flag.p,
-                                                       cnt.p + 1);
-    launched(c, "sparse_prep_kernel");
-    unsigned empty = 0;
-    d2h_sync(&empty, cnt.p + 1, s);
-    ds.segs_empty = empty != 0;
-    if (ds.segs_empty) compaction(c, flag.p, nseg, ds.seg_of_ord, tmp);
-  }
+  word_prefix(c, ds.cbm.p, nwords, ds.cbm_pre, sp.tmp, sp.b);
+  sp.c.alloc(std::max<uint64_t>(1, nseg));  // non-empty segment flags
+  prof_begin(c, "sparse_prep_kernel");
+  seg_nonempty_kernel<<<grid_1d(nseg), 256, 0, s>>>(ds.segptr.p, static_cast<uint32_t>(nseg), sp.c.p,
+                                                     sp.cnt.p + 1);
+  launched(c, "sparse_prep_kernel");
   {  // nnz-balanced column ranges, shared by every row block
-    DBuf<uint32_t> colc, incl;
-    colc.alloc(std::max<uint64_t>(1, d));
-    incl.alloc(std::max<uint64_t>(1, d));
+    sp.k_in.alloc(std::max<uint64_t>(1, d));  // column counts (the sort keys are consumed)
+    sp.b.alloc(std::max<uint64_t>(nwords + 1, d));
     prof_begin(c, "sparse_prep_kernel");
-    col_count_kernel<<<grid_1d(d), 256, 0, s>>>(ds.segptr.p, static_cast<uint32_t>(d), ds.csc_nblk, colc.p);
+    col_count_kernel<<<grid_1d(d), 256, 0, s>>>(ds.segptr.p, static_cast<uint32_t>(d), ds.csc_nblk, sp.k_in.p);
     launched(c, "sparse_prep_kernel");
     size_t bytes = 0;
-    check(cub::DeviceScan::InclusiveSum(nullptr, bytes, colc.p, incl.p, static_cast<int64_t>(d), s),
+    check(cub::DeviceScan::InclusiveSum(nullptr, bytes, sp.k_in.p, sp.b.p, static_cast<int64_t>(d), s),
           "cub scan size");
-    tmp.alloc(bytes);
-    check(cub::DeviceScan::InclusiveSum(tmp.p, bytes, colc.p, incl.p, static_cast<int64_t>(d), s), "cub scan");
+    sp.tmp.alloc(bytes);
+    bytes = sp.tmp.n;
+    check(cub::DeviceScan::InclusiveSum(sp.tmp.p, bytes, sp.k_in.p, sp.b.p, static_cast<int64_t>(d), s),
+          "cub scan");
     ds.cta_col.alloc(ds.csc_cpb + 1);
     prof_begin(c, "sparse_prep_kernel");
-    cta_col_kernel<<<grid_1d(ds.csc_cpb + 1), 256, 0, s>>>(incl.p, static_cast<uint32_t>(d), ds.csc_cpb, nnz,
+    cta_col_kernel<<<grid_1d(ds.csc_cpb + 1), 256, 0, s>>>(sp.b.p, static_cast<uint32_t>(d), ds.csc_cpb, nnz,
                                                             ds.cta_col.p);
     launched(c, "sparse_prep_kernel");
-    check(cudaStreamSynchronize(s), "prep sync");
   }
-  ds.coef.alloc(n + 8);
-  ds.coef.zero(s);
-  ds.sparse_tickets.alloc(ds.csc_cpb);
-  ds.sparse_tickets.zero(s);
+  // One host read-back: are there empty rows / segments (ordinal maps needed)?
+  unsigned empty[2] = {0, 0};
+  check(cudaMemcpyAsync(empty, sp.cnt.p, sizeof(empty), cudaMemcpyDeviceToHost, s), "D2H");
   check(cudaStreamSynchronize(s), "prep sync");
+  ds.rows_empty = empty[0] != 0;
+  ds.segs_empty = empty[1] != 0;
+  if (ds.rows_empty) compaction(c, sp.a.p, n, ds.row_of_ord, sp.tmp, sp.b);
+  if (ds.segs_empty) compaction(c, sp.c.p, nseg, ds.seg_of_ord, sp.tmp, sp.b);
+  if (ds.coef.n < n + 8) {
+    ds.coef.alloc(n + 8);
+    ds.coef.zero(s);
+  }
+  if (ds.sparse_tickets.n < ds.csc_cpb) {
+    ds.sparse_tickets.alloc(ds.csc_cpb);
+    ds.sparse_tickets.zero(s);
+  }
   ds.sparse_ready = true;
 }
 

@@ -65,9 +65,26 @@ def attach(dev: Device, group=None) -> None:
         return
 
     def hook(ptr, count, dtype, stream):
-        sum_in_place(device_view(ptr, count, dtype), group)
+        # The collective runs on the engine's stream, whatever torch's current
+        # stream is, so it is ordered with the engine's kernels.
+        with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+            sum_in_place(device_view(ptr, count, dtype), group)
 
     dev.set_allreduce(hook)
+
+
+def attach_nccl(dev: Device, group=None) -> None:
+    """Gives the engine its own NCCL communicator over the ranks of the
+    initialised process group: rank 0 creates the id (sgdb_nccl_get_unique_id),
+    the process group broadcasts it, every rank calls sgdb_ctx_init_nccl. The
+    engine then issues ncclAllReduce on its stream itself (no Python hop per
+    step; multi-rank mini-batch epochs stay CUDA-graph-replayed)."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [Device.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    dev.init_nccl(world, rank, obj[0])
 
 
 def average_ranks(dev: Device, model: DeviceModel, world: int) -> None:
