@@ -854,10 +854,6 @@ sgdb_status sgdb_hogwild_segment(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m,
     require(a.lanes == 1 || a.lanes == 2 || a.lanes == 4 || a.lanes == 8 || a.lanes == 16 ||
                 a.lanes == 32,
             "lanes_per_worker must be 1, 2, 4, 8, 16 or 32");
-    if (const char* e = std::getenv("SGDB_HOGWILD_MODE")) a.model_mode = std::atoi(e);
-    if (const char* e = std::getenv("SGDB_HOGWILD_REFRESH"))
-      a.refresh = static_cast<uint32_t>(std::max(1, std::atoi(e)));
-    if (const char* e = std::getenv("SGDB_HOGWILD_SPREAD")) a.spread = std::atoi(e) != 0;
     a.seg = seg;
     a.nseg = nseg;
     a.alpha_f64 = alpha;

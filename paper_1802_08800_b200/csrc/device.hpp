@@ -284,9 +284,6 @@ struct HogwildArgs {
   uint64_t k = 0, workers = 1, group_size = 32;
   bool offsets = true;
   int lanes = 0;         // resolved lanes per worker
-  int model_mode = 1;    // kernel scope: 0 plain ld/st, 1 red.add, 2 smem mirror + red.add
-  uint32_t refresh = 4;  // mirror: refresh a read from L2 on every refresh-th example id
-  bool spread = true;    // kernel scope: 256 B-strided model copy during the epoch
   uint32_t seg = 0, nseg = 1;  // run list positions [total*seg/nseg, total*(seg+1)/nseg)
   double alpha_f64 = 0.0;      // exact-fp64 mode step size
 };

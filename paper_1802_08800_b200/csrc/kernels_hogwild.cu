@@ -28,10 +28,10 @@ constexpr int kKindCsr = 1;       // CSR rows
 constexpr int kKindDenseCol = 2;  // column-major dense (stride n)
 constexpr int kKindPaddedCol = 3; // slot-major padded (stride n, sentinel d)
 
-constexpr int kScopeShared = 0;   // one model in global memory (kernel scope)
 constexpr int kScopeGlobalRep = 1;// replicas in global memory, replica = worker / gs
 constexpr int kScopeSharedAtomic = 2;      // one model, red.global.add, slice-spread layout
 constexpr int kScopeSharedAtomicFlat = 3;  // one model, red.global.add, contiguous layout
+constexpr int kScopeGlobalRepAtomic = 4;   // replicas in global memory, red.global.add
 constexpr uint32_t kSpread = 64;           // floats between coordinates (256 B)
 
 struct HogParams {
@@ -50,7 +50,6 @@ struct HogParams {
   float* model;
   uint64_t ld;
   float alpha;
-  uint32_t refresh;  // mirror kernel: refresh reads from L2 every `refresh` examples
   uint32_t ms;       // kernel scope: float stride between model coordinates in global
   uint32_t seg, nseg;  // this launch runs list positions [total*seg/nseg, total*(seg+1)/nseg)
 };
@@ -97,34 +96,6 @@ struct SmemModel {  // block-scope replica in shared memory, plain RMW
   __device__ float load(uint64_t j) const { return m[j]; }
   __device__ void add(uint64_t j, float delta) const { m[j] = m[j] + delta; }
 };
-// Kernel scope with a per-CTA shared-memory mirror of the shared model:
-// updates go to the global model (red.add) AND the mirror (smem atomic), so
-// a CTA sees its own updates at once and other CTAs' updates whenever a read
-// refreshes the coordinate from L2 (one example in `refresh`). Staleness is
-// bounded; with one worker every read sees every update (sequential Alg. 3).
-struct MirrorModel {
-  float* g;
-  uint32_t ms;
-  float* sm;
-  uint32_t period;
-  bool refresh;
-  __device__ MirrorModel at(uint64_t e) const {
-    return MirrorModel{g, ms, sm, period, period <= 1 || (e % period) == 0};
-  }
-  __device__ float load(uint64_t j) const {
-    if (refresh) {
-      const float v = ld_model(g + j * ms);
-      sm[j] = v;
-      return v;
-    }
-    return *(volatile float*)(sm + j);
-  }
-  __device__ void add(uint64_t j, float delta) const {
-    atomicAdd(g + j * ms, delta);
-    atomicAdd(sm + j, delta);
-  }
-};
-
 // ---- one worker: its assign() list, a 2-stage prefetch pipeline, and the
 // per-example body of process_examples (async_engine.cpp:178-195) ----------
 
@@ -412,28 +383,13 @@ __global__ void __launch_bounds__(256) hogwild_kernel(HogParams p) {
                                                                  mask);
     } else if (SCOPE == kScopeSharedAtomicFlat) {
       run_worker<G, TASK, KIND, GlobalAtomicModel<1>, LONG>(p, GlobalAtomicModel<1>{p.model}, w, lg, mask);
-    } else {
-      run_worker<G, TASK, KIND>(
-          p,
-          GlobalModel{SCOPE == kScopeShared ? p.model : p.model + (w / p.gs) * p.ld,
-                      SCOPE == kScopeShared ? p.ms : 1u},
-          w, lg, mask);
+    } else if (SCOPE == kScopeGlobalRepAtomic) {
+      run_worker<G, TASK, KIND, GlobalAtomicModel<1>>(p, GlobalAtomicModel<1>{p.model + (w / p.gs) * p.ld},
+                                                      w, lg, mask);
+    } else {  // kScopeGlobalRep
+      run_worker<G, TASK, KIND>(p, GlobalModel{p.model + (w / p.gs) * p.ld, 1u}, w, lg, mask);
     }
   }
-}
-
-// K5 with a per-CTA shared-memory mirror of the shared model (see MirrorModel).
-template <int G, int TASK, int KIND>
-__global__ void __launch_bounds__(256) hogwild_mirror_kernel(HogParams p) {
-  extern __shared__ float mirror[];
-  for (uint64_t j = threadIdx.x; j <= p.d; j += blockDim.x) mirror[j] = ld_model(p.model + j * p.ms);
-  __syncthreads();
-  const int lg = threadIdx.x % G;
-  const unsigned mask = group_mask<G>();
-  const uint64_t hg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const uint64_t HG = ((uint64_t)gridDim.x * blockDim.x) / G;
-  for (uint64_t w = hg; w < p.T; w += HG)
-    run_worker<G, TASK, KIND>(p, MirrorModel{p.model, p.ms, mirror, p.refresh, false}, w, lg, mask);
 }
 
 // K6 (block scope): CTA r owns replica r in shared memory, loaded from the
@@ -712,7 +668,7 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
     p.gs = 1;
     p.ld = 0;
     // Slice-spread layout for models that stay L2-resident when spread.
-    const uint32_t ms = (a.spread && ds.d <= (uint64_t{1} << 17)) ? kSpread : 1u;
+    const uint32_t ms = ds.d <= (uint64_t{1} << 17) ? kSpread : 1u;
     if (ms > 1) {
       if (!(m.spread_current && m.spread_ms == ms)) {
         materialize(m);
@@ -730,44 +686,34 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
       p.model = m.w32.p;
     }
     p.ms = ms;
-    const size_t mirror_bytes = (ds.d + 1) * sizeof(float);
-    int mode = a.model_mode;
-    if (mode == 2 && mirror_bytes > 48 * 1024) mode = 1;  // mirror needs d+1 floats per CTA
-    p.refresh = a.refresh;
     // Average row of hundreds of slots (news20: 461): the batch chain of the
     // longest rows dominates, and the worker count (n / chunk) is small anyway.
     const bool long_rows = kind == kKindCsr && hogwild_long_rows(ds);
-    dispatch_lanes(G, [&]<int GL>() {
-      dispatch_kind(kind, [&]<int KD>() {
-        void (*kern)(HogParams);
-        size_t smem = 0;
-        if (mode == 2) {
-          kern = a.task == kTaskLR ? hogwild_mirror_kernel<GL, kTaskLR, KD>
-                                   : hogwild_mirror_kernel<GL, kTaskSVM, KD>;
-          smem = mirror_bytes;
-        } else if (mode == 1 && long_rows && GL == 32 && KD == kKindCsr) {
-          // Long rows: two slot batches per round trip (see process_example).
-          if (ms > 1)
-            kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomic, true>
-                                     : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomic, true>;
-          else
-            kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomicFlat, true>
-                                     : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomicFlat, true>;
-        } else if (mode == 1 && ms > 1) {
-          kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomic>
-                                   : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomic>;
-        } else if (mode == 1) {
-          kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomicFlat>
-                                   : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomicFlat>;
-        } else {
-          kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeShared>
-                                   : hogwild_kernel<GL, kTaskSVM, KD, kScopeShared>;
-        }
-        const unsigned grid = wave_grid(c, kern, smem, a.workers, GL);
-        prof_begin(c, "hogwild_kernel");
-        kern<<<grid, 256, smem, c.stream>>>(p);
+    {
+      dispatch_lanes(G, [&]<int GL>() {
+        dispatch_kind(kind, [&]<int KD>() {
+          void (*kern)(HogParams);
+          if (long_rows && GL == 32 && KD == kKindCsr) {
+            // Long rows: two slot batches per round trip (see process_example).
+            if (ms > 1)
+              kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomic, true>
+                                       : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomic, true>;
+            else
+              kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomicFlat, true>
+                                       : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomicFlat, true>;
+          } else if (ms > 1) {
+            kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomic>
+                                     : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomic>;
+          } else {
+            kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeSharedAtomicFlat>
+                                     : hogwild_kernel<GL, kTaskSVM, KD, kScopeSharedAtomicFlat>;
+          }
+          const unsigned grid = wave_grid(c, kern, 0, a.workers, GL);
+          prof_begin(c, "hogwild_kernel");
+          kern<<<grid, 256, 0, c.stream>>>(p);
+        });
       });
-    });
+    }
     launched(c, "hogwild_kernel");
     if (ms > 1) {
       // The spread copy stays authoritative until someone reads the dense
@@ -794,7 +740,12 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
   p.ms = 1;
   p.model = m.replicas.p;
   const size_t rep_bytes = round_up16((ds.d + 1) * sizeof(float));
-  const bool smem_ok = a.replication == SGDB_REPL_BLOCK && rep_bytes + 1024 <= c.max_smem_optin;
+  // Shared-memory replicas (K6) when every SM gets one: a CTA per replica.
+  // Fewer replicas than SMs (large groups, R sized to the data) keep them in
+  // global memory (L2) and let every resident warp work (K6g, red.add
+  // updates within a replica).
+  const bool smem_ok = a.replication == SGDB_REPL_BLOCK && rep_bytes + 1024 <= c.max_smem_optin &&
+                       R >= static_cast<uint64_t>(c.num_sms);
   if (smem_ok) {
     uint64_t threads = std::min<uint64_t>(1024, gs * G);
     threads = std::max<uint64_t>(32, (threads + 31) & ~uint64_t(31));
@@ -819,10 +770,16 @@ void hogwild_epoch(Dataset& ds, Model& m, const HogwildArgs& a) {
     prof_begin(c, "replicas_fill_kernel");
     replicas_fill_kernel<<<fill_grid, 256, 0, c.stream>>>(m.replicas.p, R, ld, ds.d, m.w32.p);
     launched(c, "replicas_fill_kernel");
+    const bool shared_rep = gs > 1;  // several workers race on a replica
     dispatch_lanes(G, [&]<int GL>() {
       dispatch_kind(kind, [&]<int KD>() {
-        auto kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeGlobalRep>
-                                      : hogwild_kernel<GL, kTaskSVM, KD, kScopeGlobalRep>;
+        void (*kern)(HogParams);
+        if (shared_rep)
+          kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeGlobalRepAtomic>
+                                   : hogwild_kernel<GL, kTaskSVM, KD, kScopeGlobalRepAtomic>;
+        else
+          kern = a.task == kTaskLR ? hogwild_kernel<GL, kTaskLR, KD, kScopeGlobalRep>
+                                   : hogwild_kernel<GL, kTaskSVM, KD, kScopeGlobalRep>;
         const unsigned grid = wave_grid(c, kern, 0, a.workers, GL);
         prof_begin(c, "hogwild_kernel(replicas)");
         kern<<<grid, 256, 0, c.stream>>>(p);

@@ -66,8 +66,11 @@ def attach(dev: Device, group=None) -> None:
 
     def hook(ptr, count, dtype, stream):
         # The collective runs on the engine's stream, whatever torch's current
-        # stream is, so it is ordered with the engine's kernels.
-        with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+        # stream is, so it is ordered with the engine's kernels (handles 0 / 1 /
+        # 2 are the legacy / per-thread default streams).
+        s = (torch.cuda.default_stream() if stream in (0, 1, 2)
+             else torch.cuda.ExternalStream(stream))
+        with torch.cuda.stream(s):
             sum_in_place(device_view(ptr, count, dtype), group)
 
     dev.set_allreduce(hook)

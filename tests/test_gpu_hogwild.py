@@ -230,11 +230,13 @@ def test_acceptance5_eight_workers(sgdb, acceptance5, plan_text, lanes):
 
 
 @pytest.mark.parametrize("workers,gs,lanes", [(4096, 2048, 0), (4096, 2048, 32), (64, 32, 0),
-                                              (8, 4, 0)])
+                                              (8, 4, 0), (4736, 32, 0)])
 def test_block_scope_loss_curve_tracks_oracle(sgdb, dev, orc, workers, gs, lanes):
     """Block scope with racing workers per replica (async_engine.cpp:293-331):
-    the per-epoch loss curve stays within 2% of the serialized-worker oracle
-    (one legal Hogwild interleaving) on acceptance 5's fixture."""
+    the per-epoch loss curve stays within 2% above the serialized-worker oracle
+    (one legal Hogwild interleaving) on acceptance 5's fixture. R = workers /
+    gs replicas: 148 (one per SM, shared-memory replicas, K6) or fewer
+    (replicas in L2 shared by all resident warps, K6g)."""
     S = sgdb
     ds = S.fixtures.sparse_classification(20000, 10000, 50.0, 20250810).rounded_f32()
     plan = S.parse_plan("row-ch:block:0")
@@ -242,7 +244,9 @@ def test_block_scope_loss_curve_tracks_oracle(sgdb, dev, orc, workers, gs, lanes
     r = S.hogwild.train(S.Task.SVM, ds, _inc(S, S.Task.SVM, 0.1, 5, 0.97), plan, 0, device=dev)
     _, ol, _ = orc.hogwild_serial(ds, 1, 0.1, 5, 0, 1, 0, workers, group_size=gs, decay=0.97)
     for e in range(5):
-        assert rel(r.trace.epochs[e].loss, ol[e]) <= 0.02, (e, r.trace.losses(), list(ol))
+        # red.add replicas lose no updates, so racing runs may converge faster
+        # than the serialized interleaving: the bound is one-sided.
+        assert r.trace.epochs[e].loss <= 1.02 * ol[e], (e, r.trace.losses(), list(ol))
 
 
 @pytest.mark.parametrize("plan_text,workers,gs", [("row-ch:kernel:0", 4096, 32),
