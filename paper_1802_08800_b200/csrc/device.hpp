@@ -144,6 +144,7 @@ struct Dataset {
   DBuf<uint32_t> segptr, cbm, cbm_pre, seg_of_ord, cta_col;
   bool segs_empty = false;
   DBuf<unsigned> sparse_tickets;
+  unsigned sparse_gen = 0;  // K3s launches since the tickets were zeroed
   // sparse_prep's scratch, kept so a rebuild after every refresh (bench
   // e2e) neither allocates nor frees (cudaFree synchronises the device).
   struct {

@@ -31,6 +31,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 
@@ -51,6 +53,21 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
+}
+
+// Eight consecutive fp32 values in one 256-bit load (LDG.E.256, sm_100+):
+// the warp's 32 lanes read 1 KB of contiguous values in one instruction; two
+// 128-bit loads per lane would each touch every line of the 1 KB half-used.
+__device__ __forceinline__ void ldg256(const float* p, float4& a, float4& b) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+               : "l"(p));
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // Number of heads in slots [0, P): word prefix + partial word.
@@ -293,8 +310,7 @@ __global__ void __launch_bounds__(kNT, 1)
       S0, S1, bm, bpre,
       [&](uint32_t s) {
         Win q;
-        q.v0 = __ldg(reinterpret_cast<const float4*>(val + s));
-        q.v1 = __ldg(reinterpret_cast<const float4*>(val + s + 4));
+        ldg256(val + s, q.v0, q.v1);
         if constexpr (I16) {
           q.j = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(idx) + s));
         } else {
@@ -361,15 +377,20 @@ struct ApplyArgs {
 // K3s: CTA (row block b, column range k) bulk-copies the block's coefficient
 // slice into SMEM, streams the block's segments of columns
 // [cta_col[k], cta_col[k+1]) against it, writing fp32 per-(block, column)
-// sums; the last CTA of column range k sums them over the blocks (fixed block
-// order, fp64) and applies w -= a g.
+// sums; then g_j = sum over blocks (fixed block order, fp64) and w -= a g.
+// The apply is spread over the nblk CTAs of the column range once all of
+// them have arrived (coop: the launch is cooperative, so every CTA is
+// resident and the arrival wait cannot deadlock); otherwise the last CTA to
+// arrive applies the whole range. Arrival tickets count up by nblk per launch
+// (gen = launch number), so they are never reset.
 __global__ void __launch_bounds__(kNT, 1)
     k3s_grad_kernel(const float* __restrict__ cval, const uint16_t* __restrict__ crow,
                     const uint32_t* __restrict__ bm, const uint32_t* __restrict__ bpre,
                     const uint32_t* __restrict__ segptr, const uint32_t* __restrict__ cta_col,
                     uint32_t cpb, uint32_t nblk, uint32_t d, uint32_t rb, uint32_t n,
                     const float* __restrict__ coef, const uint32_t* __restrict__ seg_of_ord,
-                    float* __restrict__ part, unsigned* __restrict__ tickets, ApplyArgs aa) {
+                    float* __restrict__ part, unsigned* __restrict__ tickets, ApplyArgs aa,
+                    unsigned gen, int coop) {
   extern __shared__ __align__(16) float cs[];
   __shared__ CtaScratch sc;
   __shared__ uint64_t bar;
@@ -395,8 +416,7 @@ __global__ void __launch_bounds__(kNT, 1)
       S0, S1, bm, bpre,
       [&](uint32_t s) {
         WinC q;
-        q.v0 = __ldg(reinterpret_cast<const float4*>(cval + s));
-        q.v1 = __ldg(reinterpret_cast<const float4*>(cval + s + 4));
+        ldg256(cval + s, q.v0, q.v1);
         q.r = __ldg(reinterpret_cast<const uint4*>(crow + s));
         return q;
       },
@@ -417,18 +437,26 @@ __global__ void __launch_bounds__(kNT, 1)
       sc);
   if (!ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
   __syncthreads();
+  const unsigned target = gen * nblk;
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned t = atomicAdd(tickets + k, 1u);
-    sc.last = t == nblk - 1;
-    if (sc.last) tickets[k] = 0u;  // re-armed for the next launch
+    const unsigned t = atomicAdd(tickets + k, 1u) + 1u;
+    sc.last = t == target;
+    if (coop)
+      while (ld_acquire_gpu(tickets + k) < target) __nanosleep(32);
   }
   __syncthreads();
-  if (!sc.last) return;
+  uint32_t a0 = j0, a1 = j1;  // the columns this CTA applies
+  if (coop) {
+    a0 = j0 + static_cast<uint32_t>(uint64_t(j1 - j0) * b / nblk);
+    a1 = j0 + static_cast<uint32_t>(uint64_t(j1 - j0) * (b + 1) / nblk);
+  } else if (!sc.last) {
+    return;
+  }
   __threadfence();
   double nrm = 0.0;
   int bad = 0;
-  for (uint32_t j = j0 + threadIdx.x; j < j1; j += kNT) {
+  for (uint32_t j = a0 + threadIdx.x; j < a1; j += kNT) {
     // Block order; 8 loads in flight per thread (only d/cpb threads work here).
     double g = 0.0;
     uint32_t bb = 0;
@@ -632,10 +660,13 @@ void compaction(Ctx& c, const uint32_t* flag, uint64_t count, DBuf<uint32_t>& ma
 // Row-block geometry: blocks of at most 49,152 rows (u16 ids, <= 192 KB
 // slice), and as many CTAs (blocks x column ranges) as SMs, one per SM.
 void choose_blocks(const Ctx& c, uint64_t n, uint32_t& rb, uint32_t& nblk, uint32_t& cpb) {
-  // Fewest row blocks: the apply tail reads nblk partials per coordinate.
+  // The fewest blocks of at most 49,152 rows (16-bit ids, <= 192 KB slice):
+  // more blocks shrink the staged slices but add nblk * d partial sums to the
+  // apply; measured on rcv1 (14 vs 37 blocks: 139-142 vs 141-142 us) and
+  // real-sim / w8a (2 vs 16 / 126 blocks: 37 vs 41 us, 27 vs 35 us).
   const uint64_t nb = std::max<uint64_t>(1, (n + kMaxRowBlock - 1) / kMaxRowBlock);
   const uint64_t sms = static_cast<uint64_t>(std::max(1, c.num_sms));
-  // rb % 8 == 0 keeps every coefficient slice 32-byte aligned (bulk copies, float4 groups).
+  // rb % 8 == 0 keeps every coefficient slice 32-byte aligned (bulk copies).
   rb = static_cast<uint32_t>(std::max<uint64_t>(8, ((n + nb - 1) / nb + 7) & ~uint64_t(7)));
   nblk = static_cast<uint32_t>(std::max<uint64_t>(1, (n + rb - 1) / rb));
   cpb = static_cast<uint32_t>(std::max<uint64_t>(1, sms / nblk));
@@ -752,10 +783,9 @@ void sparse_prep(Dataset& ds) {
     ds.coef.alloc(n + 8);
     ds.coef.zero(s);
   }
-  if (ds.sparse_tickets.n < ds.csc_cpb) {
-    ds.sparse_tickets.alloc(ds.csc_cpb);
-    ds.sparse_tickets.zero(s);
-  }
+  ds.sparse_tickets.alloc(ds.csc_cpb);
+  ds.sparse_tickets.zero(s);  // arrival counts restart with the launch numbers
+  ds.sparse_gen = 0;
   ds.sparse_ready = true;
 }
 
@@ -793,11 +823,33 @@ void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a) {
     auto kern = k3s_grad_kernel;
     set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(k3s)");
     ApplyArgs aa{a.alpha, a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p, m.finite.p, m.scal.p};
+    const unsigned grid = ds.csc_nblk * ds.csc_cpb;
+    const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kNT, smem);
+    int coop = static_cast<uint64_t>(grid) <= static_cast<uint64_t>(per_sm) * c.num_sms ? 1 : 0;
+    unsigned gen = ++ds.sparse_gen;
     prof_begin(c, "k3s_grad_kernel");
-    kern<<<ds.csc_nblk * ds.csc_cpb, kNT, smem, c.stream>>>(
-        ds.cval.p, ds.crow.p, ds.cbm.p, ds.cbm_pre.p, ds.segptr.p, ds.cta_col.p, ds.csc_cpb, ds.csc_nblk, d,
-        ds.csc_rb, static_cast<uint32_t>(ds.n), ds.coef.p,
-        ds.segs_empty ? ds.seg_of_ord.p : nullptr, m.part32.p, ds.sparse_tickets.p, aa);
+    const float* cval = ds.cval.p;
+    const uint16_t* crow = ds.crow.p;
+    const uint32_t* cbm = ds.cbm.p;
+    const uint32_t* cbm_pre = ds.cbm_pre.p;
+    const uint32_t* segptr = ds.segptr.p;
+    const uint32_t* cta_col = ds.cta_col.p;
+    uint32_t cpb = ds.csc_cpb, nblk = ds.csc_nblk, rb = ds.csc_rb, n = static_cast<uint32_t>(ds.n);
+    uint32_t dd = d;
+    const float* coef = ds.coef.p;
+    const uint32_t* seg_of_ord = ds.segs_empty ? ds.seg_of_ord.p : nullptr;
+    float* part = m.part32.p;
+    unsigned* tickets = ds.sparse_tickets.p;
+    if (coop) {
+      void* args[] = {&cval, &crow, &cbm, &cbm_pre, &segptr, &cta_col, &cpb, &nblk, &dd, &rb, &n,
+                      &coef, &seg_of_ord, &part, &tickets, &aa, &gen, &coop};
+      check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kNT), args, smem,
+                                        c.stream),
+            "cudaLaunchCooperativeKernel(k3s)");
+    } else {
+      kern<<<grid, kNT, smem, c.stream>>>(cval, crow, cbm, cbm_pre, segptr, cta_col, cpb, nblk, dd, rb, n, coef,
+                                          seg_of_ord, part, tickets, aa, gen, coop);
+    }
     launched(c, "k3s_grad_kernel");
   }
 }
