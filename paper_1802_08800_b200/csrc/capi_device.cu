@@ -680,7 +680,12 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
       // Chunk plan of this epoch's order for the sparse steps (outside any
       // captured graph: it may allocate; the graph re-reads it every replay).
       if (ds->kind == Kind::Csr) csr_batch_plan(*ds, ds->order.p, ng, batch_b);
-      auto run_steps = [&](const StepArgs& sa) {
+      // Sparse steps without a collective update the fp64 master directly;
+      // the fp32 copy is refreshed once at the end of the epoch.
+      const bool direct = !hook && ds->kind == Kind::Csr;
+      auto run_steps = [&](const StepArgs& sa0) {
+        StepArgs sa = sa0;
+        sa.direct = direct;
         for (uint64_t lo = 0; lo < ng; lo += batch_b) {
           const uint64_t nb = std::min(batch_b, ng - lo);
           const uint32_t* ids = ds->order.p + lo;
@@ -691,6 +696,7 @@ sgdb_status sgdb_sync_epoch(sgdb_ctx* ctx, sgdb_dataset* ds, sgdb_model* m, int3
             apply_update(*m, alpha, false, sa.alpha_dev);
           }
         }
+        if (direct) sync_w32_from_w64(*m);
       };
       if (!hook && ds->kind == Kind::Dense && ng > batch_b &&
           dense_epoch(*ds, *m, task, alpha, batch_b)) {

@@ -86,6 +86,16 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 __device__ __forceinline__ float ld_model(const float* p) { return __ldcg(p); }
 __device__ __forceinline__ void st_model(float* p, float v) { __stcg(p, v); }
 
+// ---- programmatic dependent launch ---------------------------------------------
+// A kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization
+// may start while its predecessor drains: it issues the loads that do not
+// depend on the predecessor first, then waits here (griddepcontrol.wait:
+// the predecessor grid has completed and its writes are visible).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- mbarrier + cp.async.bulk (1-D TMA, no tensor map) ------------------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -243,6 +243,9 @@ struct StepArgs {
   const double* alpha_dev = nullptr;  // device step size (graph-captured epochs)
   bool apply = true;      // fuse w -= alpha*g (else g64 holds the gradient)
   bool want_norm = false; // accumulate ||g||^2 into model.scal[0]
+  // Sparse mini-batch steps update the fp64 master directly (no gradient
+  // buffer, no apply launch); the epoch ends with sync_w32_from_w64.
+  bool direct = false;
 };
 
 // Dense, all local rows: one full-batch gradient (deterministic).
@@ -273,6 +276,8 @@ void widen_u16(Ctx& c, const uint16_t* src, uint32_t* dst, uint64_t n);
 void loss_launch(Dataset& ds, Model& m, int task);
 // w64 = (double) w32[0..d)
 void sync_w64_from_w32(Model& m);
+// w32 = (float) w64[0..d) (after directly-updated sparse mini-batch steps)
+void sync_w32_from_w64(Model& m);
 // Weighted mean of models (w64) -> out; refresh copies it back to each input.
 void average_models(Ctx& c, Model* const* models, uint64_t count, const double* weights,
                     Model& out, bool refresh);

@@ -622,20 +622,25 @@ __global__ void mb_fill_kernel(const uint32_t* __restrict__ ids, uint64_t count,
   }
 }
 
-template <int G, int U>
+// W64: the model is read from the fp64 master, rounded to fp32 at the load
+// (the value w32 would hold), for epochs whose steps update w64 directly.
+template <int G, int U, bool W64>
 __global__ void __launch_bounds__(256) mb_margin_kernel(
     const float* __restrict__ val, const uint32_t* __restrict__ idx,
     const uint32_t* __restrict__ rowptr, const uint32_t* __restrict__ ids,
     const uint32_t* __restrict__ off, const uint4* __restrict__ meta, uint64_t cap, uint64_t lo,
-    uint64_t hi, uint64_t row_base, const float* __restrict__ w32, float* __restrict__ zpart,
-    const int* finite, int check_finite) {
-  if (check_finite && *finite == 0) return;
+    uint64_t hi, uint64_t row_base, const float* __restrict__ w32, const double* __restrict__ w64,
+    float* __restrict__ zpart, const int* finite, int check_finite) {
+  // PDL: the chunk table and the slots are fixed for the epoch, so they load
+  // while the previous step's update drains; the model is read after the wait.
+  pdl_launch_dependents();
   constexpr int RW = 32 / G;
   const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
   const uint32_t c0 = __ldg(off + lo), c1 = __ldg(off + hi);
   const bool direct = c1 <= cap;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  bool waited = false;
   for (uint64_t base = c0 + gw * RW; base < c1; base += tw * RW) {
     const uint64_t q = base + grp;
     const bool valid = q < c1;
@@ -654,23 +659,36 @@ __global__ void __launch_bounds__(256) mb_margin_kernel(
       jv[u] = s < e ? __ldg(idx + s) : 0u;
       xv[u] = s < e ? __ldg(val + s) : 0.f;
     }
+    if (!waited) {
+      pdl_wait();
+      waited = true;
+      if (check_finite && *finite == 0) return;
+    }
     float z = 0.f;
 #pragma unroll
-    for (int u = 0; u < U; ++u) z = fmaf(xv[u], b + lg + u * G < e ? __ldg(w32 + jv[u]) : 0.f, z);
+    for (int u = 0; u < U; ++u) {
+      const bool ok = b + lg + u * G < e;
+      const float wv = W64 ? (ok ? static_cast<float>(w64[jv[u]]) : 0.f) : (ok ? w32[jv[u]] : 0.f);
+      z = fmaf(xv[u], wv, z);
+    }
     z = group_sum<G>(z);
     if (valid && lg == 0) zpart[q - c0] = z;
   }
 }
 
-template <int G, int U, int TASK>
+// DIRECT: each step's update goes straight into the fp64 master
+// (w64 -= alpha * c * x with red.add.f64; the step size from alpha_dev when
+// set) and the finite flag follows the products, so no gradient buffer and no
+// apply launch are needed; otherwise c * x is accumulated into g64.
+template <int G, int U, int TASK, bool DIRECT>
 __global__ void __launch_bounds__(256) mb_scatter_kernel(
     const float* __restrict__ val, const uint32_t* __restrict__ idx,
     const uint32_t* __restrict__ rowptr, const float* __restrict__ y,
     const uint32_t* __restrict__ ids, const uint32_t* __restrict__ off,
     const uint4* __restrict__ meta, uint64_t cap, uint64_t lo, uint64_t hi, uint64_t row_base,
-    const float* __restrict__ zpart, double* g64, const int* finite, int check_finite,
-    int prefetch_next, uint64_t count) {
-  if (check_finite && *finite == 0) return;
+    const float* __restrict__ zpart, double* g64, int* finite, int check_finite,
+    int prefetch_next, uint64_t count, double alpha_in, const double* alpha_dev) {
+  pdl_launch_dependents();
   constexpr int RW = 32 / G;
   const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
   const uint32_t c0 = __ldg(off + lo), c1 = __ldg(off + hi);
@@ -678,6 +696,7 @@ __global__ void __launch_bounds__(256) mb_scatter_kernel(
   const uint64_t total = prefetch_next ? __ldg(off + count) : 0;  // chunks of the whole plan
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t tw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  bool waited = false;
   for (uint64_t q = c0 + gw * RW + grp; q < c1; q += tw * RW) {  // no shuffles: per group
     const ChunkRef r = chunk_ref<G, U>(meta, cap, off, ids, rowptr, row_base, lo, hi,
                                        static_cast<uint32_t>(q), direct);
@@ -690,13 +709,31 @@ __global__ void __launch_bounds__(256) mb_scatter_kernel(
       xv[u] = s < r.e ? __ldg(val + s) : 0.f;
     }
     const uint32_t z0 = __ldg(off + r.p) - c0, z1 = __ldg(off + r.p + 1) - c0;
+    if (!waited) {  // the chunk margins (and the zeroed gradient) come from the predecessors
+      pdl_wait();
+      waited = true;
+      if (check_finite && *finite == 0) return;
+    }
     float z = 0.f;
-    for (uint32_t k = z0; k < z1; ++k) z += __ldg(zpart + k);  // chunk order
+    for (uint32_t k = z0; k < z1; ++k) z += __ldcg(zpart + k);  // chunk order
     const float c = coef_f<TASK>(z, __ldg(y + r.row));
     if (c != 0.f) {
+      if (DIRECT) {
+        const double alpha = alpha_dev ? *alpha_dev : alpha_in;
+        bool bad = false;
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (r.b + lg + u * G < r.e) atomicAdd(&g64[jv[u]], static_cast<double>(c * xv[u]));
+        for (int u = 0; u < U; ++u)
+          if (r.b + lg + u * G < r.e) {
+            const double gx = static_cast<double>(c * xv[u]);
+            bad = bad || !isfinite(gx);
+            atomicAdd(&g64[jv[u]], -alpha * gx);  // g64 = the master here
+          }
+        if (bad) *finite = 0;
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (r.b + lg + u * G < r.e) atomicAdd(&g64[jv[u]], static_cast<double>(c * xv[u]));
+      }
     }
     if (prefetch_next && total <= cap) {
       // Pull the slots of the chunk at the same position of the next step
@@ -704,9 +741,11 @@ __global__ void __launch_bounds__(256) mb_scatter_kernel(
       const uint64_t qn = q + (c1 - c0);
       if (qn < total && lg < 16) {  // total <= cap: table entries below it are written
         const uint4 mn = __ldg(meta + qn);
-        const uint32_t lines = min((mn.y - mn.x + 31) / 32, (U * G + 31) / 32u);  // 128-byte lines
-        const char* base = lg < 8 ? reinterpret_cast<const char*>(idx + mn.x)
-                                  : reinterpret_cast<const char*>(val + mn.x);
+        // 128-byte lines spanned by slots [mn.x, mn.y), counted from the line
+        // holding mn.x (a chunk rarely starts on a line boundary).
+        const uint32_t lines = min(((mn.x & 31u) + (mn.y - mn.x) + 31) / 32, (U * G) / 32u + 1);
+        const char* base = lg < 8 ? reinterpret_cast<const char*>(idx + (mn.x & ~31u))
+                                  : reinterpret_cast<const char*>(val + (mn.x & ~31u));
         for (uint32_t l = lg & 7; l < lines; l += 8)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(base + 128ull * l));
       }
@@ -716,6 +755,8 @@ __global__ void __launch_bounds__(256) mb_scatter_kernel(
 
 __global__ void apply_kernel(uint64_t d, double alpha_in, const double* alpha_dev, double* w64,
                              float* w32, double* g64, int* finite, double* norm2, int want_norm) {
+  pdl_launch_dependents();
+  pdl_wait();  // g (and w) come from the step's kernels
   const double alpha = alpha_dev ? *alpha_dev : alpha_in;
   double nrm = 0.0;
   int bad = 0;
@@ -833,6 +874,13 @@ __global__ void __launch_bounds__(256) csr_loss_kernel(const float* __restrict__
   loss_tail(lsum, t);
 }
 
+__global__ void w32_from_w64_kernel(uint64_t d, const double* w64, float* w32) {
+  pdl_wait();
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    w32[j] = static_cast<float>(w64[j]);
+}
+
 __global__ void w64_from_w32_kernel(uint64_t d, const float* w32, double* w64) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d;
        j += (uint64_t)gridDim.x * blockDim.x)
@@ -846,6 +894,25 @@ int lanes_for(double avg) {
   if (avg <= 16.0) return 8;
   if (avg <= 40.0) return 16;
   return 32;
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// while its predecessor on the stream drains (it calls pdl_wait before
+// touching the predecessor's results). Captured into CUDA graphs as
+// programmatic edges.
+template <class... KArgs, class... Args>
+void launch_pdl(Ctx& c, void (*kern)(KArgs...), unsigned grid, unsigned block, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  check(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "cudaLaunchKernelEx");
 }
 
 unsigned grid_for(const Ctx& c, uint64_t items_per_block_unit, uint64_t units, unsigned per_sm) {
@@ -1011,15 +1078,11 @@ bool dense_epoch(Dataset& ds, Model& m, int task, double alpha, uint64_t B) {
       handled = false;
       return;
     }
-    // Measured (scripts/minibatch_time.py): 16 warps per CTA for F <= 8, else 8.
-    const int w = F <= 8 ? 16 : 8;
-    auto go = [&]<int W>() {
-      if (task == kTaskLR) launch_dense_epoch_LFW<L, F, kTaskLR, W>(ds, m, B, alpha);
-      else launch_dense_epoch_LFW<L, F, kTaskSVM, W>(ds, m, B, alpha);
-    };
-    if (w == 16) go.template operator()<16>();
-    else if (w == 32) go.template operator()<32>();
-    else go.template operator()<8>();
+    // Measured (scripts/minibatch_time.py): 16 warps per CTA for F <= 8, else
+    // 8 (only these instances are built: wider CTAs at F = 32 spill).
+    constexpr int W = F <= 8 ? 16 : 8;
+    if (task == kTaskLR) launch_dense_epoch_LFW<L, F, kTaskLR, W>(ds, m, B, alpha);
+    else launch_dense_epoch_LFW<L, F, kTaskSVM, W>(ds, m, B, alpha);
   });
   return handled;
 }
@@ -1042,7 +1105,7 @@ int batch_lanes(const Dataset& ds) {
 }
 
 template <int G, int TASK, int U>
-void launch_mb_chunks_U(Dataset& ds, Model& m, uint64_t lo, uint64_t nb, bool check) {
+void launch_mb_chunks_U(Dataset& ds, Model& m, uint64_t lo, uint64_t nb, bool check, const StepArgs& a) {
   Ctx& c = *ds.ctx;
   constexpr int RW = 32 / G;
   // Chunks of one step: the rows plus one per CH slots of their mean length.
@@ -1050,22 +1113,30 @@ void launch_mb_chunks_U(Dataset& ds, Model& m, uint64_t lo, uint64_t nb, bool ch
   const uint64_t est = nb + static_cast<uint64_t>(nb * avg / (G * U));
   const unsigned grid = grid_for(c, 8ull * RW, est, 16);
   const uint64_t hi = lo + nb;
-  prof_begin(c, "mb_margin_kernel");
-  mb_margin_kernel<G, U><<<grid, 256, 0, c.stream>>>(
-      ds.val.p, ds.idx.p, ds.rowptr.p, ds.mb_ids, ds.mb_off.p, ds.mb_meta.p, ds.mb_cap, lo, hi,
-      ds.row_base, m.w32.p, ds.mb_z.p, m.finite.p, check ? 1 : 0);
-  launched(c, "mb_margin_kernel");
-  prof_begin(c, "mb_scatter_kernel");
-  mb_scatter_kernel<G, U, TASK><<<grid, 256, 0, c.stream>>>(
-      ds.val.p, ds.idx.p, ds.rowptr.p, ds.labels.p, ds.mb_ids, ds.mb_off.p, ds.mb_meta.p,
-      ds.mb_cap, lo, hi, ds.row_base, ds.mb_z.p, m.g64.p, m.finite.p, check ? 1 : 0,
-      hi < ds.mb_count ? 1 : 0, ds.mb_count);
-  launched(c, "mb_scatter_kernel");
+  auto go = [&]<bool D>() {
+    prof_begin(c, "mb_margin_kernel");
+    launch_pdl(c, mb_margin_kernel<G, U, D>, grid, 256, ds.val.p, ds.idx.p, ds.rowptr.p,
+               static_cast<const uint32_t*>(ds.mb_ids), static_cast<const uint32_t*>(ds.mb_off.p),
+               static_cast<const uint4*>(ds.mb_meta.p), ds.mb_cap, lo, hi, ds.row_base,
+               static_cast<const float*>(m.w32.p), static_cast<const double*>(m.w64.p), ds.mb_z.p,
+               static_cast<const int*>(m.finite.p), check ? 1 : 0);
+    launched(c, "mb_margin_kernel");
+    prof_begin(c, "mb_scatter_kernel");
+    launch_pdl(c, mb_scatter_kernel<G, U, TASK, D>, grid, 256, ds.val.p, ds.idx.p, ds.rowptr.p,
+               static_cast<const float*>(ds.labels.p), static_cast<const uint32_t*>(ds.mb_ids),
+               static_cast<const uint32_t*>(ds.mb_off.p), static_cast<const uint4*>(ds.mb_meta.p),
+               ds.mb_cap, lo, hi, ds.row_base, static_cast<const float*>(ds.mb_z.p),
+               D ? m.w64.p : m.g64.p, m.finite.p, check ? 1 : 0, hi < ds.mb_count ? 1 : 0,
+               ds.mb_count, a.alpha, a.alpha_dev);
+    launched(c, "mb_scatter_kernel");
+  };
+  if (a.direct) go.template operator()<true>();
+  else go.template operator()<false>();
 }
 
 template <int G, int TASK>
-void launch_mb_chunks(Dataset& ds, Model& m, uint64_t lo, uint64_t nb, bool check) {
-  launch_mb_chunks_U<G, TASK, kChunkU>(ds, m, lo, nb, check);
+void launch_mb_chunks(Dataset& ds, Model& m, uint64_t lo, uint64_t nb, bool check, const StepArgs& a) {
+  launch_mb_chunks_U<G, TASK, kChunkU>(ds, m, lo, nb, check, a);
 }
 }  // namespace
 
@@ -1117,10 +1188,10 @@ void csr_batch_step(Dataset& ds, Model& m, const uint32_t* ids, uint64_t nb, con
     csr_batch_plan(ds, ids, nb, nb);
   const uint64_t lo = static_cast<uint64_t>(ids - ds.mb_ids);
   dispatch_G(g, [&]<int G>() {
-    if (a.task == kTaskLR) launch_mb_chunks<G, kTaskLR>(ds, m, lo, nb, a.apply);
-    else launch_mb_chunks<G, kTaskSVM>(ds, m, lo, nb, a.apply);
+    if (a.task == kTaskLR) launch_mb_chunks<G, kTaskLR>(ds, m, lo, nb, a.apply, a);
+    else launch_mb_chunks<G, kTaskSVM>(ds, m, lo, nb, a.apply, a);
   });
-  if (a.apply) apply_update(m, a.alpha, a.want_norm, a.alpha_dev);
+  if (a.apply && !a.direct) apply_update(m, a.alpha, a.want_norm, a.alpha_dev);
 }
 
 void apply_update(Model& m, double alpha, bool want_norm, const double* alpha_dev) {
@@ -1128,8 +1199,8 @@ void apply_update(Model& m, double alpha, bool want_norm, const double* alpha_de
   // One coordinate per thread (each iteration is a dependent load chain).
   const unsigned grid = grid_for(c, 256, m.d, 64);
   prof_begin(c, "apply_kernel");
-  apply_kernel<<<grid, 256, 0, c.stream>>>(m.d, alpha, alpha_dev, m.w64.p, m.w32.p, m.g64.p, m.finite.p,
-                                           m.scal.p, want_norm ? 1 : 0);
+  launch_pdl(c, apply_kernel, grid, 256, m.d, alpha, alpha_dev, m.w64.p, m.w32.p, m.g64.p, m.finite.p,
+             m.scal.p, want_norm ? 1 : 0);
   launched(c, "apply_kernel");
 }
 
@@ -1145,6 +1216,14 @@ void loss_launch(Dataset& ds, Model& m, int task) {
     const int g = lanes_for(static_cast<double>(ds.nnz) / static_cast<double>(ds.n));
     dispatch_G(g, [&]<int G>() { launch_csr_loss_G<G>(ds, m, task); });
   }
+}
+
+void sync_w32_from_w64(Model& m) {
+  Ctx& c = *m.ctx;
+  const unsigned grid = grid_for(c, 256ull * 4, m.d, 8);
+  prof_begin(c, "w32_from_w64_kernel");
+  launch_pdl(c, w32_from_w64_kernel, grid, 256, m.d, static_cast<const double*>(m.w64.p), m.w32.p);
+  launched(c, "w32_from_w64_kernel");
 }
 
 void sync_w64_from_w32(Model& m) {
