@@ -55,26 +55,28 @@ def _env_int(name, default):
         return default
 
 
-def _ncu_traffic(kernel):
+def _ncu_traffic(kernel, summary="round2_ncu_rcv1_full_batch.txt"):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
-    the committed `ncu --set full` summaries (profiles/round2_ncu_*.txt, written
-    by scripts/ncu_summary.py)."""
-    import glob
+    the committed `ncu --set full` summary of the headline configuration
+    (profiles/round2_ncu_rcv1_full_batch.txt, written by scripts/ncu_summary.py
+    from scripts/round2_profile.sh)."""
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "round2_ncu_*.txt")), reverse=True):
-        cur, got = None, {}
-        for line in open(path):
-            if line.startswith("== "):
-                if cur and kernel in cur and len(got) == 2:
-                    break
-                cur, got = line, {}
-                continue
-            parts = line.split()
-            if cur and kernel in cur and parts and parts[0] in ("dram__bytes_read.sum",
-                                                                 "dram__bytes_write.sum"):
-                got[parts[0]] = float(parts[1]) * scale.get(parts[2], 1)
-        if cur and kernel in cur and len(got) == 2:
-            return int(sum(got.values())), os.path.relpath(path, ROOT)
+    path = os.path.join(ROOT, "profiles", summary)
+    if not os.path.exists(path):
+        return None, None
+    cur, got = None, {}
+    for line in open(path):
+        if line.startswith("== "):
+            if cur and kernel in cur and len(got) == 2:
+                break
+            cur, got = line, {}
+            continue
+        parts = line.split()
+        if cur and kernel in cur and parts and parts[0] in ("dram__bytes_read.sum",
+                                                             "dram__bytes_write.sum"):
+            got[parts[0]] = float(parts[1]) * scale.get(parts[2], 1)
+    if cur and kernel in cur and len(got) == 2:
+        return int(sum(got.values())), os.path.relpath(path, ROOT)
     return None, None
 
 

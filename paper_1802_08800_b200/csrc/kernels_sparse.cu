@@ -292,6 +292,10 @@ __global__ void __launch_bounds__(kNT, 1)
   extern __shared__ __align__(16) float ws[];
   __shared__ CtaScratch sc;
   __shared__ uint64_t bar;
+  // PDL: launched while the previous step drains; the model (and the
+  // coefficients this pass overwrites) belong to it, so wait first.
+  pdl_wait();
+  pdl_launch_dependents();
   if (SMEMW && threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -379,9 +383,9 @@ struct ApplyArgs {
 // [cta_col[k], cta_col[k+1]) against it, writing fp32 per-(block, column)
 // sums; then g_j = sum over blocks (fixed block order, fp64) and w -= a g.
 // The apply is spread over the nblk CTAs of the column range once all of
-// them have arrived (coop: the launch is cooperative, so every CTA is
-// resident and the arrival wait cannot deadlock); otherwise the last CTA to
-// arrive applies the whole range. Arrival tickets count up by nblk per launch
+// them have arrived (coop: at most one CTA per SM and no more CTAs than SMs,
+// so every CTA is resident once the margin pass drains and the arrival wait
+// cannot deadlock); otherwise the last CTA to arrive applies the whole range. Arrival tickets count up by nblk per launch
 // (gen = launch number), so they are never reset.
 __global__ void __launch_bounds__(kNT, 1)
     k3s_grad_kernel(const float* __restrict__ cval, const uint16_t* __restrict__ crow,
@@ -396,6 +400,8 @@ __global__ void __launch_bounds__(kNT, 1)
   __shared__ uint64_t bar;
   const uint32_t b = blockIdx.x / cpb, k = blockIdx.x % cpb;
   const uint32_t r0 = b * rb, rows = min(rb, n - r0);  // rb % 4 == 0: 16-byte aligned slice
+  pdl_wait();  // the coefficients come from the margin pass
+  pdl_launch_dependents();
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -804,11 +810,24 @@ void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a) {
       const size_t smem = SW ? model_bytes : 0;
       set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(k2s)");
       prof_begin(c, "k2s_margin_kernel");
-      kern<<<ds.cta_n, kNT, smem, c.stream>>>(ds.val.p, I16 ? static_cast<const void*>(ds.cidx16.p)
-                                                            : static_cast<const void*>(ds.idx.p),
-                                              ds.rbm.p, ds.rbm_pre.p, ds.cta_slot.p,
-                                              ds.rows_empty ? ds.row_of_ord.p : nullptr, ds.labels.p,
-                                              static_cast<uint32_t>(ds.n), m.w32.p, d, ds.coef.p);
+      cudaLaunchConfig_t cfg{};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.gridDim = dim3(ds.cta_n);
+      cfg.blockDim = dim3(kNT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = c.stream;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      check(cudaLaunchKernelEx(&cfg, kern, static_cast<const float*>(ds.val.p),
+                               I16 ? static_cast<const void*>(ds.cidx16.p) : static_cast<const void*>(ds.idx.p),
+                               static_cast<const uint32_t*>(ds.rbm.p), static_cast<const uint32_t*>(ds.rbm_pre.p),
+                               static_cast<const uint32_t*>(ds.cta_slot.p),
+                               static_cast<const uint32_t*>(ds.rows_empty ? ds.row_of_ord.p : nullptr),
+                               static_cast<const float*>(ds.labels.p), static_cast<uint32_t>(ds.n),
+                               static_cast<const float*>(m.w32.p), d, ds.coef.p),
+            "cudaLaunchKernelEx(k2s)");
       launched(c, "k2s_margin_kernel");
     };
     if (smemw && i16) go.template operator()<true, true>();
@@ -825,7 +844,7 @@ void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a) {
     ApplyArgs aa{a.alpha, a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p, m.finite.p, m.scal.p};
     const unsigned grid = ds.csc_nblk * ds.csc_cpb;
     const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kNT, smem);
-    int coop = static_cast<uint64_t>(grid) <= static_cast<uint64_t>(per_sm) * c.num_sms ? 1 : 0;
+    int coop = per_sm >= 1 && grid <= static_cast<unsigned>(c.num_sms) ? 1 : 0;
     unsigned gen = ++ds.sparse_gen;
     prof_begin(c, "k3s_grad_kernel");
     const float* cval = ds.cval.p;
@@ -840,16 +859,22 @@ void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a) {
     const uint32_t* seg_of_ord = ds.segs_empty ? ds.seg_of_ord.p : nullptr;
     float* part = m.part32.p;
     unsigned* tickets = ds.sparse_tickets.p;
-    if (coop) {
-      void* args[] = {&cval, &crow, &cbm, &cbm_pre, &segptr, &cta_col, &cpb, &nblk, &dd, &rb, &n,
-                      &coef, &seg_of_ord, &part, &tickets, &aa, &gen, &coop};
-      check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kNT), args, smem,
-                                        c.stream),
-            "cudaLaunchCooperativeKernel(k3s)");
-    } else {
-      kern<<<grid, kNT, smem, c.stream>>>(cval, crow, cbm, cbm_pre, segptr, cta_col, cpb, nblk, dd, rb, n, coef,
-                                          seg_of_ord, part, tickets, aa, gen, coop);
-    }
+    // PDL launch (the CTAs start as the margin pass's CTAs retire). With one
+    // CTA per SM and grid <= SMs every CTA becomes resident once the margin
+    // pass has drained, so the range-arrival wait (coop) cannot deadlock.
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kNT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    check(cudaLaunchKernelEx(&cfg, kern, cval, crow, cbm, cbm_pre, segptr, cta_col, cpb, nblk, dd, rb, n, coef,
+                             seg_of_ord, part, tickets, aa, gen, coop),
+          "cudaLaunchKernelEx(k3s)");
     launched(c, "k3s_grad_kernel");
   }
 }
