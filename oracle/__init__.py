@@ -467,6 +467,35 @@ class Reference(_Lib):
             if handle is None:
                 self.lib.ref_ds_free(h)
 
+    def warpsim_epoch(self, ds: HostData, task, alpha, plan: str, warp_width=32, segment_size=8,
+                      offsets=True, w=None):
+        """warpsim::simulate_epoch (proj/src/simd_sim.cpp): returns (w, stats dict)."""
+        h = self.to_handle(ds)
+        try:
+            w = np.zeros(ds.n_features) if w is None else np.array(w, np.float64)
+            st = np.zeros(4, np.uint64)
+            L = self.lib
+            L.ref_warpsim_epoch.argtypes = [_vp, _int, _dbl, C.c_char_p, _u64, _u64, _int, _P(_dbl), _P(_u64)]
+            if L.ref_warpsim_epoch(h, task, alpha, plan.encode(), warp_width, segment_size, int(offsets),
+                                   _ptr(w, _dbl), _ptr(st, _u64)) != 0:
+                raise ValueError(self.err())
+            return w, {"attempted_updates": int(st[0]), "surviving_updates": int(st[1]),
+                       "memory_transactions": int(st[2]), "micro_steps": int(st[3])}
+        finally:
+            self.lib.ref_ds_free(h)
+
+    def count_transactions(self, lane_streams, segment_size):
+        """warpsim::count_transactions (proj/src/simd_sim.cpp:89-104)."""
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(s, np.uint64) for s in lane_streams])
+                                    if lane_streams else np.zeros(0, np.uint64), np.uint64)
+        off = np.zeros(len(lane_streams) + 1, np.uint64)
+        off[1:] = np.cumsum([len(s) for s in lane_streams])
+        L = self.lib
+        L.ref_count_transactions.restype = _u64
+        L.ref_count_transactions.argtypes = [_P(_u64), _P(_u64), _u64, _u64]
+        return int(L.ref_count_transactions(_ptr(flat, _u64), _ptr(off, _u64), len(lane_streams),
+                                            segment_size))
+
     def merge_models(self, replicas: np.ndarray, weights=None) -> np.ndarray:
         reps = np.ascontiguousarray(replicas, np.float64)
         r, d = reps.shape

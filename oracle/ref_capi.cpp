@@ -32,6 +32,7 @@
 #include "sgdbench/glm.hpp"
 #include "sgdbench/linalg.hpp"
 #include "sgdbench/sync_engine.hpp"
+#include "sgdbench/simd_sim.hpp"
 
 using namespace sgdbench;
 
@@ -391,6 +392,37 @@ int ref_elementwise(int op, const double* a, const double* b, uint64_t n, double
 
 void ref_axpy(double* w, double alpha, const double* g, uint64_t n, unsigned workers) {
   linalg::axpy(std::span<double>(w, n), alpha, std::span<const double>(g, n), workers);
+}
+
+// warpsim (proj/src/simd_sim.cpp): one lockstep epoch of the warp simulator;
+// stats_out = {attempted, surviving, memory_transactions, micro_steps}.
+int ref_warpsim_epoch(void* h, int task, double alpha, const char* plan_text, uint64_t warp_width,
+                      uint64_t segment_size, int offsets, double* w_inout, uint64_t* stats_out) {
+  try {
+    ExecutionPlan plan = parse_plan(plan_text);
+    warpsim::WarpConfig warp;
+    warp.warp_width = warp_width;
+    warp.segment_size = segment_size;
+    warp.offsets_enabled = offsets != 0;
+    std::vector<double> w(w_inout, w_inout + D(h)->n_features);
+    const auto st = warpsim::simulate_epoch(static_cast<Task>(task), *D(h), w, alpha, plan, warp, 0);
+    std::copy(w.begin(), w.end(), w_inout);
+    stats_out[0] = st.attempted_updates;
+    stats_out[1] = st.surviving_updates;
+    stats_out[2] = st.memory_transactions;
+    stats_out[3] = st.micro_steps;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// warpsim::count_transactions over lanes given as one flat array + offsets.
+uint64_t ref_count_transactions(const uint64_t* flat, const uint64_t* lane_off, uint64_t lanes,
+                                uint64_t segment_size) {
+  std::vector<std::vector<std::uint64_t>> streams(lanes);
+  for (uint64_t l = 0; l < lanes; ++l) streams[l].assign(flat + lane_off[l], flat + lane_off[l + 1]);
+  return warpsim::count_transactions(streams, segment_size);
 }
 
 }  // extern "C"
