@@ -13,14 +13,27 @@
 // Datasets are uploaded in the exact-fp64 mode (SGDB_UPLOAD_EXACT_FP64), so
 // results are bit-identical to the reference's; SGDB_PRECISION=fp32 selects
 // the fused fp32 kernels (the benchmarked path) instead.
+// Multi-GPU (one process per GPU): with SGDB_NRANKS=N,
+// SGDB_RANK=r and SGDB_NCCL_ID_FILE=<path on a shared filesystem> the context
+// attaches the engine's own NCCL communicator (rank 0 writes the id, the
+// others wait for it); sync::train / batch_gradient / epoch_batch then train
+// on the rank's contiguous row shard with the gradient all-reduced every step,
+// and hogwild::train runs each rank's shard with the replicas averaged every
+// merge_period_epochs (numa_dual_train's merge generalised to N ranks,
+// proj/src/async_engine.cpp:462-520). SGDB_DEVICE (default LOCAL_RANK, else
+// r) picks the GPU. Sharding needs row-major dense or CSR data.
 // Everything else (dataset I/O, plan grammar, harness, warp simulator) stays
 // the reference's. See INTEGRATION.md for the two ways to link it (replace
 // sync_engine.cpp / the engine half of async_engine.cpp, or interpose the
 // shared library ahead of libsgdbench).
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "sgdb.h"
 #include "sgdbench/async_engine.hpp"
@@ -40,10 +53,63 @@ void throw_for(sgdb_status st) {
   }
 }
 
+long env_long(const char* name, long fallback) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::strtol(e, nullptr, 10) : fallback;
+}
+
+struct Ranks {
+  int rank = 0, nranks = 1;
+};
+const Ranks& ranks() {
+  static const Ranks r = [] {
+    Ranks x;
+    x.nranks = static_cast<int>(env_long("SGDB_NRANKS", 1));
+    x.rank = static_cast<int>(env_long("SGDB_RANK", 0));
+    if (x.nranks < 1 || x.rank < 0 || x.rank >= x.nranks)
+      throw std::invalid_argument("SGDB_RANK / SGDB_NRANKS out of range");
+    return x;
+  }();
+  return r;
+}
+
+// File rendezvous for the 128-byte NCCL id: rank 0 writes <path>.tmp and
+// renames it (atomic), the others poll for <path>.
+void exchange_id(const std::string& path, int rank, uint8_t* id) {
+  if (rank == 0) {
+    throw_for(sgdb_nccl_get_unique_id(id));
+    const std::string tmp = path + ".tmp";
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    if (!f || std::fwrite(id, 1, 128, f) != 128) throw std::runtime_error("cannot write " + tmp);
+    std::fclose(f);
+    if (std::rename(tmp.c_str(), path.c_str()) != 0) throw std::runtime_error("cannot publish " + path);
+    return;
+  }
+  for (int t = 0; t < 6000; ++t) {  // up to 120 s
+    if (FILE* f = std::fopen(path.c_str(), "rb")) {
+      const size_t got = std::fread(id, 1, 128, f);
+      std::fclose(f);
+      if (got == 128) return;
+    }
+    std::this_thread::sleep_for(std::chrono::milliseconds(20));
+  }
+  throw std::runtime_error("timed out waiting for the NCCL id in " + path);
+}
+
 sgdb_ctx* context() {
   static sgdb_ctx* ctx = [] {
+    const Ranks& r = ranks();
+    const int device = static_cast<int>(env_long("SGDB_DEVICE", env_long("LOCAL_RANK", r.rank)));
     sgdb_ctx* c = nullptr;
-    throw_for(sgdb_ctx_create(0, nullptr, &c));
+    throw_for(sgdb_ctx_create(device, nullptr, &c));
+    const char* idf = std::getenv("SGDB_NCCL_ID_FILE");
+    if (r.nranks > 1 && !(idf && *idf))
+      throw std::invalid_argument("SGDB_NRANKS > 1 needs SGDB_NCCL_ID_FILE for the NCCL id rendezvous");
+    if (idf && *idf) {
+      uint8_t id[128];
+      exchange_id(idf, r.rank, id);
+      throw_for(sgdb_ctx_init_nccl(c, r.nranks, r.rank, id));
+    }
     return c;
   }();
   return ctx;
@@ -75,11 +141,45 @@ uint32_t upload_flags() {
   return flags;
 }
 
+// How a dataset is placed on a multi-rank context: the whole dataset on every
+// rank, a row shard of one logical dataset (sync: ids stay global, the
+// gradient is all-reduced), or a row shard trained as a dataset of its own
+// (Hogwild replicas averaged across ranks).
+enum class Placement { Whole, Shard, ShardAlone };
+
 struct Uploaded {
   sgdb_dataset* ds = nullptr;
-  explicit Uploaded(const sgdbench::Dataset& d) {
-    const sgdb_dataset_view v = view_of(d);
-    throw_for(sgdb_dataset_upload_ex(context(), &v, 0, 0, upload_flags(), &ds));
+  std::vector<std::uint64_t> offs;  // rebased CSR row offsets of a shard
+  explicit Uploaded(const sgdbench::Dataset& d, Placement place = Placement::Shard) {
+    sgdb_dataset_view v = view_of(d);
+    const Ranks& r = ranks();
+    uint64_t base = 0, n_global = 0;
+    if (r.nranks > 1 && place != Placement::Whole) {
+      // The chunk rule of assign() (dataset.cpp:484-490): ceil(N / ranks) rows each.
+      const uint64_t n = d.n_examples, chunk = (n + r.nranks - 1) / r.nranks;
+      base = std::min<uint64_t>(n, chunk * static_cast<uint64_t>(r.rank));
+      const uint64_t cnt = std::min<uint64_t>(n, base + chunk) - base;
+      if (d.layout == sgdbench::Layout::DenseRowMajor) {
+        v.values += base * d.n_features;
+        v.n_values = cnt * d.n_features;
+      } else if (d.layout == sgdbench::Layout::Csr) {
+        const uint64_t o0 = d.row_offsets[base];
+        offs.resize(cnt + 1);
+        for (uint64_t i = 0; i <= cnt; ++i) offs[i] = d.row_offsets[base + i] - o0;
+        v.values += o0;
+        v.indices += o0;
+        v.n_values = v.n_indices = offs[cnt];
+        v.row_offsets = offs.data();
+        v.n_row_offsets = cnt + 1;
+      } else {
+        throw std::invalid_argument("multi-GPU sharding needs row-major dense or CSR data");
+      }
+      v.labels += base;
+      v.n_examples = cnt;
+      n_global = place == Placement::Shard ? n : cnt;
+      if (place == Placement::ShardAlone) base = 0;
+    }
+    throw_for(sgdb_dataset_upload_ex(context(), &v, base, n_global, upload_flags(), &ds));
   }
   ~Uploaded() { sgdb_dataset_free(ds); }
 };
@@ -147,7 +247,7 @@ sgdbench::hogwild::Result run_hogwild(bool dual, sgdbench::Task task, const sgdb
   sgdbench::validate_plan(plan, ds);
   if (ds.n_examples == 0) throw std::invalid_argument("cannot train on an empty dataset");
   hyper.validate(ds.n_examples);
-  Uploaded up(ds);
+  Uploaded up(ds, Placement::ShardAlone);
   const sgdb_hyperparams h = hyper_of(task, hyper);
   const sgdb_plan p = plan_of(plan);
   Callbacks cb{&options.clock, &options.epoch_hook};
@@ -233,7 +333,7 @@ namespace linalg {
 DenseVector matvec(const Dataset& x, std::span<const std::uint32_t> rows, std::span<const double> v,
                    unsigned) {
   if (v.size() != x.n_features) throw std::invalid_argument("matvec: dimension mismatch");
-  Uploaded up(x);
+  Uploaded up(x, Placement::Whole);
   DenseVector out(rows.empty() ? x.n_examples : rows.size(), 0.0);
   throw_for(sgdb_matvec(context(), up.ds, rows.data(), rows.size(), v.data(), v.size(),
                         out.data()));
@@ -250,7 +350,7 @@ DenseVector matvec_transposed(const Dataset& x, std::span<const std::uint32_t> r
   if (a_by_position.size() != n)
     throw std::invalid_argument("matvec_transposed: dimension mismatch");
   if (n == 0) return DenseVector(x.n_features, 0.0);
-  Uploaded up(x);
+  Uploaded up(x, Placement::Whole);
   DenseVector out(x.n_features, 0.0);
   throw_for(sgdb_matvec_transposed(context(), up.ds, rows.data(), rows.size(),
                                    a_by_position.data(), a_by_position.size(), out.data()));

@@ -484,6 +484,58 @@ class Reference(_Lib):
         finally:
             self.lib.ref_ds_free(h)
 
+    def harness_run(self, ds: HostData, engine, task, alpha, batch_b, epochs, plan=None, workers=1,
+                    repetitions=1, seed=0, optimal_loss=None):
+        """harness::run (proj/src/harness.cpp): (losses, epochs_to {10,5,2,1: epoch|None}, l_used)."""
+        h = self.to_handle(ds)
+        try:
+            L = self.lib
+            L.ref_harness_run.argtypes = [_vp, _int, _int, _dbl, _u64, _u64, C.c_char_p, _u64, _u64, _u64,
+                                          _dbl, _P(_dbl), _P(_u64), _P(C.c_int64), _P(_dbl)]
+            losses = np.zeros(epochs, np.float64)
+            n = _u64(0)
+            et = np.zeros(4, np.int64)
+            lu = _dbl(0)
+            if L.ref_harness_run(h, engine, task, alpha, batch_b, epochs, (plan or "").encode(), workers,
+                                 repetitions, seed, float("nan") if optimal_loss is None else optimal_loss,
+                                 _ptr(losses, _dbl), C.byref(n), _ptr(et, C.c_int64), C.byref(lu)) != 0:
+                raise ValueError(self.err())
+            return (losses[:int(n.value)], {t: (int(e) or None) for t, e in zip((10, 5, 2, 1), et)},
+                    float(lu.value))
+        finally:
+            self.lib.ref_ds_free(h)
+
+    def estimate_optimal_loss(self, ds: HostData, task, epochs):
+        """harness::estimate_optimal_loss over the default probes' step-size grid,
+        `epochs` batch-GD epochs each (cache cleared first)."""
+        h = self.to_handle(ds)
+        try:
+            L = self.lib
+            L.ref_estimate_optimal_loss.restype = _dbl
+            L.ref_estimate_optimal_loss.argtypes = [_vp, _int, _u64]
+            return float(L.ref_estimate_optimal_loss(h, task, epochs))
+        finally:
+            self.lib.ref_ds_free(h)
+
+    def grid_search_alpha(self, ds: HostData, engine, task, batch_b, epochs, grid, plan=None, workers=1,
+                          seed=0, optimal_loss=None):
+        """harness::grid_search_alpha: (best_alpha, converged, l_used)."""
+        h = self.to_handle(ds)
+        try:
+            L = self.lib
+            L.ref_grid_search_alpha.argtypes = [_vp, _int, _int, _u64, _u64, C.c_char_p, _u64, _u64, _dbl,
+                                                _P(_dbl), _u64, _P(_dbl), _P(_int), _P(_dbl)]
+            g = np.ascontiguousarray(grid, np.float64)
+            best, conv, lu = _dbl(0), _int(0), _dbl(0)
+            if L.ref_grid_search_alpha(h, engine, task, batch_b, epochs, (plan or "").encode(), workers, seed,
+                                       float("nan") if optimal_loss is None else optimal_loss,
+                                       _ptr(g, _dbl), len(g), C.byref(best), C.byref(conv),
+                                       C.byref(lu)) != 0:
+                raise ValueError(self.err())
+            return float(best.value), bool(conv.value), float(lu.value)
+        finally:
+            self.lib.ref_ds_free(h)
+
     def count_transactions(self, lane_streams, segment_size):
         """warpsim::count_transactions (proj/src/simd_sim.cpp:89-104)."""
         flat = np.ascontiguousarray(np.concatenate([np.asarray(s, np.uint64) for s in lane_streams])

@@ -33,6 +33,7 @@
 #include "sgdbench/linalg.hpp"
 #include "sgdbench/sync_engine.hpp"
 #include "sgdbench/simd_sim.hpp"
+#include "sgdbench/harness.hpp"
 
 using namespace sgdbench;
 
@@ -392,6 +393,97 @@ int ref_elementwise(int op, const double* a, const double* b, uint64_t n, double
 
 void ref_axpy(double* w, double alpha, const double* g, uint64_t n, unsigned workers) {
   linalg::axpy(std::span<double>(w, n), alpha, std::span<const double>(g, n), workers);
+}
+
+// harness (proj/src/harness.cpp): run / estimate_optimal_loss /
+// grid_search_alpha with the Sync or Async engine. losses_out: the first
+// repetition's losses (n_out entries); epochs_to_out[4]: epochs to 10/5/2/1 %
+// of the loss used (0 = not reached).
+namespace {
+harness::RunConfig harness_config(int engine, int task, double alpha, uint64_t batch_b,
+                                  uint64_t epochs, const char* plan_text, uint64_t workers,
+                                  uint64_t repetitions, uint64_t seed, double optimal_loss) {
+  harness::RunConfig c;
+  c.engine = engine == 0 ? harness::Engine::Sync : harness::Engine::Async;
+  c.task = static_cast<Task>(task);
+  c.hyper.task = c.task;
+  c.hyper.alpha = alpha;
+  c.hyper.batch_b = batch_b;
+  c.hyper.epochs = epochs;
+  c.workers = workers;
+  if (plan_text && *plan_text) {
+    ExecutionPlan p = parse_plan(plan_text);
+    p.workers = workers;
+    c.plan = p;
+  }
+  c.repetitions = repetitions;
+  c.seed = seed;
+  c.wall_clock_budget_seconds = 600.0;
+  if (!std::isnan(optimal_loss)) c.optimal_loss = optimal_loss;
+  return c;
+}
+void report_out(const harness::RunReport& r, double* losses_out, uint64_t* n_out, int64_t* epochs_to_out,
+                double* l_used) {
+  *n_out = r.trace.epochs.size();
+  for (std::size_t i = 0; i < r.trace.epochs.size(); ++i) losses_out[i] = r.trace.epochs[i].loss;
+  const int tols[4] = {10, 5, 2, 1};
+  for (int k = 0; k < 4; ++k) {
+    auto it = r.epochs_to.find(tols[k]);
+    epochs_to_out[k] = it != r.epochs_to.end() && it->second ? static_cast<int64_t>(*it->second) : 0;
+  }
+  *l_used = r.optimal_loss_used;
+}
+}  // namespace
+
+int ref_harness_run(void* h, int engine, int task, double alpha, uint64_t batch_b, uint64_t epochs,
+                    const char* plan_text, uint64_t workers, uint64_t repetitions, uint64_t seed,
+                    double optimal_loss, double* losses_out, uint64_t* n_out, int64_t* epochs_to_out,
+                    double* l_used) {
+  try {
+    const auto c = harness_config(engine, task, alpha, batch_b, epochs, plan_text, workers, repetitions,
+                                  seed, optimal_loss);
+    report_out(harness::run(c, *D(h)), losses_out, n_out, epochs_to_out, l_used);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// estimate_optimal_loss with the default probes' construction
+// (harness.cpp:275-289: batch GD over default_alpha_grid) but `epochs`
+// epochs each instead of 100,000 under a wall-clock budget.
+double ref_estimate_optimal_loss(void* h, int task, uint64_t epochs) {
+  harness::clear_optimal_loss_cache();
+  std::vector<harness::RunConfig> probes;
+  for (double alpha : harness::default_alpha_grid()) {
+    harness::RunConfig c;
+    c.engine = harness::Engine::Sync;
+    c.task = static_cast<Task>(task);
+    c.hyper.task = c.task;
+    c.hyper.alpha = alpha;
+    c.hyper.batch_b = D(h)->n_examples;
+    c.hyper.epochs = epochs;
+    c.max_epochs = epochs;
+    probes.push_back(std::move(c));
+  }
+  return harness::estimate_optimal_loss(static_cast<Task>(task), *D(h), probes, 600.0);
+}
+
+int ref_grid_search_alpha(void* h, int engine, int task, uint64_t batch_b, uint64_t epochs,
+                          const char* plan_text, uint64_t workers, uint64_t seed, double optimal_loss,
+                          const double* grid, uint64_t n_grid, double* best_alpha, int* converged,
+                          double* l_used) {
+  try {
+    auto c = harness_config(engine, task, grid[0], batch_b, epochs, plan_text, workers, 1, seed,
+                            optimal_loss);
+    const auto r = harness::grid_search_alpha(c, *D(h), std::vector<double>(grid, grid + n_grid));
+    *best_alpha = r.best_alpha;
+    *converged = r.converged ? 1 : 0;
+    *l_used = r.optimal_loss_used;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
 }
 
 // warpsim (proj/src/simd_sim.cpp): one lockstep epoch of the warp simulator;

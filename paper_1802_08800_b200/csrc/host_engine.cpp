@@ -180,6 +180,13 @@ LoopResult hogwild_loop(sgdb_ctx* ctx, sgdb_dataset* ds, Task task, const Hyperp
       throw_status(sgdb_models_average(ctx, pair, 2, nullptr, merged->m, merge_due ? 1 : 0));
       view = merged->m;
     }
+    // Multi-GPU (an NCCL communicator on the context): every rank trains its
+    // replica, averaged across ranks every merge period (numa_dual_train's
+    // merge generalised to N ranks, async_engine.cpp:478-501).
+    int32_t rank = 0, nranks = 1;
+    throw_status(sgdb_ctx_world(ctx, &rank, &nranks));
+    if (!dual && nranks > 1 && plan.merge_period_epochs > 0 && epoch % plan.merge_period_epochs == 0)
+      throw_status(sgdb_model_average_ranks(ctx, a.m, static_cast<uint64_t>(nranks)));
     throw_status(sgdb_ctx_synchronize(ctx));  // epoch work is stream-asynchronous
     const double t1 = o.now();
     r.evals.push_back(static_cast<std::size_t>(ea + eb));
