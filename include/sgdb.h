@@ -230,6 +230,11 @@ sgdb_status sgdb_dataset_upload(sgdb_ctx* ctx, const sgdb_dataset_view* view, ui
  * (kernels_linalg.cu, libm_exp.hpp). Results then equal the reference's bit
  * for bit (LR losses to the ulp of log1p). Whole (unsharded) datasets only. */
 #define SGDB_UPLOAD_EXACT_FP64 1u
+/* SGDB_UPLOAD_PADDED: a CSR view is uploaded and its slot-major padded copy
+ * (convert_layout(Csr -> PaddedDense), proj/src/dataset.cpp:380-402: width =
+ * the longest row, sentinel index d with value 0) is built on the device; the
+ * dataset then behaves as a PaddedDense upload (column access paths). */
+#define SGDB_UPLOAD_PADDED 2u
 sgdb_status sgdb_dataset_upload_ex(sgdb_ctx* ctx, const sgdb_dataset_view* view, uint64_t row_base,
                                    uint64_t n_global, uint32_t flags, sgdb_dataset** out);
 /* Re-copy host arrays of the same shape into an existing device dataset

@@ -17,6 +17,7 @@ P = C.POINTER
 
 SGDB_OK = 0
 SGDB_UPLOAD_EXACT_FP64 = 1
+SGDB_UPLOAD_PADDED = 2
 STATUS_NAMES = {
     1: "invalid_argument", 2: "domain_error", 3: "parse_error", 4: "capacity_error",
     5: "runtime_error", 6: "cuda_error", 7: "unsupported",

@@ -469,7 +469,10 @@ class DeviceDataset:
     mode), optionally a row shard."""
 
     def __init__(self, dev: Device, ds: Optional[Dataset], row_base: int = 0, n_global: int = 0,
-                 exact: Optional[bool] = None, _handle=None):
+                 exact: Optional[bool] = None, _handle=None, padded: bool = False):
+        """padded=True (CSR input): the slot-major padded copy is built on the
+        device (SGDB_UPLOAD_PADDED) and the dataset serves the column access
+        paths like a PaddedDense upload."""
         self.dev = dev
         self.host = ds
         self.exact = bool(default_exact() if exact is None else exact) if _handle is None else False
@@ -478,15 +481,15 @@ class DeviceDataset:
         else:
             self._h = L.vp()
             v = ds.view()
-            check(_lib().sgdb_dataset_upload_ex(dev.handle, C.byref(v), row_base, n_global,
-                                                L.SGDB_UPLOAD_EXACT_FP64 if self.exact else 0,
+            flags = (L.SGDB_UPLOAD_EXACT_FP64 if self.exact else 0) | (L.SGDB_UPLOAD_PADDED if padded else 0)
+            check(_lib().sgdb_dataset_upload_ex(dev.handle, C.byref(v), row_base, n_global, flags,
                                                 C.byref(self._h)))
         n, d, nnz, rb, ng = (L.u64() for _ in range(5))
         check(_lib().sgdb_dataset_shape(self._h, C.byref(n), C.byref(d), C.byref(nnz),
                                         C.byref(rb), C.byref(ng)))
         self.n_local, self.n_features, self.nnz = int(n.value), int(d.value), int(nnz.value)
         self.row_base, self.n_global = int(rb.value), int(ng.value)
-        self.layout = ds.layout if ds is not None else Layout.DenseRowMajor
+        self.layout = (Layout.PaddedDense if padded else ds.layout) if ds is not None else Layout.DenseRowMajor
 
     @classmethod
     def generate_dense(cls, dev: Device, n_local: int, d: int, seed: int, row_base: int = 0,

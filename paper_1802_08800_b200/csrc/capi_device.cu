@@ -383,7 +383,12 @@ sgdb_status sgdb_dataset_upload_ex(sgdb_ctx* ctx, const sgdb_dataset_view* v, ui
                                    uint64_t n_global, uint32_t flags, sgdb_dataset** out) {
   return sgdb_guard([&] {
     require(ctx && v && out, "null argument");
-    require((flags & ~uint32_t(SGDB_UPLOAD_EXACT_FP64)) == 0, "unknown upload flags");
+    require((flags & ~uint32_t(SGDB_UPLOAD_EXACT_FP64 | SGDB_UPLOAD_PADDED)) == 0, "unknown upload flags");
+    if (flags & SGDB_UPLOAD_PADDED) {
+      require(v->layout == SGDB_LAYOUT_CSR, "SGDB_UPLOAD_PADDED converts a CSR view");
+      if (flags & SGDB_UPLOAD_EXACT_FP64)
+        throw Unsupported("SGDB_UPLOAD_PADDED with the exact-fp64 mode: convert on the host");
+    }
     const uint64_t n = v->n_examples, d = v->n_features;
     require(n == 0 || v->labels != nullptr, "labels missing");
     if (n_global == 0) n_global = n;
@@ -483,6 +488,10 @@ sgdb_status sgdb_dataset_upload_ex(sgdb_ctx* ctx, const sgdb_dataset_view* v, ui
       }
       default:
         throw std::invalid_argument("unknown layout");
+    }
+    if (flags & SGDB_UPLOAD_PADDED) {
+      build_padded_from_csr(*ds);  // device-side csr_to_padded
+      ds->layout_in = SGDB_LAYOUT_PADDED;
     }
     if (flags & SGDB_UPLOAD_EXACT_FP64) {
       // fp64 copy aligned with the fp32 storage built above.

@@ -324,6 +324,9 @@ void exact_epoch_batch(Dataset& ds, Model& m, int task, double alpha);
 void exact_loss(Dataset& ds, Model& m, int task);
 void exact_hogwild(Dataset& ds, Model& m, const HogwildArgs& a);
 void build_col(Dataset& ds);
+// Slot-major padded copy (pval / pidx, width = longest row, sentinel d) of the
+// uploaded CSR, on the device (convert_layout(Csr -> PaddedDense)).
+void build_padded_from_csr(Dataset& ds);
 
 }  // namespace sgdb::dev
 

@@ -515,6 +515,22 @@ __global__ void copy_model_kernel(uint64_t d, const double* src64, double* dst64
   }
 }
 
+// K8p: CSR -> slot-major padded (proj/src/dataset.cpp:380-402): thread per
+// row, slot s of row e at s*n + e (coalesced over e), padding = (0, d).
+__global__ void csr_to_padded_kernel(const float* __restrict__ val, const uint32_t* __restrict__ idx,
+                                     const uint32_t* __restrict__ rowptr, uint64_t n, uint64_t d,
+                                     uint64_t pw, float* pval, uint32_t* pidx) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = rowptr[e], len = rowptr[e + 1] - b;
+    for (uint64_t s = 0; s < pw; ++s) {
+      const bool in = s < len;
+      pval[s * n + e] = in ? val[b + s] : 0.f;
+      pidx[s * n + e] = in ? idx[b + s] : static_cast<uint32_t>(d);
+    }
+  }
+}
+
 // K8: dense row-major -> column-major (32x32 tiles through shared memory).
 __global__ void transpose_kernel(const float* __restrict__ in, float* __restrict__ out,
                                  uint64_t rows, uint64_t cols) {
@@ -852,6 +868,24 @@ void scale_model(Model& m, double scale) {
   prof_begin(c, "scale_model_kernel");
   scale_model_kernel<<<grid, 256, 0, c.stream>>>(m.d, scale, m.w64.p, m.w32.p);
   launched(c, "scale_model_kernel");
+}
+
+void build_padded_from_csr(Dataset& ds) {
+  Ctx& c = *ds.ctx;
+  const uint64_t n = ds.n, pw = ds.max_row;
+  ds.pw = pw;
+  ds.pval.alloc(std::max<uint64_t>(1, n * pw));
+  ds.pidx.alloc(std::max<uint64_t>(1, n * pw));
+  if (n && pw) {
+    const unsigned grid =
+        static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, c.num_sms * 8ull)));
+    prof_begin(c, "csr_to_padded_kernel");
+    csr_to_padded_kernel<<<grid, 256, 0, c.stream>>>(ds.val.p, ds.idx.p, ds.rowptr.p, n, ds.d, pw, ds.pval.p,
+                                                     ds.pidx.p);
+    launched(c, "csr_to_padded_kernel");
+  }
+  check(cudaStreamSynchronize(c.stream), "padded build");
+  ds.col_built = true;
 }
 
 void build_col(Dataset& ds) {
