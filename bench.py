@@ -524,6 +524,15 @@ def extra_shapes(S, dev):
             rec["hogwild"] = {"plan": plan_text, "workers": plan.workers, "epoch_ms": ams,
                               "value": n / (ams / 1e3), "unit": UNIT,
                               "frac_one_sweep": sweep / (ams / 1e3) / 1e9 / peak}
+        if name == "C3_rcv1_lr":  # block scope, 8 replicas in L2 (C3: "per-block model replication")
+            plan = S.parse_plan("row-ch:block:0")
+            plan.workers = dev.resident_workers(dds)
+            plan.group_size = plan.workers // 8
+            hm = S.DeviceModel(dev, host.n_features)
+            ams = _time_hogwild(S, dds, hm, task, 0.03, plan, 5, 2, flush)
+            rec["hogwild_block_R8"] = {"plan": "row-ch:block:0", "workers": plan.workers,
+                                       "group_size": plan.group_size, "epoch_ms": ams,
+                                       "value": n / (ams / 1e3), "unit": UNIT}
         out[name] = rec
         del dds, host
     return out
