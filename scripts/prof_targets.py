@@ -1,6 +1,8 @@
 """Small driver for ncu captures: runs a few epochs of one target op.
 
-    python scripts/prof_targets.py {hogwild_w8a|hogwild_rcv1_block|sync_covtype|sync_rcv1|sync_realsim|sync_news20|sync_dense1000|sync_c5} [epochs]
+    python scripts/prof_targets.py {hogwild_w8a|hogwild_rcv1_block|hogwild_rcv1_block8|hogwild_w8a_example|
+                                    sync_covtype|sync_rcv1|sync_realsim|sync_news20|sync_dense1000|sync_c5|
+                                    minibatch_covtype|minibatch_rcv1} [epochs]
 """
 import os
 import sys
@@ -26,15 +28,37 @@ def main():
         for _ in range(epochs):
             flush.zero_()
             S.hogwild_epoch(dds, model, S.Task.SVM, 0.01, plan)
-    elif target == "hogwild_rcv1_block":
+    elif target in ("hogwild_rcv1_block", "hogwild_rcv1_block8"):
         host = S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813)
         dds = S.DeviceDataset(dev, host)
         plan = S.parse_plan("row-ch:block:0")
         plan.workers = dev.resident_workers(dds)
+        if target.endswith("8"):
+            plan.group_size = plan.workers // 8  # 8 replicas in L2 (K6g)
         model = S.DeviceModel(dev, host.n_features)
         for _ in range(epochs):
             flush.zero_()
             S.hogwild_epoch(dds, model, S.Task.LR, 0.01, plan)
+    elif target == "hogwild_w8a_example":
+        host = S.fixtures.sparse_classification(64700, 300, 11.65, 20250811)
+        dds = S.DeviceDataset(dev, host)
+        plan = S.parse_plan("row-ch:example:0")
+        plan.workers = dev.resident_workers(dds)
+        model = S.DeviceModel(dev, host.n_features)
+        for _ in range(epochs):
+            flush.zero_()
+            S.hogwild_epoch(dds, model, S.Task.SVM, 0.01, plan)
+    elif target in ("minibatch_covtype", "minibatch_rcv1"):
+        if target.endswith("covtype"):
+            host, task, alpha = S.fixtures.dense_classification(581012, 54, 20250810), S.Task.LR, 1e-3
+        else:
+            host, task, alpha = S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813), S.Task.LR, 1e-2
+        dds = S.DeviceDataset(dev, host)
+        model = S.DeviceModel(dev, host.n_features)
+        order = S.Schedule(1, host.n_examples).next()
+        for _ in range(epochs):
+            flush.zero_()
+            S.sync_epoch(dds, model, task, alpha, order, 4096)
     elif target == "sync_c5":
         # C5 shape (d = 1000), device Philox generator; 2M rows = 8 GB > L2.
         dds = S.DeviceDataset.generate_dense(dev, 2_000_000, 1000, 20250814)
