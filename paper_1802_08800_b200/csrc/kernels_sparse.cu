@@ -202,10 +202,16 @@ struct CtaScratch {
 // split evenly over the warps (4-slot aligned), streamed, and the segments
 // cut between warps finished in slot order. emit(X, z) receives every
 // complete segment once.
-template <int E, int NB, class Win, class Ld, class Prod, class Emit>
+// emit(X, z) receives the segments the warps complete inside their streams
+// (each warp's are the consecutive ordinals [lo, hi) reported to
+// warp_done(lo, hi), called by every lane of the warp as soon as its stream
+// ends, before the CTA barrier); emit_final(X, z) the segments assembled
+// after the barrier (cut between warps, or closed by the CTA end).
+template <int E, int NB, class Win, class Ld, class Prod, class Emit, class EmitFinal, class WarpDone>
 __device__ __forceinline__ void cta_segments(uint32_t S0, uint32_t S1, const uint32_t* __restrict__ bm,
                                              const uint32_t* __restrict__ bpre, Ld ld, Prod prod,
-                                             Emit emit, CtaScratch& sc) {
+                                             Emit emit, EmitFinal emit_final, WarpDone warp_done,
+                                             CtaScratch& sc) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   auto split = [&](int k) -> uint32_t {
     if (k <= 0) return S0;
@@ -219,7 +225,8 @@ __device__ __forceinline__ void cta_segments(uint32_t S0, uint32_t S1, const uin
   // Ordinal of the CTA's first segment: closings of lower ordinals (the
   // segment ending at S0 - 1) belong to the previous CTA and are dropped.
   const int32_t xmin = S1 > S0 ? heads_before(bm, bpre, S0) : 0;
-  int32_t ord = S1 > S0 ? heads_before(bm, bpre, P) - 1 : 0;
+  const int32_t ord0 = S1 > S0 ? heads_before(bm, bpre, P) - 1 : 0;
+  int32_t ord = ord0;
   float carry = 0.f;
   bool had = false;
   seg_stream<E, NB, Win>(P, Q, bm, ord, carry, had, ld, prod, [&](int32_t X, float z, bool first) {
@@ -233,12 +240,14 @@ __device__ __forceinline__ void cta_segments(uint32_t S0, uint32_t S1, const uin
     }
   });
   __syncwarp();
+  // The warp's first closing (ordinal ord0) is a piece; the rest are whole.
+  warp_done(had ? ord0 + 1 : ord, ord);
   if (lane == 0) {
     sc.pl[w] = carry;
     sc.had[w] = had;
     if (w == kNW - 1 && S1 > S0) {  // the CTA end closes the open segment
       if (had) {
-        emit(ord, carry);
+        emit_final(ord, carry);
       } else {
         sc.pf[w] = carry;
         sc.pf_ord[w] = ord;
@@ -256,7 +265,7 @@ __device__ __forceinline__ void cta_segments(uint32_t S0, uint32_t S1, const uin
     while (v0 > 0 && !sc.had[v0]) --v0;
     float z = 0.f;
     for (int v = v0; v < t; ++v) z += sc.pl[v];
-    emit(sc.pf_ord[t], z + sc.pf[t]);
+    emit_final(sc.pf_ord[t], z + sc.pf[t]);
   }
 }
 
@@ -276,10 +285,11 @@ struct WinC {
 constexpr int kE = 8;
 
 // K2s: margins and coefficients c = coef(z, y) of all local rows
-// (glm.cpp:30-34). The stream emits each row's margin z in place; once the
-// CTA's rows are all complete, the CTA turns its (contiguous) rows' margins
-// into coefficients with coalesced label loads — no label load on the
-// stream's emission path. One CTA per SM; the fp32 model is bulk-copied (1-D
+// (glm.cpp:30-34). The stream emits each row's margin z in place; each warp
+// then turns its own (consecutive) rows into coefficients with coalesced
+// label loads while the CTA's other warps still stream — no label load on
+// the stream's emission path; rows finished after the CTA barrier (cut
+// between warps) get their coefficient directly. One CTA per SM; the fp32 model is bulk-copied (1-D
 // TMA) into SMEM when it fits (SMEMW), else gathered through L1/L2. I16:
 // 16-bit column ids (d <= 65536).
 template <int TASK, bool SMEMW, bool I16>
@@ -341,31 +351,33 @@ __global__ void __launch_bounds__(kNT, 1)
         for (int u = 0; u < 8; ++u) p[u] = x[u] * (SMEMW ? w[j[u]] : __ldg(w + j[u]));
       },
       [&](int32_t X, float z) { coef[row_of_ord ? __ldg(row_of_ord + X) : static_cast<uint32_t>(X)] = z; },
+      [&](int32_t X, float z) {
+        const uint32_t r = row_of_ord ? __ldg(row_of_ord + X) : static_cast<uint32_t>(X);
+        coef[r] = coef_fast<TASK>(z, __ldg(y + r));
+      },
+      [&](int32_t lo, int32_t hi) {
+        // The warp's own rows turn their margins into coefficients while the
+        // CTA's other warps still stream (coalesced, all loads in flight).
+        for (int32_t o0 = lo + (threadIdx.x & 31); o0 < hi; o0 += 32 * 4) {
+          uint32_t r[4];
+          float z[4], yy[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int32_t o = o0 + 32 * i;
+            r[i] = o < hi ? (row_of_ord ? __ldg(row_of_ord + o) : static_cast<uint32_t>(o)) : 0u;
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            z[i] = coef[r[i]];
+            yy[i] = __ldg(y + r[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (o0 + 32 * i < hi) coef[r[i]] = coef_fast<TASK>(z[i], yy[i]);
+        }
+      },
       sc);
   if (SMEMW && !ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
-  // cta_segments ends with the cut-segment fix-ups: wait for them, then the
-  // CTA's ordinals [xmin, xend) hold margins.
-  __syncthreads();
-  if (S1 <= S0) return;
-  const int32_t xmin = heads_before(bm, bpre, S0), xend = heads_before(bm, bpre, S1);
-  constexpr int KU = 8;  // rows per thread per round, all loads in flight together
-  for (int32_t o0 = xmin + threadIdx.x; o0 < xend; o0 += KU * kNT) {
-    uint32_t r[KU];
-    float z[KU], yy[KU];
-#pragma unroll
-    for (int i = 0; i < KU; ++i) {
-      const int32_t o = o0 + i * kNT;
-      r[i] = o < xend ? (row_of_ord ? __ldg(row_of_ord + o) : static_cast<uint32_t>(o)) : 0u;
-    }
-#pragma unroll
-    for (int i = 0; i < KU; ++i) {
-      z[i] = __ldcg(coef + r[i]);
-      yy[i] = __ldg(y + r[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < KU; ++i)
-      if (o0 + i * kNT < xend) coef[r[i]] = coef_fast<TASK>(z[i], yy[i]);
-  }
 }
 
 struct ApplyArgs {
@@ -436,10 +448,9 @@ __global__ void __launch_bounds__(kNT, 1)
         p[4] = q.v1.x * cs[q.r.z & 0xffffu], p[5] = q.v1.y * cs[q.r.z >> 16];
         p[6] = q.v1.z * cs[q.r.w & 0xffffu], p[7] = q.v1.w * cs[q.r.w >> 16];
       },
-      [&](int32_t X, float z) {
-        const uint32_t q = seg_of_ord ? __ldg(seg_of_ord + X) : static_cast<uint32_t>(X);
-        part[q] = z;
-      },
+      [&](int32_t X, float z) { part[seg_of_ord ? __ldg(seg_of_ord + X) : static_cast<uint32_t>(X)] = z; },
+      [&](int32_t X, float z) { part[seg_of_ord ? __ldg(seg_of_ord + X) : static_cast<uint32_t>(X)] = z; },
+      [&](int32_t, int32_t) {},
       sc);
   if (!ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
   __syncthreads();
