@@ -19,6 +19,8 @@
 #include <numeric>
 #include <random>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a tool attached
+
 #include "device.hpp"
 #include "errors.hpp"
 #include "sgdb_b200.hpp"
@@ -117,8 +119,10 @@ LoopResult sync_loop(sgdb_ctx* ctx, sgdb_dataset* ds, Task task, const Hyperpara
     if (o.shuffle && !full) std::shuffle(order.begin(), order.end(), rng);
     const double t0 = o.now();
     int32_t finite = 1;
+    nvtxRangePushA("sgdb sync epoch");
     throw_status(sgdb_sync_epoch(ctx, ds, model.m, static_cast<int32_t>(task), alpha,
                                  full ? nullptr : order.data(), b, &finite));
+    nvtxRangePop();
     const double t1 = o.now();
     const double loss = device_loss(ctx, ds, model.m, task);
     r.trace.epochs.push_back({epoch, loss, t1 - t0});
@@ -171,6 +175,7 @@ LoopResult hogwild_loop(sgdb_ctx* ctx, sgdb_dataset* ds, Task task, const Hyperp
     const double alpha = hyper.step_size(epoch);
     const double t0 = o.now();
     uint64_t ea = 0, eb = 0;
+    nvtxRangePushA("sgdb hogwild epoch");
     throw_status(sgdb_hogwild_epoch(ctx, ds, a.m, static_cast<int32_t>(task), alpha, &cp, &ea));
     sgdb_model* view = a.m;
     if (dual) {
@@ -188,6 +193,7 @@ LoopResult hogwild_loop(sgdb_ctx* ctx, sgdb_dataset* ds, Task task, const Hyperp
     if (!dual && nranks > 1 && plan.merge_period_epochs > 0 && epoch % plan.merge_period_epochs == 0)
       throw_status(sgdb_model_average_ranks(ctx, a.m, static_cast<uint64_t>(nranks)));
     throw_status(sgdb_ctx_synchronize(ctx));  // epoch work is stream-asynchronous
+    nvtxRangePop();
     const double t1 = o.now();
     r.evals.push_back(static_cast<std::size_t>(ea + eb));
     const double loss = device_loss(ctx, ds, view, task);
