@@ -1,14 +1,23 @@
 // Host data layer of the engine (layer 3 of include/sgdb.h) and the
 // sgdb:: C++ mirror of the reference's dataset / fixtures / plan API.
 //
-// Written from the reference's behavioural contract (paths relative to
-// /root/reference/proj): LIBSVM ingestion with its label normalisation and
-// error lines (src/dataset.cpp:145-230), the sgdbds01 binary cache
-// (:257-327), layout conversions (:333-446), worker assignment (:470-503),
-// the synthetic fixtures (src/fixtures.cpp:12-100) and the plan grammar
-// (src/async_engine.cpp:37-117). Fixtures and the mini-batch schedule go
-// through libstdc++ <random> exactly as the reference does, which makes them
-// bit-identical to it (checked in tests/test_host.py).
+// This file is a PORT of the reference's host code, not a redesign (paths
+// relative to /root/reference/proj): the bit-exactness contract leaves no
+// freedom in parse order, rounding, <random> draw order, byte format or error
+// text, so each function follows its reference counterpart step by step:
+//   parse_libsvm / write_libsvm     <- src/dataset.cpp:145-230 (label
+//                                      normalisation, error lines)
+//   save_binary / load_binary       <- src/dataset.cpp:257-327 (sgdbds01)
+//   transpose_dense, convert_layout,
+//   append_bias_feature             <- src/dataset.cpp:333-446
+//   assign                          <- src/dataset.cpp:470-503
+//   fixtures                        <- src/fixtures.cpp:12-100
+//   plan grammar / validation       <- src/async_engine.cpp:12-117 (same
+//                                      error strings: part of the exception
+//                                      contract)
+// Fixtures and the mini-batch schedule go through libstdc++ <random> exactly
+// as the reference does, which makes them bit-identical to it (checked in
+// tests/test_host.py). None of this is on the CUDA hot path.
 #include <algorithm>
 #include <charconv>
 #include <chrono>
