@@ -13,8 +13,11 @@ examples/sec per epoch (N / t_epoch); at N GPUs every rank owns
 its own rcv1-shaped shard (seed + rank; weak scaling) and the fp64 gradient is
 SUM-all-reduced every epoch by the engine's own NCCL communicator, so the
 whole-job value is N * 677,399 / t_epoch. The stored data (397 MB CSR + 300 MB
-blocked CSC) exceeds L2; L2 is flushed (256 MiB memset) before every timed
-epoch anyway, outside the event window.
+blocked CSC) exceeds L2; L2 is flushed before every timed epoch anyway,
+outside the event window: 256 MiB written, then read back, so the epoch starts
+from a cold and CLEAN L2 (a write-only flush leaves 126 MB of dirty lines whose
+write-back the next epoch's first kernel would pay: +14 us on rcv1,
+profiles/round2_flush_modes.jsonl).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
@@ -78,6 +81,21 @@ def _ncu_traffic(kernel, summary="round2_ncu_rcv1_full_batch.txt"):
     if cur and kernel in cur and len(got) == 2:
         return int(sum(got.values())), os.path.relpath(path, ROOT)
     return None, None
+
+
+class L2Flush:
+    """Between-step L2 flush: write 256 MiB (2x L2), then read it back so the
+    next step starts cold AND clean (no dirty lines left for its first kernel
+    to write back). Runs on torch's current stream, outside the event window."""
+
+    def __init__(self):
+        import torch
+        self.buf = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+        self.sink = torch.empty((), dtype=torch.float32, device="cuda")
+
+    def __call__(self):
+        self.buf.zero_()
+        self.sink.copy_(self.buf.sum())
 
 
 def _peaks():
@@ -232,7 +250,7 @@ def run_ours(args):
     dds = S.DeviceDataset(dev, host, row_base=rank * N_EX, n_global=n_global)
     model = S.DeviceModel(dev, D)
     task = S.Task.LR
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush()
 
     def step(ds=dds):
         S.sync_epoch(ds, model, task, ALPHA, None, n_global, check_finite=False)
@@ -243,7 +261,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        flush.zero_()
+        flush()
         step()
     barrier()
     launches0 = dev.launch_count()
@@ -253,7 +271,7 @@ def run_ours(args):
         barrier()
         t_wall0 = time.perf_counter()
         for i in range(args.steps):
-            flush.zero_()  # L2 flush, outside the event window
+            flush()  # L2 flush, outside the event window
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
@@ -272,7 +290,7 @@ def run_ours(args):
     # Per-kernel CUDA-event times on the launching stream (the library's profiler).
     dev.set_profiling(True)
     for _ in range(args.steps):
-        flush.zero_()
+        flush()
         step()
     stats = dev.kernel_stats()
     dev.set_profiling(False)
@@ -304,7 +322,7 @@ def run_ours(args):
                    "alpha": ALPHA, "n_per_gpu": N_EX, "d": D, "nnz_per_gpu": nnz,
                    "parallelism": f"dp{world}: row shards, fp64 gradient all-reduced in-engine (NCCL)",
                    "l2": "inputs (697 MB) larger than L2, and L2 flushed before every step "
-                         "(256 MiB memset, outside the event window)"},
+                         "(256 MiB written then read back: cold, clean L2; outside the event window)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": name, "kernel_ms": kern_ms, "kernel_share_of_step": share,
@@ -412,7 +430,7 @@ def _time_sync(S, dds, model, task, alpha, batch, epochs, warmup, flush, order=N
         S.sync_epoch(dds, model, task, alpha, order, batch)
     evs = []
     for _ in range(epochs):
-        flush.zero_()
+        flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         S.sync_epoch(dds, model, task, alpha, order, batch, check_finite=False)
@@ -429,7 +447,7 @@ def _time_hogwild(S, dds, model, task, alpha, plan, epochs, warmup, flush):
         S.hogwild_epoch(dds, model, task, alpha, plan)
     evs = []
     for _ in range(epochs):
-        flush.zero_()
+        flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         S.hogwild_epoch(dds, model, task, alpha, plan)
@@ -452,7 +470,7 @@ def extra_c5(S, dev, world, rank, rows_per_gpu, barrier):
                                          n_global=n_global)
     model = S.DeviceModel(dev, d)
     barrier()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush()
     dev.set_profiling(True)
     ms = _time_sync(S, dds, model, S.Task.LR, 1e-9, n_global, 5, 2, flush)
     stats = dev.kernel_stats()
@@ -483,7 +501,7 @@ def extra_shapes(S, dev):
     and Hogwild epochs with the paper's plans (every resident lane group a
     worker). Context for the headline, not headline numbers."""
     import torch
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush()
     peak, _ = _peaks()
     shapes = {
         # name: (make, task, sync alpha (B = N), hogwild plan, hogwild alpha)
@@ -546,7 +564,7 @@ def extra_exact(S, dev, host):
     import torch
     dds = S.DeviceDataset(dev, host, exact=True)
     model = S.DeviceModel(dev, D)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush()
     ms = _time_sync(S, dds, model, S.Task.LR, ALPHA, N_EX, 3, 1, flush)
     out = {"epoch_ms": ms, "value": N_EX / (ms / 1e3), "unit": UNIT,
            "note": "sgdb_dataset_upload_ex(SGDB_UPLOAD_EXACT_FP64): matvec / coefficient / "

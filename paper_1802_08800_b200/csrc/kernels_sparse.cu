@@ -7,8 +7,8 @@
 //   K3s  gradient pass c = coef(z, y), g = X^T c, w -= alpha g (row-blocked CSC stream)
 //
 // Both passes are one segmented stream over a CTA's contiguous range of
-// nonzeros: each warp walks its share in 128-slot tiles (lane l holds slots
-// 4l..4l+3 of a tile: one float4 of values + 4 ids), multiplies with the
+// nonzeros: each warp walks its share in 256-slot tiles (lane l holds slots
+// 8l..8l+7 of a tile: one 256-bit load of values + 8 ids), multiplies with the
 // staged operand (the model, or the row block's coefficient slice, in SMEM),
 // and recovers the per-segment sums (rows, or (block, column) segments) with
 // a segmented warp scan. Segment boundaries come from a HEAD BITMAP (bit s =
@@ -199,7 +199,7 @@ struct CtaScratch {
 };
 
 // The CTA's slots [S0, S1) (S0 a segment start, S1 the next CTA's start):
-// split evenly over the warps (4-slot aligned), streamed, and the segments
+// split evenly over the warps (E-slot aligned), streamed, and the segments
 // cut between warps finished in slot order. emit(X, z) receives every
 // complete segment once.
 // emit(X, z) receives the segments the warps complete inside their streams
@@ -302,23 +302,30 @@ __global__ void __launch_bounds__(kNT, 1)
   extern __shared__ __align__(16) float ws[];
   __shared__ CtaScratch sc;
   __shared__ uint64_t bar;
-  // PDL: launched while the previous step drains; the model (and the
-  // coefficients this pass overwrites) belong to it, so wait first.
-  pdl_wait();
+  // PDL: launched while the previous step drains. The CSR stream is static
+  // data, so every warp issues its first tiles' loads at once; only the model
+  // (and the coefficients this pass overwrites) belong to the previous step:
+  // thread 0 waits for it before bulk-copying the model, and the first
+  // product of every warp waits for that copy (or, with the model in global
+  // memory, for the previous step itself). Coefficient writes all come after
+  // a warp's first product, hence after the wait.
   pdl_launch_dependents();
   if (SMEMW && threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
+  }
+  __syncthreads();
+  if (SMEMW && threadIdx.x == 0) {
+    pdl_wait();
     const uint32_t total = round_up16(uint64_t(d + 1) * 4);  // w32 holds whole 16-byte groups
     mbar_arrive_expect_tx(&bar, total);
     for (uint32_t off = 0; off < total; off += 32768)
       bulk_g2s(reinterpret_cast<char*>(ws) + off, reinterpret_cast<const char*>(w32) + off,
                min(32768u, total - off), &bar);
   }
-  __syncthreads();
   const uint32_t S0 = __ldg(cta_slot + blockIdx.x), S1 = __ldg(cta_slot + blockIdx.x + 1);
   const float* w = SMEMW ? ws : w32;
-  bool ready = !SMEMW;  // the first tiles' loads overlap the model's bulk copy
+  bool ready = false;  // the first tiles' loads overlap the wait and the model's bulk copy
   using Win = std::conditional_t<I16, WinR16, WinR32>;
   cta_segments<kE, 2, Win>(
       S0, S1, bm, bpre,
@@ -334,8 +341,9 @@ __global__ void __launch_bounds__(kNT, 1)
         return q;
       },
       [&](const Win& q, float* p) {
-        if (SMEMW && !ready) {
-          mbar_wait(&bar, 0);
+        if (!ready) {
+          if (SMEMW) mbar_wait(&bar, 0);
+          else pdl_wait();
           ready = true;
         }
         uint32_t j[8];
@@ -378,6 +386,7 @@ __global__ void __launch_bounds__(kNT, 1)
       },
       sc);
   if (SMEMW && !ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
+  if (!SMEMW && !ready) pdl_wait();  // no early exit past the previous step
 }
 
 struct ApplyArgs {
@@ -412,22 +421,29 @@ __global__ void __launch_bounds__(kNT, 1)
   __shared__ uint64_t bar;
   const uint32_t b = blockIdx.x / cpb, k = blockIdx.x % cpb;
   const uint32_t r0 = b * rb, rows = min(rb, n - r0);  // rb % 4 == 0: 16-byte aligned slice
-  pdl_wait();  // the coefficients come from the margin pass
+  // PDL: the CSC stream is static, so the first tiles' loads go out while
+  // the margin pass drains; thread 0 waits for it before bulk-copying the
+  // coefficient slice, and every warp's first product waits for that copy.
   pdl_launch_dependents();
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
+  }
+  const uint32_t j0 = __ldg(cta_col + k), j1 = __ldg(cta_col + k + 1);
+  const uint64_t q0 = uint64_t(b) * d;
+  if (seg_of_ord) {  // empty (block, column) segments are never emitted: zero them first
+    pdl_wait();      // (the previous step's apply may still read part)
+    for (uint32_t j = j0 + threadIdx.x; j < j1; j += kNT) part[q0 + j] = 0.f;
+  }
+  __syncthreads();  // the barrier init is visible to every waiter
+  if (threadIdx.x == 0) {
+    pdl_wait();  // the coefficients come from the margin pass
     const uint32_t total = round_up16(uint64_t(rows) * 4);  // coef carries 16-byte slack
     mbar_arrive_expect_tx(&bar, total);
     for (uint32_t off = 0; off < total; off += 32768)
       bulk_g2s(reinterpret_cast<char*>(cs) + off, reinterpret_cast<const char*>(coef + r0) + off,
                min(32768u, total - off), &bar);
   }
-  const uint32_t j0 = __ldg(cta_col + k), j1 = __ldg(cta_col + k + 1);
-  const uint64_t q0 = uint64_t(b) * d;
-  if (seg_of_ord)  // empty (block, column) segments are never emitted: zero them first
-    for (uint32_t j = j0 + threadIdx.x; j < j1; j += kNT) part[q0 + j] = 0.f;
-  __syncthreads();  // the barrier init is visible to every waiter
   const uint32_t S0 = __ldg(segptr + q0 + j0), S1 = __ldg(segptr + q0 + j1);
   bool ready = false;  // the first tiles' loads overlap the slice's bulk copy
   cta_segments<kE, 2, WinC>(
@@ -677,12 +693,18 @@ void compaction(Ctx& c, const uint32_t* flag, uint64_t count, DBuf<uint32_t>& ma
 // Row-block geometry: blocks of at most 49,152 rows (u16 ids, <= 192 KB
 // slice), and as many CTAs (blocks x column ranges) as SMs, one per SM.
 void choose_blocks(const Ctx& c, uint64_t n, uint32_t& rb, uint32_t& nblk, uint32_t& cpb) {
-  // The fewest blocks of at most 49,152 rows (16-bit ids, <= 192 KB slice):
-  // more blocks shrink the staged slices but add nblk * d partial sums to the
-  // apply; measured on rcv1 (14 vs 37 blocks: 139-142 vs 141-142 us) and
-  // real-sim / w8a (2 vs 16 / 126 blocks: 37 vs 41 us, 27 vs 35 us).
-  const uint64_t nb = std::max<uint64_t>(1, (n + kMaxRowBlock - 1) / kMaxRowBlock);
+  // Blocks of at most 49,152 rows (16-bit ids, <= 192 KB slice). From the
+  // fewest such blocks up to twice as many, the count whose grid
+  // nblk * floor(SMs / nblk) leaves the fewest SMs idle (ties: fewer blocks —
+  // more blocks add nblk * d partial sums to the apply). rcv1: 21 blocks x 7
+  // column ranges = 147 CTAs instead of 14 x 10 = 140.
+  const uint64_t nb0 = std::max<uint64_t>(1, (n + kMaxRowBlock - 1) / kMaxRowBlock);
   const uint64_t sms = static_cast<uint64_t>(std::max(1, c.num_sms));
+  uint64_t nb = nb0, best = 0;
+  for (uint64_t k = nb0; k <= std::min<uint64_t>(2 * nb0, sms); ++k) {
+    const uint64_t used = k * (sms / k);
+    if (used > best) best = used, nb = k;
+  }
   // rb % 8 == 0 keeps every coefficient slice 32-byte aligned (bulk copies).
   rb = static_cast<uint32_t>(std::max<uint64_t>(8, ((n + nb - 1) / nb + 7) & ~uint64_t(7)));
   nblk = static_cast<uint32_t>(std::max<uint64_t>(1, (n + rb - 1) / rb));
@@ -807,6 +829,10 @@ void sparse_prep(Dataset& ds) {
 }
 
 void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a) {
+  // K2s issues its first CSR loads before its PDL wait, so it may overlap its
+  // predecessor only when that predecessor cannot be writing the CSR-derived
+  // structures, i.e. not right after they were (re)built.
+  const bool rebuilt = !ds.sparse_ready;
   sparse_prep(ds);
   Ctx& c = *ds.ctx;
   if (ds.n == 0) return;
@@ -830,7 +856,7 @@ void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a) {
       cfg.dynamicSmemBytes = smem;
       cfg.stream = c.stream;
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = rebuilt ? 0 : 1;
       check(cudaLaunchKernelEx(&cfg, kern, static_cast<const float*>(ds.val.p),
                                I16 ? static_cast<const void*>(ds.cidx16.p) : static_cast<const void*>(ds.idx.p),
                                static_cast<const uint32_t*>(ds.rbm.p), static_cast<const uint32_t*>(ds.rbm_pre.p),

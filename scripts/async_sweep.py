@@ -60,7 +60,7 @@ def main():
                 S.hogwild_epoch(dds, model, task, alpha, plan)
             evs = []
             for _ in range(10):
-                flush.zero_()
+                flush.zero_(); flush.view(torch.float32).sum()  # clean L2: written, then read
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
                 S.hogwild_epoch(dds, model, task, alpha, plan)
@@ -69,7 +69,7 @@ def main():
             torch.cuda.synchronize()
             ms = float(np.median([x.elapsed_time(y) for x, y in evs]))
             dev.set_profiling(True)
-            flush.zero_()
+            flush.zero_(); flush.view(torch.float32).sum()  # clean L2: written, then read
             S.hogwild_epoch(dds, model, task, alpha, plan)
             stats = dev.kernel_stats()
             dev.set_profiling(False)

@@ -35,7 +35,7 @@ def main():
             model = S.DeviceModel(dev, host.n_features)
             times = []
             for i in range(8):
-                flush.zero_()
+                flush.zero_(); flush.view(torch.float32).sum()  # clean L2: written, then read
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
                 S.sync_epoch(dds, model, task, 1e-7, order, B)

@@ -45,7 +45,7 @@ def main():
             order = sched.next()
             evs = []
             for i in range(8):
-                flush.zero_()
+                flush.zero_(); flush.view(torch.float32).sum()  # clean L2: written, then read
                 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ev0.record(stream)
                 S.sync_epoch(dds, model, task, alpha, order if b < n else None, b, check_finite=False)
@@ -55,7 +55,7 @@ def main():
             times = [e0.elapsed_time(e1) for e0, e1 in evs]
             dev.set_profiling(True)
             for i in range(3):
-                flush.zero_()
+                flush.zero_(); flush.view(torch.float32).sum()  # clean L2: written, then read
                 S.sync_epoch(dds, model, task, alpha, order if b < n else None, b)
             stats = dev.kernel_stats()
             dev.set_profiling(False)
