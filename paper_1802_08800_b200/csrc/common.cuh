@@ -91,6 +91,15 @@ __device__ __forceinline__ void st_model(float* p, float v) { __stcg(p, v); }
 // may start while its predecessor drains: it issues the loads that do not
 // depend on the predecessor first, then waits here (griddepcontrol.wait:
 // the predecessor grid has completed and its writes are visible).
+// Arrival on a gpu-scope counter with acquire-release semantics: after a CTA
+// barrier the CTA's prior writes are ordered before it (release is
+// cumulative), and the arriving thread sees every earlier arrival's writes.
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

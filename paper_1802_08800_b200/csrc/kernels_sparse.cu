@@ -472,8 +472,7 @@ __global__ void __launch_bounds__(kNT, 1)
   __syncthreads();
   const unsigned target = gen * nblk;
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned t = atomicAdd(tickets + k, 1u) + 1u;
+    const unsigned t = atom_add_acq_rel_gpu(tickets + k, 1u) + 1u;
     sc.last = t == target;
     if (coop)
       while (ld_acquire_gpu(tickets + k) < target) __nanosleep(32);

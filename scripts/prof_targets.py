@@ -2,7 +2,7 @@
 
     python scripts/prof_targets.py {hogwild_w8a|hogwild_rcv1_block|hogwild_rcv1_block8|hogwild_w8a_example|
                                     sync_covtype|sync_rcv1|sync_realsim|sync_news20|sync_dense1000|sync_c5|
-                                    minibatch_covtype|minibatch_rcv1} [epochs]
+                                    minibatch_covtype|minibatch_rcv1|minibatch_w8a} [epochs]
 """
 import os
 import sys
@@ -48,9 +48,11 @@ def main():
         for _ in range(epochs):
             flush.zero_()
             S.hogwild_epoch(dds, model, S.Task.SVM, 0.01, plan)
-    elif target in ("minibatch_covtype", "minibatch_rcv1"):
+    elif target in ("minibatch_covtype", "minibatch_rcv1", "minibatch_w8a"):
         if target.endswith("covtype"):
             host, task, alpha = S.fixtures.dense_classification(581012, 54, 20250810), S.Task.LR, 1e-3
+        elif target.endswith("w8a"):
+            host, task, alpha = S.fixtures.sparse_classification(64700, 300, 11.65, 20250811), S.Task.SVM, 1e-3
         else:
             host, task, alpha = S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813), S.Task.LR, 1e-2
         dds = S.DeviceDataset(dev, host)
