@@ -292,7 +292,7 @@ constexpr int kE = 8;
 // between warps) get their coefficient directly. One CTA per SM; the fp32 model is bulk-copied (1-D
 // TMA) into SMEM when it fits (SMEMW), else gathered through L1/L2. I16:
 // 16-bit column ids (d <= 65536).
-template <int TASK, bool SMEMW, bool I16>
+template <int TASK, bool SMEMW, bool I16, bool RMAP>  // RMAP: empty rows, ordinals map through row_of_ord
 __global__ void __launch_bounds__(kNT, 1)
     k2s_margin_kernel(const float* __restrict__ val, const void* __restrict__ idx,
                       const uint32_t* __restrict__ bm, const uint32_t* __restrict__ bpre,
@@ -358,9 +358,9 @@ __global__ void __launch_bounds__(kNT, 1)
 #pragma unroll
         for (int u = 0; u < 8; ++u) p[u] = x[u] * (SMEMW ? w[j[u]] : __ldg(w + j[u]));
       },
-      [&](int32_t X, float z) { coef[row_of_ord ? __ldg(row_of_ord + X) : static_cast<uint32_t>(X)] = z; },
+      [&](int32_t X, float z) { coef[RMAP ? __ldg(row_of_ord + X) : static_cast<uint32_t>(X)] = z; },
       [&](int32_t X, float z) {
-        const uint32_t r = row_of_ord ? __ldg(row_of_ord + X) : static_cast<uint32_t>(X);
+        const uint32_t r = RMAP ? __ldg(row_of_ord + X) : static_cast<uint32_t>(X);
         coef[r] = coef_fast<TASK>(z, __ldg(y + r));
       },
       [&](int32_t lo, int32_t hi) {
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kNT, 1)
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int32_t o = o0 + 32 * i;
-            r[i] = o < hi ? (row_of_ord ? __ldg(row_of_ord + o) : static_cast<uint32_t>(o)) : 0u;
+            r[i] = o < hi ? (RMAP ? __ldg(row_of_ord + o) : static_cast<uint32_t>(o)) : 0u;
           }
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -408,6 +408,7 @@ struct ApplyArgs {
 // so every CTA is resident once the margin pass drains and the arrival wait
 // cannot deadlock); otherwise the last CTA to arrive applies the whole range. Arrival tickets count up by nblk per launch
 // (gen = launch number), so they are never reset.
+template <bool SMAP>  // some (block, column) segments are empty: ordinals map through seg_of_ord
 __global__ void __launch_bounds__(kNT, 1)
     k3s_grad_kernel(const float* __restrict__ cval, const uint16_t* __restrict__ crow,
                     const uint32_t* __restrict__ bm, const uint32_t* __restrict__ bpre,
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(kNT, 1)
   }
   const uint32_t j0 = __ldg(cta_col + k), j1 = __ldg(cta_col + k + 1);
   const uint64_t q0 = uint64_t(b) * d;
-  if (seg_of_ord) {  // empty (block, column) segments are never emitted: zero them first
+  if (SMAP) {  // empty (block, column) segments are never emitted: zero them first
     pdl_wait();      // (the previous step's apply may still read part)
     for (uint32_t j = j0 + threadIdx.x; j < j1; j += kNT) part[q0 + j] = 0.f;
   }
@@ -464,8 +465,8 @@ __global__ void __launch_bounds__(kNT, 1)
         p[4] = q.v1.x * cs[q.r.z & 0xffffu], p[5] = q.v1.y * cs[q.r.z >> 16];
         p[6] = q.v1.z * cs[q.r.w & 0xffffu], p[7] = q.v1.w * cs[q.r.w >> 16];
       },
-      [&](int32_t X, float z) { part[seg_of_ord ? __ldg(seg_of_ord + X) : static_cast<uint32_t>(X)] = z; },
-      [&](int32_t X, float z) { part[seg_of_ord ? __ldg(seg_of_ord + X) : static_cast<uint32_t>(X)] = z; },
+      [&](int32_t X, float z) { part[SMAP ? __ldg(seg_of_ord + X) : static_cast<uint32_t>(X)] = z; },
+      [&](int32_t X, float z) { part[SMAP ? __ldg(seg_of_ord + X) : static_cast<uint32_t>(X)] = z; },
       [&](int32_t, int32_t) {},
       sc);
   if (!ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
@@ -842,7 +843,10 @@ void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a) {
     const bool smemw = model_bytes + sizeof(CtaScratch) + 64 <= c.max_smem_optin;
     const bool i16 = ds.cidx16.p != nullptr;
     auto go = [&]<bool SW, bool I16>() {
-      auto kern = a.task == kTaskLR ? k2s_margin_kernel<kTaskLR, SW, I16> : k2s_margin_kernel<kTaskSVM, SW, I16>;
+      auto kern = a.task == kTaskLR
+                      ? (ds.rows_empty ? k2s_margin_kernel<kTaskLR, SW, I16, true> : k2s_margin_kernel<kTaskLR, SW, I16, false>)
+                      : (ds.rows_empty ? k2s_margin_kernel<kTaskSVM, SW, I16, true>
+                                       : k2s_margin_kernel<kTaskSVM, SW, I16, false>);
       const size_t smem = SW ? model_bytes : 0;
       set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(k2s)");
       prof_begin(c, "k2s_margin_kernel");
@@ -875,7 +879,7 @@ void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a) {
   {
     m.part32.alloc(uint64_t(ds.csc_nblk) * d + 1);
     const size_t smem = round_up16(uint64_t(ds.csc_rb) * 4);
-    auto kern = k3s_grad_kernel;
+    auto kern = ds.segs_empty ? k3s_grad_kernel<true> : k3s_grad_kernel<false>;
     set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(k3s)");
     ApplyArgs aa{a.alpha, a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p, m.finite.p, m.scal.p};
     const unsigned grid = ds.csc_nblk * ds.csc_cpb;
