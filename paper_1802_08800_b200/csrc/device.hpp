@@ -101,6 +101,25 @@ size_t static_smem_of(const void* kern);
 // Device storage kind chosen at upload.
 enum class Kind { Dense, Csr };
 
+// A blocked, segmented copy of the nonzeros (kernels_sparse.cu). The major
+// dimension (rows for the gradient pass's CSC, columns for the wide margin
+// pass) is split into nblk blocks of rb (< 2^16, % 8 == 0) entries; segment
+// (b, m) = block b's entries of minor index m, at segptr[b*nminor + m] ..
+// segptr[b*nminor + m + 1], stored as fp32 values + 16-bit block-local major
+// ids in (block, minor, major) order; its head bitmap (bit s = slot s starts
+// a non-empty segment) + word prefix; seg_of_ord when some segments are
+// empty; cpb nnz-balanced minor ranges (cta) shared by all blocks; arrival
+// tickets (monotonic: gen launches since they were zeroed).
+struct Blocked {
+  uint32_t rb = 0, nblk = 0, cpb = 0;
+  DBuf<float> val;
+  DBuf<uint16_t> id;
+  DBuf<uint32_t> segptr, bm, bm_pre, seg_of_ord, cta;
+  bool segs_empty = false;
+  DBuf<unsigned> tickets;
+  unsigned gen = 0;
+};
+
 struct Dataset {
   Ctx* ctx = nullptr;
   uint64_t uid = 0;  // unique per upload (keys cached epoch graphs)
@@ -126,25 +145,19 @@ struct Dataset {
   //    non-empty row's ordinal to its row id when some rows are empty;
   //  * 16-bit column ids (d <= 65536) for the margin pass;
   //  * margin-pass CTA ranges (cta_n CTAs, each starting at a row start);
-  //  * the row-blocked CSC: rows split into csc_nblk blocks of csc_rb
-  //    (< 2^16, % 4 == 0) rows, segment (b, j) = block b's entries of column
-  //    j at segptr[b*d + j] .. segptr[b*d + j + 1], 16-bit block-local rows;
-  //    its head bitmap / prefix (cbm, cbm_pre), seg_of_ord when some segments
-  //    are empty, csc_cpb nnz-balanced column ranges (cta_col) shared by all
-  //    blocks, and their arrival tickets.
+  //  * the row-blocked CSC of the gradient pass (csc) and, for models too
+  //    large for shared memory, the column-blocked CSR of the margin pass
+  //    (wide; see Blocked).
   bool sparse_ready = false;
   DBuf<uint32_t> rbm, rbm_pre, row_of_ord;
   bool rows_empty = false;
   DBuf<uint16_t> cidx16;
   uint32_t cta_n = 0;
   DBuf<uint32_t> cta_slot;
-  uint32_t csc_rb = 0, csc_nblk = 0, csc_cpb = 0;
-  DBuf<float> cval;
-  DBuf<uint16_t> crow;
-  DBuf<uint32_t> segptr, cbm, cbm_pre, seg_of_ord, cta_col;
-  bool segs_empty = false;
-  DBuf<unsigned> sparse_tickets;
-  unsigned sparse_gen = 0;  // K3s launches since the tickets were zeroed
+  Blocked csc;       // major = rows, minor = columns
+  bool wide = false;  // margin pass over `wmajor` below instead of the CSR stream
+  Blocked wmajor;    // major = columns, minor = rows
+  DBuf<float> mpart;  // wmajor.nblk * n partial margins
   // sparse_prep's scratch, kept so a rebuild after every refresh (bench
   // e2e) neither allocates nor frees (cudaFree synchronises the device).
   struct {

@@ -3,8 +3,9 @@
 // (proj/src/sync_engine.cpp:22-42 -> linalg::matvec, the LR/SVM coefficient,
 // linalg::matvec_transposed; proj/src/linalg.cpp:30-109, glm.cpp:30-34).
 //
-//   K2s  margin pass   z = X w                                (CSR stream)
-//   K3s  gradient pass c = coef(z, y), g = X^T c, w -= alpha g (row-blocked CSC stream)
+//   K2s  margin pass   z = X w, c = coef(z, y)                (CSR stream, model in SMEM)
+//   K2w  margin pass of a model too large for SMEM                (column-blocked CSR stream)
+//   K3s  gradient pass g = X^T c, w -= alpha g                    (row-blocked CSC stream)
 //
 // Both passes are one segmented stream over a CTA's contiguous range of
 // nonzeros: each warp walks its share in 256-slot tiles (lane l holds slots
@@ -26,8 +27,12 @@
 // blocks in block order and applies the update: deterministic, no atomics on
 // data, no grid barrier, any grid size.
 //
-// The row-blocked CSC (16-bit block-local row ids) is built on the device by a
-// stable radix sort of (block, column) keys, at upload and after a refresh.
+// K2w and K3s are the same blocked pass (blocked_pass_kernel) over a blocked
+// copy of the nonzeros with 16-bit block-local major ids (Blocked in
+// device.hpp): rows blocked for K3s (operand slice: the coefficients),
+// columns blocked for K2w (operand slice: the model). Both copies are built
+// on the device by a stable radix sort of (block, minor) keys, at upload and
+// after a refresh.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -270,10 +275,6 @@ __device__ __forceinline__ void cta_segments(uint32_t S0, uint32_t S1, const uin
 }
 
 // E = 8 slots per lane: two float4 of values + eight ids.
-struct WinR32 {
-  float4 v0, v1;
-  uint4 j0, j1;
-};
 struct WinR16 {
   float4 v0, v1;
   uint4 j;  // eight u16
@@ -289,12 +290,13 @@ constexpr int kE = 8;
 // then turns its own (consecutive) rows into coefficients with coalesced
 // label loads while the CTA's other warps still stream — no label load on
 // the stream's emission path; rows finished after the CTA barrier (cut
-// between warps) get their coefficient directly. One CTA per SM; the fp32 model is bulk-copied (1-D
-// TMA) into SMEM when it fits (SMEMW), else gathered through L1/L2. I16:
-// 16-bit column ids (d <= 65536).
-template <int TASK, bool SMEMW, bool I16, bool RMAP>  // RMAP: empty rows, ordinals map through row_of_ord
+// between warps) get their coefficient directly. One CTA per SM; the fp32
+// model is bulk-copied (1-D TMA) into SMEM (models too large for SMEM take
+// the column-blocked margin pass K2w instead, so d < 65,536 here and the
+// column ids are 16-bit).
+template <int TASK, bool RMAP>  // RMAP: empty rows, ordinals map through row_of_ord
 __global__ void __launch_bounds__(kNT, 1)
-    k2s_margin_kernel(const float* __restrict__ val, const void* __restrict__ idx,
+    k2s_margin_kernel(const float* __restrict__ val, const uint16_t* __restrict__ idx,
                       const uint32_t* __restrict__ bm, const uint32_t* __restrict__ bpre,
                       const uint32_t* __restrict__ cta_slot, const uint32_t* __restrict__ row_of_ord,
                       const float* __restrict__ y, uint32_t n, const float* __restrict__ w32, uint32_t d,
@@ -310,12 +312,12 @@ __global__ void __launch_bounds__(kNT, 1)
   // memory, for the previous step itself). Coefficient writes all come after
   // a warp's first product, hence after the wait.
   pdl_launch_dependents();
-  if (SMEMW && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (SMEMW && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     pdl_wait();
     const uint32_t total = round_up16(uint64_t(d + 1) * 4);  // w32 holds whole 16-byte groups
     mbar_arrive_expect_tx(&bar, total);
@@ -324,39 +326,27 @@ __global__ void __launch_bounds__(kNT, 1)
                min(32768u, total - off), &bar);
   }
   const uint32_t S0 = __ldg(cta_slot + blockIdx.x), S1 = __ldg(cta_slot + blockIdx.x + 1);
-  const float* w = SMEMW ? ws : w32;
   bool ready = false;  // the first tiles' loads overlap the wait and the model's bulk copy
-  using Win = std::conditional_t<I16, WinR16, WinR32>;
+  using Win = WinR16;
   cta_segments<kE, 2, Win>(
       S0, S1, bm, bpre,
       [&](uint32_t s) {
         Win q;
         ldg256(val + s, q.v0, q.v1);
-        if constexpr (I16) {
-          q.j = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(idx) + s));
-        } else {
-          q.j0 = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(idx) + s));
-          q.j1 = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(idx) + s + 4));
-        }
+        q.j = __ldg(reinterpret_cast<const uint4*>(idx + s));
         return q;
       },
       [&](const Win& q, float* p) {
         if (!ready) {
-          if (SMEMW) mbar_wait(&bar, 0);
-          else pdl_wait();
+          mbar_wait(&bar, 0);
           ready = true;
         }
         uint32_t j[8];
-        if constexpr (I16) {
-          j[0] = q.j.x & 0xffffu, j[1] = q.j.x >> 16, j[2] = q.j.y & 0xffffu, j[3] = q.j.y >> 16;
-          j[4] = q.j.z & 0xffffu, j[5] = q.j.z >> 16, j[6] = q.j.w & 0xffffu, j[7] = q.j.w >> 16;
-        } else {
-          j[0] = q.j0.x, j[1] = q.j0.y, j[2] = q.j0.z, j[3] = q.j0.w;
-          j[4] = q.j1.x, j[5] = q.j1.y, j[6] = q.j1.z, j[7] = q.j1.w;
-        }
+        j[0] = q.j.x & 0xffffu, j[1] = q.j.x >> 16, j[2] = q.j.y & 0xffffu, j[3] = q.j.y >> 16;
+        j[4] = q.j.z & 0xffffu, j[5] = q.j.z >> 16, j[6] = q.j.w & 0xffffu, j[7] = q.j.w >> 16;
         const float x[8] = {q.v0.x, q.v0.y, q.v0.z, q.v0.w, q.v1.x, q.v1.y, q.v1.z, q.v1.w};
 #pragma unroll
-        for (int u = 0; u < 8; ++u) p[u] = x[u] * (SMEMW ? w[j[u]] : __ldg(w + j[u]));
+        for (int u = 0; u < 8; ++u) p[u] = x[u] * ws[j[u]];
       },
       [&](int32_t X, float z) { coef[RMAP ? __ldg(row_of_ord + X) : static_cast<uint32_t>(X)] = z; },
       [&](int32_t X, float z) {
@@ -385,8 +375,7 @@ __global__ void __launch_bounds__(kNT, 1)
         }
       },
       sc);
-  if (SMEMW && !ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
-  if (!SMEMW && !ready) pdl_wait();  // no early exit past the previous step
+  if (!ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
 }
 
 struct ApplyArgs {
@@ -399,90 +388,114 @@ struct ApplyArgs {
   double* norm2;
 };
 
-// K3s: CTA (row block b, column range k) bulk-copies the block's coefficient
-// slice into SMEM, streams the block's segments of columns
-// [cta_col[k], cta_col[k+1]) against it, writing fp32 per-(block, column)
-// sums; then g_j = sum over blocks (fixed block order, fp64) and w -= a g.
-// The apply is spread over the nblk CTAs of the column range once all of
-// them have arrived (coop: at most one CTA per SM and no more CTAs than SMs,
-// so every CTA is resident once the margin pass drains and the arrival wait
-// cannot deadlock); otherwise the last CTA to arrive applies the whole range. Arrival tickets count up by nblk per launch
-// (gen = launch number), so they are never reset.
-template <bool SMAP>  // some (block, column) segments are empty: ordinals map through seg_of_ord
-__global__ void __launch_bounds__(kNT, 1)
-    k3s_grad_kernel(const float* __restrict__ cval, const uint16_t* __restrict__ crow,
-                    const uint32_t* __restrict__ bm, const uint32_t* __restrict__ bpre,
-                    const uint32_t* __restrict__ segptr, const uint32_t* __restrict__ cta_col,
-                    uint32_t cpb, uint32_t nblk, uint32_t d, uint32_t rb, uint32_t n,
-                    const float* __restrict__ coef, const uint32_t* __restrict__ seg_of_ord,
-                    float* __restrict__ part, unsigned* __restrict__ tickets, ApplyArgs aa,
-                    unsigned gen, int coop) {
+struct PassArgs {
+  const float* val;
+  const uint16_t* id;
+  const uint32_t* bm;
+  const uint32_t* bpre;
+  const uint32_t* segptr;
+  const uint32_t* cta;
+  uint32_t cpb, nblk, nminor, rb, nmajor;
+  const float* slice;           // gradient: the coefficients; margin: the fp32 model
+  const uint32_t* seg_of_ord;   // SMAP only
+  float* part;                  // nblk * nminor partial sums
+  unsigned* tickets;
+  unsigned gen;
+  int coop;
+  ApplyArgs aa;                 // gradient pass: the update
+  const float* y;               // margin pass: labels -> coefficients
+  float* coef;
+};
+
+constexpr int kPassGrad = 0;
+constexpr int kPassMargin = 1;
+
+// One blocked segmented pass (Blocked in device.hpp). CTA (major block b,
+// minor range k) bulk-copies the block's slice of the operand into SMEM
+// (gradient pass: the coefficients of rows [b*rb, ..); margin pass of a wide
+// model: the model's columns [b*rb, ..)), streams the block's segments of
+// minor indices [cta[k], cta[k+1]) against it and writes fp32
+// per-(block, minor) sums. Then, per minor index, the sum over blocks in
+// fixed block order (fp64):
+//   K3s, gradient pass: g_j, w -= alpha g (or g64 = g), finite flag, |g|^2;
+//   K2w, margin pass:   z_i, coef_i = coef(z_i, y_i) (glm.cpp:30-34).
+// The finish is spread over the minor range's nblk CTAs once all of them
+// have arrived (coop: at most one CTA per SM and no more CTAs than SMs, so
+// every CTA is resident once the previous pass drains and the arrival wait
+// cannot deadlock); otherwise the last CTA to arrive finishes the whole
+// range. Arrival tickets count up by nblk per launch (gen = launch number),
+// so they are never reset. SMAP: some segments are empty, ordinals map
+// through seg_of_ord (and the range's partials are zeroed first).
+template <int MODE, int TASK, bool SMAP>
+__global__ void __launch_bounds__(kNT, 1) blocked_pass_kernel(PassArgs p) {
   extern __shared__ __align__(16) float cs[];
   __shared__ CtaScratch sc;
   __shared__ uint64_t bar;
-  const uint32_t b = blockIdx.x / cpb, k = blockIdx.x % cpb;
-  const uint32_t r0 = b * rb, rows = min(rb, n - r0);  // rb % 4 == 0: 16-byte aligned slice
-  // PDL: the CSC stream is static, so the first tiles' loads go out while
-  // the margin pass drains; thread 0 waits for it before bulk-copying the
-  // coefficient slice, and every warp's first product waits for that copy.
+  const uint32_t b = blockIdx.x / p.cpb, k = blockIdx.x % p.cpb;
+  const uint32_t r0 = b * p.rb, len = min(p.rb, p.nmajor - r0);  // rb % 8 == 0: 32-byte aligned slice
+  // PDL: the blocked stream is static, so the first tiles' loads go out
+  // while the previous pass drains; thread 0 waits for it before
+  // bulk-copying the slice, and every warp's first product waits for that.
   pdl_launch_dependents();
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
   }
-  const uint32_t j0 = __ldg(cta_col + k), j1 = __ldg(cta_col + k + 1);
-  const uint64_t q0 = uint64_t(b) * d;
-  if (SMAP) {  // empty (block, column) segments are never emitted: zero them first
-    pdl_wait();      // (the previous step's apply may still read part)
-    for (uint32_t j = j0 + threadIdx.x; j < j1; j += kNT) part[q0 + j] = 0.f;
+  const uint32_t j0 = __ldg(p.cta + k), j1 = __ldg(p.cta + k + 1);
+  const uint64_t q0 = uint64_t(b) * p.nminor;
+  if (SMAP) {   // empty segments are never emitted: zero them first
+    pdl_wait();  // (the previous launch's finish may still read part)
+    for (uint32_t j = j0 + threadIdx.x; j < j1; j += kNT) p.part[q0 + j] = 0.f;
   }
   __syncthreads();  // the barrier init is visible to every waiter
   if (threadIdx.x == 0) {
-    pdl_wait();  // the coefficients come from the margin pass
-    const uint32_t total = round_up16(uint64_t(rows) * 4);  // coef carries 16-byte slack
+    pdl_wait();  // the slice comes from the previous pass
+    const uint32_t total = round_up16(uint64_t(len) * 4);  // both operands carry 16-byte slack
     mbar_arrive_expect_tx(&bar, total);
     for (uint32_t off = 0; off < total; off += 32768)
-      bulk_g2s(reinterpret_cast<char*>(cs) + off, reinterpret_cast<const char*>(coef + r0) + off,
+      bulk_g2s(reinterpret_cast<char*>(cs) + off, reinterpret_cast<const char*>(p.slice + r0) + off,
                min(32768u, total - off), &bar);
   }
-  const uint32_t S0 = __ldg(segptr + q0 + j0), S1 = __ldg(segptr + q0 + j1);
+  const uint32_t S0 = __ldg(p.segptr + q0 + j0), S1 = __ldg(p.segptr + q0 + j1);
   bool ready = false;  // the first tiles' loads overlap the slice's bulk copy
+  float* __restrict__ part = p.part;
+  const uint32_t* __restrict__ som = p.seg_of_ord;
   cta_segments<kE, 2, WinC>(
-      S0, S1, bm, bpre,
+      S0, S1, p.bm, p.bpre,
       [&](uint32_t s) {
         WinC q;
-        ldg256(cval + s, q.v0, q.v1);
-        q.r = __ldg(reinterpret_cast<const uint4*>(crow + s));
+        ldg256(p.val + s, q.v0, q.v1);
+        q.r = __ldg(reinterpret_cast<const uint4*>(p.id + s));
         return q;
       },
-      [&](const WinC& q, float* p) {
+      [&](const WinC& q, float* pr) {
         if (!ready) {
           mbar_wait(&bar, 0);
           ready = true;
         }
-        p[0] = q.v0.x * cs[q.r.x & 0xffffu], p[1] = q.v0.y * cs[q.r.x >> 16];
-        p[2] = q.v0.z * cs[q.r.y & 0xffffu], p[3] = q.v0.w * cs[q.r.y >> 16];
-        p[4] = q.v1.x * cs[q.r.z & 0xffffu], p[5] = q.v1.y * cs[q.r.z >> 16];
-        p[6] = q.v1.z * cs[q.r.w & 0xffffu], p[7] = q.v1.w * cs[q.r.w >> 16];
+        pr[0] = q.v0.x * cs[q.r.x & 0xffffu], pr[1] = q.v0.y * cs[q.r.x >> 16];
+        pr[2] = q.v0.z * cs[q.r.y & 0xffffu], pr[3] = q.v0.w * cs[q.r.y >> 16];
+        pr[4] = q.v1.x * cs[q.r.z & 0xffffu], pr[5] = q.v1.y * cs[q.r.z >> 16];
+        pr[6] = q.v1.z * cs[q.r.w & 0xffffu], pr[7] = q.v1.w * cs[q.r.w >> 16];
       },
-      [&](int32_t X, float z) { part[SMAP ? __ldg(seg_of_ord + X) : static_cast<uint32_t>(X)] = z; },
-      [&](int32_t X, float z) { part[SMAP ? __ldg(seg_of_ord + X) : static_cast<uint32_t>(X)] = z; },
+      [&](int32_t X, float z) { part[SMAP ? __ldg(som + X) : static_cast<uint32_t>(X)] = z; },
+      [&](int32_t X, float z) { part[SMAP ? __ldg(som + X) : static_cast<uint32_t>(X)] = z; },
       [&](int32_t, int32_t) {},
       sc);
   if (!ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
   __syncthreads();
-  const unsigned target = gen * nblk;
+  const unsigned target = p.gen * p.nblk;
   if (threadIdx.x == 0) {
-    const unsigned t = atom_add_acq_rel_gpu(tickets + k, 1u) + 1u;
+    const unsigned t = atom_add_acq_rel_gpu(p.tickets + k, 1u) + 1u;
     sc.last = t == target;
-    if (coop)
-      while (ld_acquire_gpu(tickets + k) < target) __nanosleep(32);
+    if (p.coop)
+      while (ld_acquire_gpu(p.tickets + k) < target) __nanosleep(32);
   }
   __syncthreads();
-  uint32_t a0 = j0, a1 = j1;  // the columns this CTA applies
-  if (coop) {
-    a0 = j0 + static_cast<uint32_t>(uint64_t(j1 - j0) * b / nblk);
-    a1 = j0 + static_cast<uint32_t>(uint64_t(j1 - j0) * (b + 1) / nblk);
+  uint32_t a0 = j0, a1 = j1;  // the minor indices this CTA finishes
+  if (p.coop) {
+    a0 = j0 + static_cast<uint32_t>(uint64_t(j1 - j0) * b / p.nblk);
+    a1 = j0 + static_cast<uint32_t>(uint64_t(j1 - j0) * (b + 1) / p.nblk);
   } else if (!sc.last) {
     return;
   }
@@ -490,31 +503,37 @@ __global__ void __launch_bounds__(kNT, 1)
   double nrm = 0.0;
   int bad = 0;
   for (uint32_t j = a0 + threadIdx.x; j < a1; j += kNT) {
-    // Block order; 8 loads in flight per thread (only d/cpb threads work here).
+    // Block order; 8 loads in flight per thread.
     double g = 0.0;
     uint32_t bb = 0;
-    for (; bb + 8 <= nblk; bb += 8) {
+    for (; bb + 8 <= p.nblk; bb += 8) {
       float v[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = __ldcg(part + uint64_t(bb + i) * d + j);
+      for (int i = 0; i < 8; ++i) v[i] = __ldcg(part + uint64_t(bb + i) * p.nminor + j);
 #pragma unroll
       for (int i = 0; i < 8; ++i) g += static_cast<double>(v[i]);
     }
-    for (; bb < nblk; ++bb) g += static_cast<double>(__ldcg(part + uint64_t(bb) * d + j));
+    for (; bb < p.nblk; ++bb) g += static_cast<double>(__ldcg(part + uint64_t(bb) * p.nminor + j));
+    if (MODE == kPassMargin) {
+      p.coef[j] = coef_fast<TASK>(static_cast<float>(g), __ldg(p.y + j));
+      continue;
+    }
     if (!isfinite(g)) bad = 1;
-    if (aa.apply) {
-      const double wn = aa.w64[j] - aa.alpha * g;
-      aa.w64[j] = wn;
-      aa.w32[j] = static_cast<float>(wn);
+    if (p.aa.apply) {
+      const double wn = p.aa.w64[j] - p.aa.alpha * g;
+      p.aa.w64[j] = wn;
+      p.aa.w32[j] = static_cast<float>(wn);
     } else {
-      aa.g64[j] = g;
+      p.aa.g64[j] = g;
     }
     nrm += g * g;
   }
-  if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) *aa.finite = 0;
-  if (aa.want_norm) {
-    nrm = warp_sum_d(nrm);
-    if ((threadIdx.x & 31) == 0 && nrm != 0.0) atomicAdd(aa.norm2, nrm);
+  if (MODE == kPassGrad) {
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) *p.aa.finite = 0;
+    if (p.aa.want_norm) {
+      nrm = warp_sum_d(nrm);
+      if ((threadIdx.x & 31) == 0 && nrm != 0.0) atomicAdd(p.aa.norm2, nrm);
+    }
   }
 }
 
@@ -571,28 +590,39 @@ __global__ void narrow_u16_kernel(const uint32_t* __restrict__ src, uint64_t n, 
     dst[i] = static_cast<uint16_t>(src[i]);
 }
 
-// Sort keys (block*d + column) and payloads (value bits << 16 | block-local
-// row) of every nonzero, warp per row.
-__global__ void csc_keys_kernel(const float* __restrict__ val, const uint32_t* __restrict__ idx,
-                                const uint32_t* __restrict__ rowptr, uint32_t n, uint32_t d,
-                                uint32_t rb, uint32_t* keys, uint64_t* pay) {
+// Sort keys and payloads of every nonzero (row r, column j), warp per row:
+// by rows (the CSC): key = (r / rb) * d + j, payload = value bits << 16 | r % rb;
+// by columns (the wide margin pass): key = (j / rb) * n + r, payload = value
+// bits << 16 | j % rb.
+template <bool BY_COL>
+__global__ void blocked_keys_kernel(const float* __restrict__ val, const uint32_t* __restrict__ idx,
+                                    const uint32_t* __restrict__ rowptr, uint32_t n, uint32_t d,
+                                    uint32_t rb, uint32_t* keys, uint64_t* pay) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t r = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
     const uint32_t b = static_cast<uint32_t>(r / rb), lr = static_cast<uint32_t>(r - uint64_t(b) * rb);
     const uint32_t s1 = rowptr[r + 1];
     for (uint32_t s = rowptr[r] + lane; s < s1; s += 32) {
-      keys[s] = b * d + idx[s];
-      pay[s] = (uint64_t(__float_as_uint(val[s])) << 16) | lr;
+      const uint32_t j = idx[s];
+      const uint64_t v = uint64_t(__float_as_uint(val[s])) << 16;
+      if (BY_COL) {
+        const uint32_t jb = j / rb;
+        keys[s] = jb * n + static_cast<uint32_t>(r);
+        pay[s] = v | (j - jb * rb);
+      } else {
+        keys[s] = b * d + j;
+        pay[s] = v | lr;
+      }
     }
   }
 }
 
 // Unpack the sorted payloads, write the CSC head bitmap (one ballot per 32
 // slots) and the segment pointers (segptr[q] = first slot of key >= q).
-__global__ void csc_unpack_kernel(const uint32_t* __restrict__ keys, const uint64_t* __restrict__ pay,
-                                  uint32_t nnz, uint32_t nseg, float* cval, uint16_t* crow,
-                                  uint32_t* bm, uint32_t* segptr) {
+__global__ void blocked_unpack_kernel(const uint32_t* __restrict__ keys, const uint64_t* __restrict__ pay,
+                                      uint32_t nnz, uint32_t nseg, float* cval, uint16_t* crow,
+                                      uint32_t* bm, uint32_t* segptr) {
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t total = (uint64_t(nnz) + 32) & ~uint64_t(31);  // whole warps, one past the end
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -624,8 +654,8 @@ __global__ void seg_nonempty_kernel(const uint32_t* __restrict__ segptr, uint32_
 }
 
 // Column totals over the row blocks (for nnz-balanced column ranges).
-__global__ void col_count_kernel(const uint32_t* __restrict__ segptr, uint32_t d, uint32_t nblk,
-                                 uint32_t* cnt) {
+__global__ void minor_count_kernel(const uint32_t* __restrict__ segptr, uint32_t d, uint32_t nblk,
+                                   uint32_t* cnt) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d) return;
   uint32_t c = 0;
@@ -633,9 +663,9 @@ __global__ void col_count_kernel(const uint32_t* __restrict__ segptr, uint32_t d
   cnt[j] = c;
 }
 
-// cta_col[k] = first column whose inclusive column prefix exceeds k*nnz/cpb.
-__global__ void cta_col_kernel(const uint32_t* __restrict__ incl, uint32_t d, uint32_t cpb,
-                               uint64_t nnz, uint32_t* cta_col) {
+// cta_col[k] = first minor index whose inclusive count prefix exceeds k*nnz/cpb.
+__global__ void cta_minor_kernel(const uint32_t* __restrict__ incl, uint32_t d, uint32_t cpb,
+                                 uint64_t nnz, uint32_t* cta_col) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k > cpb) return;
   if (k == 0 || k == cpb) {
@@ -713,58 +743,36 @@ void choose_blocks(const Ctx& c, uint64_t n, uint32_t& rb, uint32_t& nblk, uint3
 
 }  // namespace
 
-void sparse_prep(Dataset& ds) {
-  if (ds.sparse_ready) return;
+// The blocked segmented copy (see Blocked in device.hpp) by a stable radix
+// sort of (block, minor) keys: within a segment the major ids stay ascending
+// (deterministic sums). by_col: major = columns (the wide margin pass).
+void build_blocked(Dataset& ds, bool by_col, Blocked& B) {
   Ctx& c = *ds.ctx;
   cudaStream_t s = c.stream;
-  const uint64_t n = ds.n, d = ds.d, nnz = ds.nnz;
-  if (d * std::max<uint64_t>(1, (n + kMaxRowBlock - 1) / kMaxRowBlock) >= (uint64_t(1) << 31) ||
-      n >= (uint64_t(1) << 31))
-    throw Unsupported("full-batch sparse step: rows and (row blocks x d) segments must fit 31 bits");
   auto& sp = ds.prep;
-  sp.cnt.alloc(2);
-  check(cudaMemsetAsync(sp.cnt.p, 0, 2 * sizeof(unsigned), s), "memset");
-  // Row heads, 16-bit ids, margin CTA partition.
+  const uint64_t n = ds.n, d = ds.d, nnz = ds.nnz;
+  const uint64_t nmajor = by_col ? d : n, nminor = by_col ? n : d;
+  choose_blocks(c, nmajor, B.rb, B.nblk, B.cpb);
+  const uint64_t nseg = uint64_t(B.nblk) * nminor;
+  if (nseg >= (uint64_t(1) << 31))
+    throw Unsupported("full-batch sparse step: (blocks x minor) segments must fit 31 bits");
   const uint64_t nwords = (nnz + 256) / 32 + 2;
-  ds.rbm.alloc(nwords);
-  ds.rbm.zero(s);
-  sp.a.alloc(std::max<uint64_t>(1, n));  // non-empty row flags
-  prof_begin(c, "sparse_prep_kernel");
-  row_heads_kernel<<<grid_1d(n), 256, 0, s>>>(ds.rowptr.p, static_cast<uint32_t>(n), ds.rbm.p, sp.a.p, sp.cnt.p);
-  launched(c, "sparse_prep_kernel");
-  word_prefix(c, ds.rbm.p, nwords, ds.rbm_pre, sp.tmp, sp.b);
-  if (d <= 65536) {
-    ds.cidx16.alloc(nnz + 1024);
-    check(cudaMemsetAsync(ds.cidx16.p + nnz, 0, 1024 * sizeof(uint16_t), s), "memset");
-    prof_begin(c, "sparse_prep_kernel");
-    narrow_u16_kernel<<<c.num_sms * 8, 256, 0, s>>>(ds.idx.p, nnz, ds.cidx16.p);
-    launched(c, "sparse_prep_kernel");
-  }
-  ds.cta_n = static_cast<uint32_t>(std::max(1, c.num_sms));
-  ds.cta_slot.alloc(ds.cta_n + 1);
-  prof_begin(c, "sparse_prep_kernel");
-  cta_slot_kernel<<<grid_1d(ds.cta_n + 1), 256, 0, s>>>(ds.rowptr.p, static_cast<uint32_t>(n), ds.cta_n,
-                                                         ds.cta_slot.p);
-  launched(c, "sparse_prep_kernel");
-
-  // Row-blocked CSC by a stable radix sort of (block, column) keys.
-  choose_blocks(c, n, ds.csc_rb, ds.csc_nblk, ds.csc_cpb);
-  const uint64_t nseg = uint64_t(ds.csc_nblk) * d;
-  ds.cval.alloc(nnz + 1024);
-  ds.crow.alloc(nnz + 1024);
-  check(cudaMemsetAsync(ds.cval.p + nnz, 0, 1024 * sizeof(float), s), "memset");
-  check(cudaMemsetAsync(ds.crow.p + nnz, 0, 1024 * sizeof(uint16_t), s), "memset");
-  ds.segptr.alloc(nseg + 1);
-  ds.cbm.alloc(nwords);
-  ds.cbm.zero(s);
+  B.val.alloc(nnz + 1024);
+  B.id.alloc(nnz + 1024);
+  check(cudaMemsetAsync(B.val.p + nnz, 0, 1024 * sizeof(float), s), "memset");
+  check(cudaMemsetAsync(B.id.p + nnz, 0, 1024 * sizeof(uint16_t), s), "memset");
+  B.segptr.alloc(nseg + 1);
+  B.bm.alloc(nwords);
+  B.bm.zero(s);
   if (nnz > 0) {
     sp.k_in.alloc(nnz);
     sp.k_out.alloc(nnz);
     sp.p_in.alloc(nnz);
     sp.p_out.alloc(nnz);
     prof_begin(c, "sparse_prep_kernel");
-    csc_keys_kernel<<<c.num_sms * 8, 256, 0, s>>>(ds.val.p, ds.idx.p, ds.rowptr.p, static_cast<uint32_t>(n),
-                                                  static_cast<uint32_t>(d), ds.csc_rb, sp.k_in.p, sp.p_in.p);
+    auto keys = by_col ? blocked_keys_kernel<true> : blocked_keys_kernel<false>;
+    keys<<<c.num_sms * 8, 256, 0, s>>>(ds.val.p, ds.idx.p, ds.rowptr.p, static_cast<uint32_t>(n),
+                                       static_cast<uint32_t>(d), B.rb, sp.k_in.p, sp.p_in.p);
     launched(c, "sparse_prep_kernel");
     int end_bit = 1;
     while (end_bit < 32 && (uint64_t(1) << end_bit) < nseg) ++end_bit;
@@ -778,145 +786,185 @@ void sparse_prep(Dataset& ds) {
                                           static_cast<int64_t>(nnz), 0, end_bit, s),
           "cub sort");
     prof_begin(c, "sparse_prep_kernel");
-    csc_unpack_kernel<<<c.num_sms * 8, 256, 0, s>>>(sp.k_out.p, sp.p_out.p, static_cast<uint32_t>(nnz),
-                                                    static_cast<uint32_t>(nseg), ds.cval.p, ds.crow.p,
-                                                    ds.cbm.p, ds.segptr.p);
+    blocked_unpack_kernel<<<c.num_sms * 8, 256, 0, s>>>(sp.k_out.p, sp.p_out.p, static_cast<uint32_t>(nnz),
+                                                        static_cast<uint32_t>(nseg), B.val.p, B.id.p, B.bm.p,
+                                                        B.segptr.p);
     launched(c, "sparse_prep_kernel");
   } else {
-    ds.segptr.zero(s);
+    B.segptr.zero(s);
   }
-  word_prefix(c, ds.cbm.p, nwords, ds.cbm_pre, sp.tmp, sp.b);
+  word_prefix(c, B.bm.p, nwords, B.bm_pre, sp.tmp, sp.b);
   sp.c.alloc(std::max<uint64_t>(1, nseg));  // non-empty segment flags
+  check(cudaMemsetAsync(sp.cnt.p + 1, 0, sizeof(unsigned), s), "memset");
   prof_begin(c, "sparse_prep_kernel");
-  seg_nonempty_kernel<<<grid_1d(nseg), 256, 0, s>>>(ds.segptr.p, static_cast<uint32_t>(nseg), sp.c.p,
+  seg_nonempty_kernel<<<grid_1d(nseg), 256, 0, s>>>(B.segptr.p, static_cast<uint32_t>(nseg), sp.c.p,
                                                      sp.cnt.p + 1);
   launched(c, "sparse_prep_kernel");
-  {  // nnz-balanced column ranges, shared by every row block
-    sp.k_in.alloc(std::max<uint64_t>(1, d));  // column counts (the sort keys are consumed)
-    sp.b.alloc(std::max<uint64_t>(nwords + 1, d));
+  {  // nnz-balanced minor ranges, shared by every block
+    sp.k_in.alloc(std::max<uint64_t>(1, nminor));  // per-minor counts (the sort keys are consumed)
+    sp.b.alloc(std::max<uint64_t>(nwords + 1, nminor));
     prof_begin(c, "sparse_prep_kernel");
-    col_count_kernel<<<grid_1d(d), 256, 0, s>>>(ds.segptr.p, static_cast<uint32_t>(d), ds.csc_nblk, sp.k_in.p);
+    minor_count_kernel<<<grid_1d(nminor), 256, 0, s>>>(B.segptr.p, static_cast<uint32_t>(nminor), B.nblk,
+                                                        sp.k_in.p);
     launched(c, "sparse_prep_kernel");
     size_t bytes = 0;
-    check(cub::DeviceScan::InclusiveSum(nullptr, bytes, sp.k_in.p, sp.b.p, static_cast<int64_t>(d), s),
+    check(cub::DeviceScan::InclusiveSum(nullptr, bytes, sp.k_in.p, sp.b.p, static_cast<int64_t>(nminor), s),
           "cub scan size");
     sp.tmp.alloc(bytes);
     bytes = sp.tmp.n;
-    check(cub::DeviceScan::InclusiveSum(sp.tmp.p, bytes, sp.k_in.p, sp.b.p, static_cast<int64_t>(d), s),
+    check(cub::DeviceScan::InclusiveSum(sp.tmp.p, bytes, sp.k_in.p, sp.b.p, static_cast<int64_t>(nminor), s),
           "cub scan");
-    ds.cta_col.alloc(ds.csc_cpb + 1);
+    B.cta.alloc(B.cpb + 1);
     prof_begin(c, "sparse_prep_kernel");
-    cta_col_kernel<<<grid_1d(ds.csc_cpb + 1), 256, 0, s>>>(sp.b.p, static_cast<uint32_t>(d), ds.csc_cpb, nnz,
-                                                            ds.cta_col.p);
+    cta_minor_kernel<<<grid_1d(B.cpb + 1), 256, 0, s>>>(sp.b.p, static_cast<uint32_t>(nminor), B.cpb, nnz,
+                                                         B.cta.p);
     launched(c, "sparse_prep_kernel");
   }
-  // One host read-back: are there empty rows / segments (ordinal maps needed)?
-  unsigned empty[2] = {0, 0};
-  check(cudaMemcpyAsync(empty, sp.cnt.p, sizeof(empty), cudaMemcpyDeviceToHost, s), "D2H");
+  unsigned empty = 0;
+  check(cudaMemcpyAsync(&empty, sp.cnt.p + 1, sizeof(empty), cudaMemcpyDeviceToHost, s), "D2H");
   check(cudaStreamSynchronize(s), "prep sync");
-  ds.rows_empty = empty[0] != 0;
-  ds.segs_empty = empty[1] != 0;
+  B.segs_empty = empty != 0;
+  if (B.segs_empty) compaction(c, sp.c.p, nseg, B.seg_of_ord, sp.tmp, sp.b);
+  B.tickets.alloc(B.cpb);
+  B.tickets.zero(s);  // arrival counts restart with the launch numbers
+  B.gen = 0;
+}
+
+void sparse_prep(Dataset& ds) {
+  if (ds.sparse_ready) return;
+  Ctx& c = *ds.ctx;
+  cudaStream_t s = c.stream;
+  const uint64_t n = ds.n, d = ds.d, nnz = ds.nnz;
+  if (n >= (uint64_t(1) << 31))
+    throw Unsupported("full-batch sparse step: rows must fit 31 bits");
+  auto& sp = ds.prep;
+  sp.cnt.alloc(2);
+  check(cudaMemsetAsync(sp.cnt.p, 0, 2 * sizeof(unsigned), s), "memset");
+  const uint64_t nwords = (nnz + 256) / 32 + 2;
+  // Row heads, 16-bit ids, margin CTA partition.
+  ds.rbm.alloc(nwords);
+  ds.rbm.zero(s);
+  sp.a.alloc(std::max<uint64_t>(1, n));  // non-empty row flags
+  prof_begin(c, "sparse_prep_kernel");
+  row_heads_kernel<<<grid_1d(n), 256, 0, s>>>(ds.rowptr.p, static_cast<uint32_t>(n), ds.rbm.p, sp.a.p, sp.cnt.p);
+  launched(c, "sparse_prep_kernel");
+  word_prefix(c, ds.rbm.p, nwords, ds.rbm_pre, sp.tmp, sp.b);
+  const size_t model_bytes = round_up16(uint64_t(d + 1) * 4);
+  ds.wide = model_bytes + sizeof(CtaScratch) + 64 > c.max_smem_optin;
+  if (!ds.wide) {  // K2s: the model fits in SMEM, so d < 65,536
+    ds.cidx16.alloc(nnz + 1024);
+    check(cudaMemsetAsync(ds.cidx16.p + nnz, 0, 1024 * sizeof(uint16_t), s), "memset");
+    prof_begin(c, "sparse_prep_kernel");
+    narrow_u16_kernel<<<c.num_sms * 8, 256, 0, s>>>(ds.idx.p, nnz, ds.cidx16.p);
+    launched(c, "sparse_prep_kernel");
+  }
+  ds.cta_n = static_cast<uint32_t>(std::max(1, c.num_sms));
+  ds.cta_slot.alloc(ds.cta_n + 1);
+  prof_begin(c, "sparse_prep_kernel");
+  cta_slot_kernel<<<grid_1d(ds.cta_n + 1), 256, 0, s>>>(ds.rowptr.p, static_cast<uint32_t>(n), ds.cta_n,
+                                                         ds.cta_slot.p);
+  launched(c, "sparse_prep_kernel");
+
+  build_blocked(ds, false, ds.csc);
+  // Models too large for shared memory: the margin pass runs blocked too.
+  if (ds.wide) {
+    build_blocked(ds, true, ds.wmajor);
+    ds.mpart.alloc(uint64_t(ds.wmajor.nblk) * n + 1);
+  }
+  // One host read-back: are there empty rows (ordinal map needed)?
+  unsigned empty = 0;
+  check(cudaMemcpyAsync(&empty, sp.cnt.p, sizeof(empty), cudaMemcpyDeviceToHost, s), "D2H");
+  check(cudaStreamSynchronize(s), "prep sync");
+  ds.rows_empty = empty != 0;
   if (ds.rows_empty) compaction(c, sp.a.p, n, ds.row_of_ord, sp.tmp, sp.b);
-  if (ds.segs_empty) compaction(c, sp.c.p, nseg, ds.seg_of_ord, sp.tmp, sp.b);
   if (ds.coef.n < n + 8) {
     ds.coef.alloc(n + 8);
     ds.coef.zero(s);
   }
-  ds.sparse_tickets.alloc(ds.csc_cpb);
-  ds.sparse_tickets.zero(s);  // arrival counts restart with the launch numbers
-  ds.sparse_gen = 0;
   ds.sparse_ready = true;
 }
 
+namespace {
+// Launch one blocked pass over B (PDL unless the structures were just
+// rebuilt by the previous kernels on the stream).
+template <int MODE>
+void launch_pass(Dataset& ds, Blocked& B, uint64_t nminor, uint64_t nmajor, const float* slice, float* part,
+                 int task, const ApplyArgs& aa, bool pdl, const char* name) {
+  Ctx& c = *ds.ctx;
+  const size_t smem = round_up16(uint64_t(B.rb) * 4);
+  void (*kern)(PassArgs);
+  if (task == kTaskLR)
+    kern = B.segs_empty ? blocked_pass_kernel<MODE, kTaskLR, true> : blocked_pass_kernel<MODE, kTaskLR, false>;
+  else
+    kern = B.segs_empty ? blocked_pass_kernel<MODE, kTaskSVM, true> : blocked_pass_kernel<MODE, kTaskSVM, false>;
+  set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(blocked_pass)");
+  const unsigned grid = B.nblk * B.cpb;
+  const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kNT, smem);
+  PassArgs p{B.val.p, B.id.p, B.bm.p, B.bm_pre.p, B.segptr.p, B.cta.p, B.cpb, B.nblk,
+             static_cast<uint32_t>(nminor), B.rb, static_cast<uint32_t>(nmajor), slice,
+             B.segs_empty ? B.seg_of_ord.p : nullptr, part, B.tickets.p, ++B.gen,
+             // With one CTA per SM and grid <= SMs every CTA becomes resident
+             // once the previous pass has drained: the arrival wait cannot deadlock.
+             per_sm >= 1 && grid <= static_cast<unsigned>(c.num_sms) ? 1 : 0, aa, ds.labels.p, ds.coef.p};
+  prof_begin(c, name);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kNT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  check(cudaLaunchKernelEx(&cfg, kern, p), "cudaLaunchKernelEx(blocked_pass)");
+  launched(c, name);
+}
+}  // namespace
+
 void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a) {
-  // K2s issues its first CSR loads before its PDL wait, so it may overlap its
-  // predecessor only when that predecessor cannot be writing the CSR-derived
-  // structures, i.e. not right after they were (re)built.
+  // The first pass issues its first static-data loads before its PDL wait,
+  // so it may overlap its predecessor only when that predecessor cannot be
+  // writing the derived structures, i.e. not right after they were (re)built.
   const bool rebuilt = !ds.sparse_ready;
   sparse_prep(ds);
   Ctx& c = *ds.ctx;
   if (ds.n == 0) return;
   const uint32_t d = static_cast<uint32_t>(ds.d);
-  // K2s
-  {
+  ApplyArgs aa{a.alpha, a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p, m.finite.p, m.scal.p};
+  if (ds.wide) {
+    // K2w: margins of a model too large for SMEM, blocked by columns.
+    launch_pass<kPassMargin>(ds, ds.wmajor, ds.n, d, m.w32.p, ds.mpart.p, a.task, aa, !rebuilt,
+                             "k2w_margin_kernel");
+  } else {  // K2s (d < 65,536 here: the 16-bit ids exist)
     const size_t model_bytes = round_up16(uint64_t(d + 1) * 4);
-    const bool smemw = model_bytes + sizeof(CtaScratch) + 64 <= c.max_smem_optin;
-    const bool i16 = ds.cidx16.p != nullptr;
-    auto go = [&]<bool SW, bool I16>() {
-      auto kern = a.task == kTaskLR
-                      ? (ds.rows_empty ? k2s_margin_kernel<kTaskLR, SW, I16, true> : k2s_margin_kernel<kTaskLR, SW, I16, false>)
-                      : (ds.rows_empty ? k2s_margin_kernel<kTaskSVM, SW, I16, true>
-                                       : k2s_margin_kernel<kTaskSVM, SW, I16, false>);
-      const size_t smem = SW ? model_bytes : 0;
-      set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(k2s)");
-      prof_begin(c, "k2s_margin_kernel");
-      cudaLaunchConfig_t cfg{};
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = 1;
-      cfg.gridDim = dim3(ds.cta_n);
-      cfg.blockDim = dim3(kNT);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = c.stream;
-      cfg.attrs = attr;
-      cfg.numAttrs = rebuilt ? 0 : 1;
-      check(cudaLaunchKernelEx(&cfg, kern, static_cast<const float*>(ds.val.p),
-                               I16 ? static_cast<const void*>(ds.cidx16.p) : static_cast<const void*>(ds.idx.p),
-                               static_cast<const uint32_t*>(ds.rbm.p), static_cast<const uint32_t*>(ds.rbm_pre.p),
-                               static_cast<const uint32_t*>(ds.cta_slot.p),
-                               static_cast<const uint32_t*>(ds.rows_empty ? ds.row_of_ord.p : nullptr),
-                               static_cast<const float*>(ds.labels.p), static_cast<uint32_t>(ds.n),
-                               static_cast<const float*>(m.w32.p), d, ds.coef.p),
-            "cudaLaunchKernelEx(k2s)");
-      launched(c, "k2s_margin_kernel");
-    };
-    if (smemw && i16) go.template operator()<true, true>();
-    else if (smemw) go.template operator()<true, false>();
-    else if (i16) go.template operator()<false, true>();
-    else go.template operator()<false, false>();
-  }
-  // K3s
-  {
-    m.part32.alloc(uint64_t(ds.csc_nblk) * d + 1);
-    const size_t smem = round_up16(uint64_t(ds.csc_rb) * 4);
-    auto kern = ds.segs_empty ? k3s_grad_kernel<true> : k3s_grad_kernel<false>;
-    set_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(k3s)");
-    ApplyArgs aa{a.alpha, a.apply ? 1 : 0, a.want_norm ? 1 : 0, m.w64.p, m.w32.p, m.g64.p, m.finite.p, m.scal.p};
-    const unsigned grid = ds.csc_nblk * ds.csc_cpb;
-    const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kNT, smem);
-    int coop = per_sm >= 1 && grid <= static_cast<unsigned>(c.num_sms) ? 1 : 0;
-    unsigned gen = ++ds.sparse_gen;
-    prof_begin(c, "k3s_grad_kernel");
-    const float* cval = ds.cval.p;
-    const uint16_t* crow = ds.crow.p;
-    const uint32_t* cbm = ds.cbm.p;
-    const uint32_t* cbm_pre = ds.cbm_pre.p;
-    const uint32_t* segptr = ds.segptr.p;
-    const uint32_t* cta_col = ds.cta_col.p;
-    uint32_t cpb = ds.csc_cpb, nblk = ds.csc_nblk, rb = ds.csc_rb, n = static_cast<uint32_t>(ds.n);
-    uint32_t dd = d;
-    const float* coef = ds.coef.p;
-    const uint32_t* seg_of_ord = ds.segs_empty ? ds.seg_of_ord.p : nullptr;
-    float* part = m.part32.p;
-    unsigned* tickets = ds.sparse_tickets.p;
-    // PDL launch (the CTAs start as the margin pass's CTAs retire). With one
-    // CTA per SM and grid <= SMs every CTA becomes resident once the margin
-    // pass has drained, so the range-arrival wait (coop) cannot deadlock.
+    auto kern = a.task == kTaskLR
+                    ? (ds.rows_empty ? k2s_margin_kernel<kTaskLR, true> : k2s_margin_kernel<kTaskLR, false>)
+                    : (ds.rows_empty ? k2s_margin_kernel<kTaskSVM, true> : k2s_margin_kernel<kTaskSVM, false>);
+    set_max_dyn_smem(reinterpret_cast<const void*>(kern), model_bytes, "cudaFuncSetAttribute(k2s)");
+    prof_begin(c, "k2s_margin_kernel");
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = dim3(ds.cta_n);
     cfg.blockDim = dim3(kNT);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = model_bytes;
     cfg.stream = c.stream;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    check(cudaLaunchKernelEx(&cfg, kern, cval, crow, cbm, cbm_pre, segptr, cta_col, cpb, nblk, dd, rb, n, coef,
-                             seg_of_ord, part, tickets, aa, gen, coop),
-          "cudaLaunchKernelEx(k3s)");
-    launched(c, "k3s_grad_kernel");
+    cfg.numAttrs = rebuilt ? 0 : 1;
+    check(cudaLaunchKernelEx(&cfg, kern, static_cast<const float*>(ds.val.p),
+                             static_cast<const uint16_t*>(ds.cidx16.p), static_cast<const uint32_t*>(ds.rbm.p),
+                             static_cast<const uint32_t*>(ds.rbm_pre.p), static_cast<const uint32_t*>(ds.cta_slot.p),
+                             static_cast<const uint32_t*>(ds.rows_empty ? ds.row_of_ord.p : nullptr),
+                             static_cast<const float*>(ds.labels.p), static_cast<uint32_t>(ds.n),
+                             static_cast<const float*>(m.w32.p), d, ds.coef.p),
+          "cudaLaunchKernelEx(k2s)");
+    launched(c, "k2s_margin_kernel");
   }
+  // K3s: the gradient pass and the update.
+  m.part32.alloc(uint64_t(ds.csc.nblk) * d + 1);
+  launch_pass<kPassGrad>(ds, ds.csc, d, ds.n, ds.coef.p, m.part32.p, a.task, aa, true, "k3s_grad_kernel");
 }
 
 }  // namespace sgdb::dev
