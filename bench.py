@@ -64,6 +64,9 @@ def _ncu_traffic(kernel, summary="round2_ncu_rcv1_full_batch.txt"):
     (profiles/round2_ncu_rcv1_full_batch.txt, written by scripts/ncu_summary.py
     from scripts/round2_profile.sh)."""
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    # The library's profiler names -> the CUDA function ncu reports.
+    kernel = {"k3s_grad_kernel": "blocked_pass_kernel<0,",
+              "k2w_margin_kernel": "blocked_pass_kernel<1,"}.get(kernel, kernel)
     path = os.path.join(ROOT, "profiles", summary)
     if not os.path.exists(path):
         return None, None

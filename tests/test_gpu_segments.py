@@ -1,14 +1,15 @@
-"""Edge cases of the full-batch sparse passes (K2s / K3s, kernels_sparse.cu).
+"""Edge cases of the full-batch sparse passes (K2s / K2w / K3s, kernels_sparse.cu).
 
 The margin pass and the blocked-CSC gradient pass walk each warp's nonzeros
-in 128-slot tiles, find segment boundaries in a head bitmap and recover
+in 256-slot tiles, find segment boundaries in a head bitmap and recover
 per-row / per-(block, column) sums with a segmented warp scan; segments cut
 between warps are finished in SMEM, empty segments go through ordinal maps.
 These inputs put boundaries where that bookkeeping can go wrong: empty rows
 (single, in long runs, leading and trailing), one-slot rows (several heads
 per lane), rows spanning many tiles and warps, tiny inputs (most warps
-empty), a model too wide to stage in shared memory, 32-bit column ids, and
-more row blocks than SMs. Full-batch gradients are compared with the CPU
+empty), a model too wide to stage in shared memory (its margins through the
+column-blocked pass K2w, where an empty row is empty in every column block),
+and more row blocks than SMs. Full-batch gradients are compared with the CPU
 oracle (proj/src/sync_engine.cpp:22-42 restated) at the sync tolerance of
 DESIGN.md §Numerics.
 """
@@ -54,8 +55,8 @@ SHAPES = _shapes()
 @pytest.mark.parametrize("name", sorted(SHAPES))
 @pytest.mark.parametrize("d", [600, 100_000])
 def test_full_batch_gradient_segments(sgdb, dev, orc, name, d):
-    """d = 600: model in SMEM, 16-bit ids; d = 100,000: model gathered from
-    L2, 32-bit ids."""
+    """d = 600: K2s (model in SMEM); d = 100,000: the model does not fit in
+    SMEM, margins through the column-blocked pass K2w (4 column blocks)."""
     S = sgdb
     lengths = [min(ln, d) for ln in SHAPES[name]]
     ds = _csr(S, lengths, d, seed=len(lengths) + d)
@@ -71,10 +72,12 @@ def test_full_batch_gradient_segments(sgdb, dev, orc, name, d):
 
 
 @pytest.mark.parametrize("name", ["mixed_pareto", "empty_runs", "long_rows"])
-def test_full_batch_epochs_segments(sgdb, dev, orc, name):
-    """Several B = N epochs (margin pass reads the updated model each time)."""
+@pytest.mark.parametrize("d", [3000, 100_000])
+def test_full_batch_epochs_segments(sgdb, dev, orc, name, d):
+    """Several B = N epochs (margin pass reads the updated model each time;
+    d = 100,000 through K2w's model slices)."""
     S = sgdb
-    ds = _csr(S, SHAPES[name], 3000, seed=5)
+    ds = _csr(S, SHAPES[name], d, seed=5)
     dds = S.DeviceDataset(dev, ds)
     model = S.DeviceModel(dev, ds.n_features)
     om, ol, _ = orc.sync_train(ds, 0, 0.05, ds.n_examples, 4, 7)
@@ -83,13 +86,15 @@ def test_full_batch_epochs_segments(sgdb, dev, orc, name):
         assert rel_l2(model.get(), om[e]) <= 1e-5
 
 
-def test_refresh_rebuilds_full_batch_structures(sgdb, dev, orc):
+@pytest.mark.parametrize("d", [500, 100_000])
+def test_refresh_rebuilds_full_batch_structures(sgdb, dev, orc, d):
     """sgdb_dataset_refresh_f32 with new values, column ids and row offsets
-    (same n, nnz): the head bitmaps, 16-bit ids and the blocked CSC are
-    rebuilt on the device, so full-batch gradients, the mini-batch chunk plan
-    (longest row recomputed) and Hogwild all see the new data."""
+    (same n, nnz): the head bitmaps, 16-bit ids, the blocked CSC and (d =
+    100,000) the column-blocked copy of K2w are rebuilt on the device, so
+    full-batch gradients, the mini-batch chunk plan (longest row recomputed)
+    and Hogwild all see the new data."""
     S = sgdb
-    a = S.fixtures.sparse_classification(3000, 500, 12.0, 31).rounded_f32()
+    a = S.fixtures.sparse_classification(3000, d, 12.0, 31).rounded_f32()
     dds = S.DeviceDataset(dev, a)
     model = S.DeviceModel(dev, a.n_features)
     assert S.sync_epoch(dds, model, S.Task.LR, 0.1, None, a.n_examples)
