@@ -1,6 +1,6 @@
 """Small driver for ncu captures: runs a few epochs of one target op.
 
-    python scripts/prof_targets.py {hogwild_w8a|hogwild_rcv1_block|hogwild_rcv1_block8|hogwild_w8a_example|
+    python scripts/prof_targets.py {hogwild_w8a|hogwild_rcv1|hogwild_rcv1_block|hogwild_rcv1_block8|hogwild_w8a_example|
                                     sync_covtype|sync_rcv1|sync_realsim|sync_news20|sync_dense1000|sync_c5|
                                     minibatch_covtype|minibatch_rcv1|minibatch_w8a} [epochs]
 """
@@ -28,6 +28,15 @@ def main():
         for _ in range(epochs):
             flush.zero_()
             S.hogwild_epoch(dds, model, S.Task.SVM, 0.01, plan)
+    elif target == "hogwild_rcv1":
+        host = S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813)
+        dds = S.DeviceDataset(dev, host)
+        plan = S.parse_plan("row-ch:kernel:0")
+        plan.workers = dev.resident_workers(dds)
+        model = S.DeviceModel(dev, host.n_features)
+        for _ in range(epochs):
+            flush.zero_()
+            S.hogwild_epoch(dds, model, S.Task.LR, 0.01, plan)
     elif target in ("hogwild_rcv1_block", "hogwild_rcv1_block8"):
         host = S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813)
         dds = S.DeviceDataset(dev, host)
