@@ -741,8 +741,6 @@ void choose_blocks(const Ctx& c, uint64_t n, uint32_t& rb, uint32_t& nblk, uint3
   cpb = static_cast<uint32_t>(std::max<uint64_t>(1, sms / nblk));
 }
 
-}  // namespace
-
 // The blocked segmented copy (see Blocked in device.hpp) by a stable radix
 // sort of (block, minor) keys: within a segment the major ids stay ascending
 // (deterministic sums). by_col: major = columns (the wide margin pass).
@@ -829,6 +827,8 @@ void build_blocked(Dataset& ds, bool by_col, Blocked& B) {
   B.tickets.zero(s);  // arrival counts restart with the launch numbers
   B.gen = 0;
 }
+
+}  // namespace
 
 void sparse_prep(Dataset& ds) {
   if (ds.sparse_ready) return;
