@@ -224,3 +224,24 @@ def test_more_row_blocks_than_sms(sgdb, dev, orc):
         g = S.sync.batch_gradient(S.Task(task), ds, None, w, device=dev)
         og = orc.batch_gradient(ds, task, None, w)
         assert rel_l2(g, og) <= 1e-5, (task, rel_l2(g, og))
+
+
+@pytest.mark.parametrize("n,d", [
+    (49_153, 600),      # two row blocks, the second holding one row
+    (3_000, 57_000),    # K2s with the model just inside shared memory
+    (3_000, 57_700),    # just past it: K2w
+    (3_000, 98_305),    # K2w, the last column block holding one column
+    (2_000, 1_000_003)])  # K2w, many column blocks, most segments empty (seg_of_ord)
+def test_full_batch_block_boundaries(sgdb, dev, orc, n, d):
+    """Row / column block boundaries of the blocked passes and the K2s / K2w
+    switch, against the oracle for both tasks."""
+    S = sgdb
+    rng = np.random.default_rng(n + d)
+    lengths = rng.integers(0, 9, n).tolist()
+    lengths[0], lengths[-1] = 8, 8  # the first and last rows and columns take part
+    ds = _csr(S, lengths, d, seed=n + d)
+    w = rng.normal(0, 0.5, d)
+    for task in (0, 1):
+        g = S.sync.batch_gradient(S.Task(task), ds, None, w, device=dev)
+        og = orc.batch_gradient(ds, task, None, w)
+        assert rel_l2(g, og) <= 1e-5, (n, d, task, rel_l2(g, og))
