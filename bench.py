@@ -419,8 +419,22 @@ def e2e_leg(S, dev, host, model, task, stream, n_global, world, args, barrier):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     del bufs
+    # The link's own rate for the same bytes: one pinned host -> device copy
+    # (the floor of a step that must move them).
+    src = torch.empty(h2d // 4 + 1, dtype=torch.float32).pin_memory()
+    dst = torch.empty(h2d // 4 + 1, dtype=torch.float32, device="cuda")
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    link_gbps = 3 * h2d / (time.perf_counter() - t0) / 1e9
+    del src, dst
     return {"value": n_global / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": steps,
+            "h2d_link_GBps_probe": link_gbps,
+            "step_vs_link_floor": (h2d / (link_gbps * 1e9)) / e2e_s,
             "pipeline": "double-buffered: step k+1's H2D (two copy streams) overlaps step k's "
                         "device rebuild of the full-batch structures + epoch; the model is read "
                         "back every step"}
