@@ -1,3 +1,5 @@
+# HISTORICAL (round 1): the sparse kernels this script captures (csr_coef*, csc_*, apply_partials)
+# were replaced in round 2 by K2s / K2w / K3s; scripts/round2_profile.sh is the current recipe.
 # ncu evidence for profiles/ (one GPU; never under torchrun). Raw reports land in
 # gpurun_out/; scripts/ncu_summary.py turns them into the committed summaries.
 set -x
