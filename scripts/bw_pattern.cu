@@ -32,6 +32,27 @@ __global__ void __launch_bounds__(1024, 1) k_stride(const float* x, size_t nf, f
   if (s == 12345.f) out[0] = s;
 }
 
+// Grid-stride with U independent 256-bit loads in flight per thread.
+template <int U>
+__global__ void __launch_bounds__(1024, 1) k_stride_u(const float* x, size_t nf, float* out) {
+  float s = 0.f;
+  const size_t step = size_t(gridDim.x) * blockDim.x * 8;
+  size_t i = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  for (; i + (U - 1) * step + 8 <= nf; i += U * step) {
+    float4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) ld256(x + i + u * step, a[u], b[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) s += a[u].x + a[u].y + a[u].z + a[u].w + b[u].x + b[u].y + b[u].z + b[u].w;
+  }
+  for (; i + 8 <= nf; i += step) {
+    float4 a, b;
+    ld256(x + i, a, b);
+    s += a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
+  }
+  if (s == 12345.f) out[0] = s;
+}
+
 // One stream per warp: slots [P, Q) of nf floats.
 __global__ void __launch_bounds__(1024, 1) k_chunk1(const float* x, size_t nf, float* out) {
   const size_t W = size_t(gridDim.x) * 32, w = size_t(blockIdx.x) * 32 + threadIdx.x / 32;
@@ -125,6 +146,29 @@ int main() {
   time("chunk3_nb2", [&] { k_chunk3<2><<<sms, 1024>>>(v, id, bm, ns, out); }, bytes);
   time("chunk3_nb3", [&] { k_chunk3<3><<<sms, 1024>>>(v, id, bm, ns, out); }, bytes);
   time("stride_2cta", [&] { k_stride<<<2 * sms, 1024>>>(big, nf_all, out); }, bytes);
+  time("stride_u2", [&] { k_stride_u<2><<<sms, 1024>>>(big, nf_all, out); }, bytes);
+  time("stride_u4", [&] { k_stride_u<4><<<sms, 1024>>>(big, nf_all, out); }, bytes);
+  {  // two passes: one launch over 2x the bytes vs two launches back to back
+    float* big2;
+    if (cudaMalloc(&big2, nf_all * 8 + 4096) == cudaSuccess) {
+      cudaMemset(big2, 0, nf_all * 8);
+      time("stride_2x_one_launch", [&] { k_stride<<<sms, 1024>>>(big2, 2 * nf_all, out); }, 2 * bytes);
+      time("stride_2x_two_launches", [&] {
+        k_stride<<<sms, 1024>>>(big2, nf_all, out);
+        k_stride<<<sms, 1024>>>(big2 + nf_all, nf_all, out);
+      }, 2 * bytes);
+      cudaFree(big2);
+    }
+  }
+  {  // a 4 GiB read (the copy peak's size) with 4 loads in flight per thread
+    float* huge;
+    const size_t nh = size_t(1) << 30;
+    if (cudaMalloc(&huge, nh * 4) == cudaSuccess) {
+      cudaMemset(huge, 0, nh * 4);
+      time("stride_u4_4GiB", [&] { k_stride_u<4><<<sms, 1024>>>(huge, nh, out); }, double(nh) * 4);
+      cudaFree(huge);
+    }
+  }
   cudaError_t err = cudaDeviceSynchronize();
   if (err != cudaSuccess) printf("error %s\n", cudaGetErrorString(err));
   return 0;
