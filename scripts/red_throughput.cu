@@ -18,6 +18,15 @@ __device__ __forceinline__ uint32_t mix(uint32_t x) {
   return x;
 }
 
+// fp64 reductions (the sparse mini-batch step's update of the fp64 master).
+__global__ void __launch_bounds__(256) k64(double* m, uint32_t d, uint32_t stride, uint64_t total, uint32_t salt) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t j = mix(static_cast<uint32_t>(i) ^ salt) % d;
+    atomicAdd(m + uint64_t(j) * stride, 1e-9);
+  }
+}
+
 template <int MODE>  // 0: red.add.f32, 1: plain store, 2: load (gather) only
 __global__ void __launch_bounds__(256) k(float* m, uint32_t d, uint32_t stride, uint64_t total, float* out) {
   float acc = 0.f;
@@ -76,6 +85,21 @@ int main() {
       printf("{\"case\": \"%s\", \"op\": \"%s\", \"us\": %.1f, \"G_ops_per_s\": %.1f}\n", c.name, modes[mode], us,
              c.total / us / 1e3);
     }
+  }
+  // One rcv1 mini-batch step's worth of fp64 reductions (4,096 rows x 73 slots).
+  for (uint32_t stride : {1u, 4u, 32u}) {
+    float sum = 0.f;
+    for (int r = 0; r < 13; ++r) {
+      cudaEventRecord(e0);
+      k64<<<sms * 4, 256>>>(reinterpret_cast<double*>(m), 47236, stride, 299662, r);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r >= 3) sum += ms;
+    }
+    printf("{\"case\": \"rcv1 mini-batch step: 300K fp64 red.add on 47,236 coords, stride %u doubles\", \"us\": %.2f}\n",
+           stride, 1e3 * sum / 10);
   }
   cudaError_t err = cudaDeviceSynchronize();
   if (err != cudaSuccess) printf("error %s\n", cudaGetErrorString(err));
