@@ -359,18 +359,20 @@ __global__ void __launch_bounds__(32 * W) dense_batch_kernel(DenseBatchParams p)
 // Barrier across a co-resident grid (cooperative launch). `count` only grows:
 // barrier k of the launch completes when it reaches k * gridDim.x, so an
 // arrival is one atomic and the wait one acquire-load poll (no reset, no
-// generation word). Thread 0 fences the block's global writes (the gradient
-// REDs, ordered before it by the __syncthreads) before arriving.
+// generation word). Thread 0 arrives with a release-add, which orders the
+// block's global writes (the gradient REDs, ordered before it by the
+// __syncthreads) before the arrival.
 __device__ __forceinline__ void grid_sync(unsigned* count, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(count, 1u);
+    // Release-add: the CTA's REDs (ordered before it by the barrier; release
+    // is cumulative) are visible to whoever acquires the count — no separate
+    // full fence.
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
     unsigned v;
     while (true) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
       if (v >= target) break;
-      __nanosleep(20);
     }
   }
   __syncthreads();
