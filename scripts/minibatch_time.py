@@ -15,6 +15,7 @@ SHAPES = {
     "dense256": (lambda: S.fixtures.dense_classification(300000, 256, 9), S.Task.SVM),
     "rcv1": (lambda: S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813), S.Task.LR),
     "realsim": (lambda: S.fixtures.sparse_classification(72309, 20958, 51.3, 20250812), S.Task.SVM),
+    "w8a": (lambda: S.fixtures.sparse_classification(64700, 300, 11.65, 20250811), S.Task.SVM),
     "news20": (lambda: S.fixtures.sparse_classification(19996, 1355191, 455.0, 20250814), S.Task.SVM),
 }
 
