@@ -107,14 +107,14 @@ enum class Kind { Dense, Csr };
 // (b, m) = block b's entries of minor index m, at segptr[b*nminor + m] ..
 // segptr[b*nminor + m + 1], stored as fp32 values + 16-bit block-local major
 // ids in (block, minor, major) order; its head bitmap (bit s = slot s starts
-// a non-empty segment) + word prefix; seg_of_ord when some segments are
-// empty; cpb nnz-balanced minor ranges (cta) shared by all blocks; arrival
+// a non-empty segment) + word prefix; ord_of_seg (exclusive count of the
+// non-empty segments before each) when some segments are empty; cpb nnz-balanced minor ranges (cta) shared by all blocks; arrival
 // tickets (monotonic: gen launches since they were zeroed).
 struct Blocked {
   uint32_t rb = 0, nblk = 0, cpb = 0;
   DBuf<float> val;
   DBuf<uint16_t> id;
-  DBuf<uint32_t> segptr, bm, bm_pre, seg_of_ord, cta;
+  DBuf<uint32_t> segptr, bm, bm_pre, ord_of_seg, cta;
   bool segs_empty = false;
   DBuf<unsigned> tickets;
   unsigned gen = 0;

@@ -397,8 +397,8 @@ struct PassArgs {
   const uint32_t* cta;
   uint32_t cpb, nblk, nminor, rb, nmajor;
   const float* slice;           // gradient: the coefficients; margin: the fp32 model
-  const uint32_t* seg_of_ord;   // SMAP only
-  float* part;                  // nblk * nminor partial sums
+  const uint32_t* ord_of_seg;   // SMAP only: ordinal of segment q = exclusive count of non-empty segments
+  float* part;                  // partial sums: nblk * nminor, or (SMAP) one per non-empty segment
   unsigned* tickets;
   unsigned gen;
   int coop;
@@ -424,8 +424,10 @@ constexpr int kPassMargin = 1;
 // every CTA is resident once the previous pass drains and the arrival wait
 // cannot deadlock); otherwise the last CTA to arrive finishes the whole
 // range. Arrival tickets count up by nblk per launch (gen = launch number),
-// so they are never reset. SMAP: some segments are empty, ordinals map
-// through seg_of_ord (and the range's partials are zeroed first).
+// so they are never reset. SMAP: some segments are empty; the partials are
+// stored compactly by segment ordinal (the stream's emission index, no
+// lookup on the hot path) and the finish finds segment q's through
+// ord_of_seg (empty segments contribute 0).
 template <int MODE, int TASK, bool SMAP>
 __global__ void __launch_bounds__(kNT, 1) blocked_pass_kernel(PassArgs p) {
   extern __shared__ __align__(16) float cs[];
@@ -443,10 +445,6 @@ __global__ void __launch_bounds__(kNT, 1) blocked_pass_kernel(PassArgs p) {
   }
   const uint32_t j0 = __ldg(p.cta + k), j1 = __ldg(p.cta + k + 1);
   const uint64_t q0 = uint64_t(b) * p.nminor;
-  if (SMAP) {   // empty segments are never emitted: zero them first
-    pdl_wait();  // (the previous launch's finish may still read part)
-    for (uint32_t j = j0 + threadIdx.x; j < j1; j += kNT) p.part[q0 + j] = 0.f;
-  }
   __syncthreads();  // the barrier init is visible to every waiter
   if (threadIdx.x == 0) {
     pdl_wait();  // the slice comes from the previous pass
@@ -459,7 +457,6 @@ __global__ void __launch_bounds__(kNT, 1) blocked_pass_kernel(PassArgs p) {
   const uint32_t S0 = __ldg(p.segptr + q0 + j0), S1 = __ldg(p.segptr + q0 + j1);
   bool ready = false;  // the first tiles' loads overlap the slice's bulk copy
   float* __restrict__ part = p.part;
-  const uint32_t* __restrict__ som = p.seg_of_ord;
   cta_segments<kE, 2, WinC>(
       S0, S1, p.bm, p.bpre,
       [&](uint32_t s) {
@@ -478,8 +475,8 @@ __global__ void __launch_bounds__(kNT, 1) blocked_pass_kernel(PassArgs p) {
         pr[4] = q.v1.x * cs[q.r.z & 0xffffu], pr[5] = q.v1.y * cs[q.r.z >> 16];
         pr[6] = q.v1.z * cs[q.r.w & 0xffffu], pr[7] = q.v1.w * cs[q.r.w >> 16];
       },
-      [&](int32_t X, float z) { part[SMAP ? __ldg(som + X) : static_cast<uint32_t>(X)] = z; },
-      [&](int32_t X, float z) { part[SMAP ? __ldg(som + X) : static_cast<uint32_t>(X)] = z; },
+      [&](int32_t X, float z) { part[static_cast<uint32_t>(X)] = z; },
+      [&](int32_t X, float z) { part[static_cast<uint32_t>(X)] = z; },
       [&](int32_t, int32_t) {},
       sc);
   if (!ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
@@ -506,14 +503,22 @@ __global__ void __launch_bounds__(kNT, 1) blocked_pass_kernel(PassArgs p) {
     // Block order; 8 loads in flight per thread.
     double g = 0.0;
     uint32_t bb = 0;
+    // Segment (b, j)'s partial: at b*nminor + j, or (SMAP) at its ordinal
+    // when the segment is non-empty.
+    auto partial = [&](uint32_t b2) -> float {
+      const uint64_t q = uint64_t(b2) * p.nminor + j;
+      if (!SMAP) return __ldcg(part + q);
+      const uint32_t o0 = __ldg(p.ord_of_seg + q), o1 = __ldg(p.ord_of_seg + q + 1);
+      return o1 > o0 ? __ldcg(part + o0) : 0.f;
+    };
     for (; bb + 8 <= p.nblk; bb += 8) {
       float v[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = __ldcg(part + uint64_t(bb + i) * p.nminor + j);
+      for (int i = 0; i < 8; ++i) v[i] = partial(bb + i);
 #pragma unroll
       for (int i = 0; i < 8; ++i) g += static_cast<double>(v[i]);
     }
-    for (; bb < p.nblk; ++bb) g += static_cast<double>(__ldcg(part + uint64_t(bb) * p.nminor + j));
+    for (; bb < p.nblk; ++bb) g += static_cast<double>(partial(bb));
     if (MODE == kPassMargin) {
       p.coef[j] = coef_fast<TASK>(static_cast<float>(g), __ldg(p.y + j));
       continue;
@@ -792,7 +797,7 @@ void build_blocked(Dataset& ds, bool by_col, Blocked& B) {
     B.segptr.zero(s);
   }
   word_prefix(c, B.bm.p, nwords, B.bm_pre, sp.tmp, sp.b);
-  sp.c.alloc(std::max<uint64_t>(1, nseg));  // non-empty segment flags
+  sp.c.alloc(nseg + 1);  // non-empty segment flags (+ a zero for the prefix's end)
   check(cudaMemsetAsync(sp.cnt.p + 1, 0, sizeof(unsigned), s), "memset");
   prof_begin(c, "sparse_prep_kernel");
   seg_nonempty_kernel<<<grid_1d(nseg), 256, 0, s>>>(B.segptr.p, static_cast<uint32_t>(nseg), sp.c.p,
@@ -822,7 +827,17 @@ void build_blocked(Dataset& ds, bool by_col, Blocked& B) {
   check(cudaMemcpyAsync(&empty, sp.cnt.p + 1, sizeof(empty), cudaMemcpyDeviceToHost, s), "D2H");
   check(cudaStreamSynchronize(s), "prep sync");
   B.segs_empty = empty != 0;
-  if (B.segs_empty) compaction(c, sp.c.p, nseg, B.seg_of_ord, sp.tmp, sp.b);
+  if (B.segs_empty) {  // ord_of_seg: exclusive prefix of the non-empty flags (nseg + 1 entries)
+    check(cudaMemsetAsync(sp.c.p + nseg, 0, sizeof(uint32_t), s), "memset");
+    B.ord_of_seg.alloc(nseg + 1);
+    size_t bytes = 0;
+    check(cub::DeviceScan::ExclusiveSum(nullptr, bytes, sp.c.p, B.ord_of_seg.p, static_cast<int64_t>(nseg + 1), s),
+          "cub scan size");
+    sp.tmp.alloc(bytes);
+    bytes = sp.tmp.n;
+    check(cub::DeviceScan::ExclusiveSum(sp.tmp.p, bytes, sp.c.p, B.ord_of_seg.p, static_cast<int64_t>(nseg + 1), s),
+          "cub scan");
+  }
   B.tickets.alloc(B.cpb);
   B.tickets.zero(s);  // arrival counts restart with the launch numbers
   B.gen = 0;
@@ -902,7 +917,7 @@ void launch_pass(Dataset& ds, Blocked& B, uint64_t nminor, uint64_t nmajor, cons
   const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kNT, smem);
   PassArgs p{B.val.p, B.id.p, B.bm.p, B.bm_pre.p, B.segptr.p, B.cta.p, B.cpb, B.nblk,
              static_cast<uint32_t>(nminor), B.rb, static_cast<uint32_t>(nmajor), slice,
-             B.segs_empty ? B.seg_of_ord.p : nullptr, part, B.tickets.p, ++B.gen,
+             B.segs_empty ? B.ord_of_seg.p : nullptr, part, B.tickets.p, ++B.gen,
              // With one CTA per SM and grid <= SMs every CTA becomes resident
              // once the previous pass has drained: the arrival wait cannot deadlock.
              per_sm >= 1 && grid <= static_cast<unsigned>(c.num_sms) ? 1 : 0, aa, ds.labels.p, ds.coef.p};
