@@ -66,7 +66,8 @@ def _ncu_traffic(kernel, summary="round2_ncu_rcv1_full_batch.txt"):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     # The library's profiler names -> the CUDA function ncu reports.
     kernel = {"k3s_grad_kernel": "blocked_pass_kernel<0,",
-              "k2w_margin_kernel": "blocked_pass_kernel<1,"}.get(kernel, kernel)
+              "k2w_margin_kernel": "blocked_pass_kernel<1,",
+              "k23g_step_kernel": "glued_step_kernel<"}.get(kernel, kernel)
     path = os.path.join(ROOT, "profiles", summary)
     if not os.path.exists(path):
         return None, None
@@ -306,6 +307,8 @@ def run_ours(args):
     idx_bytes = 2 if D <= 65536 else 4
     alg = {"k2s_margin_kernel": nnz * (4 + idx_bytes) + nnz // 8 + 2 * N_EX * 4,
            "k3s_grad_kernel": nnz * 6 + nnz // 8 + N_EX * 4}
+    # K23g (the default): both passes in one launch.
+    alg["k23g_step_kernel"] = alg["k2s_margin_kernel"] + alg["k3s_grad_kernel"]
     per = {k: (v[1] / max(1, v[0])) for k, v in stats.items() if k in alg}
     name = max(per, key=per.get)
     kern_ms = per[name]

@@ -154,6 +154,8 @@ struct Dataset {
   DBuf<uint16_t> cidx16;
   uint32_t cta_n = 0;
   DBuf<uint32_t> cta_slot;
+  DBuf<uint32_t> cta_row;  // first row of each margin CTA (cta_n + 1)
+  DBuf<unsigned> blk_ready, blk_expect;  // K23g: per row block, released / expected margin CTAs
   Blocked csc;       // major = rows, minor = columns
   bool wide = false;  // margin pass over `wmajor` below instead of the CSR stream
   Blocked wmajor;    // major = columns, minor = rows

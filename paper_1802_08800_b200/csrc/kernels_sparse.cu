@@ -6,6 +6,8 @@
 //   K2s  margin pass   z = X w, c = coef(z, y)                (CSR stream, model in SMEM)
 //   K2w  margin pass of a model too large for SMEM                (column-blocked CSR stream)
 //   K3s  gradient pass g = X^T c, w -= alpha g                    (row-blocked CSC stream)
+//   K23g K2s then K3s in ONE launch (models in SMEM; the default), the
+//        dependency between them carried by per-row-block release counts
 //
 // Both passes are one segmented stream over a CTA's contiguous range of
 // nonzeros: each warp walks its share in 256-slot tiles (lane l holds slots
@@ -294,16 +296,22 @@ constexpr int kE = 8;
 // model is bulk-copied (1-D TMA) into SMEM (models too large for SMEM take
 // the column-blocked margin pass K2w instead, so d < 65,536 here and the
 // column ids are 16-bit).
+struct K2sArgs {
+  const float* val;
+  const uint16_t* idx;
+  const uint32_t* bm;
+  const uint32_t* bpre;
+  const uint32_t* cta_slot;
+  const uint32_t* row_of_ord;  // RMAP only
+  const float* y;
+  uint32_t n;
+  const float* w32;
+  uint32_t d;
+  float* coef;
+};
+
 template <int TASK, bool RMAP>  // RMAP: empty rows, ordinals map through row_of_ord
-__global__ void __launch_bounds__(kNT, 1)
-    k2s_margin_kernel(const float* __restrict__ val, const uint16_t* __restrict__ idx,
-                      const uint32_t* __restrict__ bm, const uint32_t* __restrict__ bpre,
-                      const uint32_t* __restrict__ cta_slot, const uint32_t* __restrict__ row_of_ord,
-                      const float* __restrict__ y, uint32_t n, const float* __restrict__ w32, uint32_t d,
-                      float* __restrict__ coef) {
-  extern __shared__ __align__(16) float ws[];
-  __shared__ CtaScratch sc;
-  __shared__ uint64_t bar;
+__device__ __forceinline__ void k2s_phase(const K2sArgs& a, float* ws, CtaScratch& sc, uint64_t* bar) {
   // PDL: launched while the previous step drains. The CSR stream is static
   // data, so every warp issues its first tiles' loads at once; only the model
   // (and the coefficients this pass overwrites) belong to the previous step:
@@ -313,32 +321,35 @@ __global__ void __launch_bounds__(kNT, 1)
   // a warp's first product, hence after the wait.
   pdl_launch_dependents();
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     pdl_wait();
-    const uint32_t total = round_up16(uint64_t(d + 1) * 4);  // w32 holds whole 16-byte groups
-    mbar_arrive_expect_tx(&bar, total);
+    const uint32_t total = round_up16(uint64_t(a.d + 1) * 4);  // w32 holds whole 16-byte groups
+    mbar_arrive_expect_tx(bar, total);
     for (uint32_t off = 0; off < total; off += 32768)
-      bulk_g2s(reinterpret_cast<char*>(ws) + off, reinterpret_cast<const char*>(w32) + off,
-               min(32768u, total - off), &bar);
+      bulk_g2s(reinterpret_cast<char*>(ws) + off, reinterpret_cast<const char*>(a.w32) + off,
+               min(32768u, total - off), bar);
   }
-  const uint32_t S0 = __ldg(cta_slot + blockIdx.x), S1 = __ldg(cta_slot + blockIdx.x + 1);
+  const uint32_t S0 = __ldg(a.cta_slot + blockIdx.x), S1 = __ldg(a.cta_slot + blockIdx.x + 1);
   bool ready = false;  // the first tiles' loads overlap the wait and the model's bulk copy
   using Win = WinR16;
+  const float* __restrict__ y = a.y;
+  const uint32_t* __restrict__ row_of_ord = a.row_of_ord;
+  float* __restrict__ coef = a.coef;
   cta_segments<kE, 2, Win>(
-      S0, S1, bm, bpre,
+      S0, S1, a.bm, a.bpre,
       [&](uint32_t s) {
         Win q;
-        ldg256(val + s, q.v0, q.v1);
-        q.j = __ldg(reinterpret_cast<const uint4*>(idx + s));
+        ldg256(a.val + s, q.v0, q.v1);
+        q.j = __ldg(reinterpret_cast<const uint4*>(a.idx + s));
         return q;
       },
       [&](const Win& q, float* p) {
         if (!ready) {
-          mbar_wait(&bar, 0);
+          mbar_wait(bar, 0);
           ready = true;
         }
         uint32_t j[8];
@@ -375,7 +386,15 @@ __global__ void __launch_bounds__(kNT, 1)
         }
       },
       sc);
-  if (!ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
+  if (!ready && threadIdx.x == 0) mbar_wait(bar, 0);  // the bulk copy must land before exit
+}
+
+template <int TASK, bool RMAP>
+__global__ void __launch_bounds__(kNT, 1) k2s_margin_kernel(K2sArgs a) {
+  extern __shared__ __align__(16) float ws[];
+  __shared__ CtaScratch sc;
+  __shared__ uint64_t bar;
+  k2s_phase<TASK, RMAP>(a, ws, sc, &bar);
 }
 
 struct ApplyArgs {
@@ -428,31 +447,41 @@ constexpr int kPassMargin = 1;
 // stored compactly by segment ordinal (the stream's emission index, no
 // lookup on the hot path) and the finish finds segment q's through
 // ord_of_seg (empty segments contribute 0).
-template <int MODE, int TASK, bool SMAP>
-__global__ void __launch_bounds__(kNT, 1) blocked_pass_kernel(PassArgs p) {
-  extern __shared__ __align__(16) float cs[];
-  __shared__ CtaScratch sc;
-  __shared__ uint64_t bar;
-  const uint32_t b = blockIdx.x / p.cpb, k = blockIdx.x % p.cpb;
+// GLUED (the one-launch epoch, K23g): the slice's coefficients come from the
+// margin phase of other CTAs of the same launch; thread 0 acquires block b's
+// ready count (every margin CTA holding rows of the block has released it)
+// instead of waiting for a previous grid, then orders the async-proxy bulk
+// copy after that acquire.
+template <int MODE, int TASK, bool SMAP, bool GLUED>
+__device__ __forceinline__ void blocked_phase(const PassArgs& p, uint32_t item, float* cs, CtaScratch& sc,
+                                              uint64_t* bar, const unsigned* blk_ready, const unsigned* blk_expect) {
+  const uint32_t b = item / p.cpb, k = item % p.cpb;
   const uint32_t r0 = b * p.rb, len = min(p.rb, p.nmajor - r0);  // rb % 8 == 0: 32-byte aligned slice
   // PDL: the blocked stream is static, so the first tiles' loads go out
   // while the previous pass drains; thread 0 waits for it before
   // bulk-copying the slice, and every warp's first product waits for that.
-  pdl_launch_dependents();
+  if (!GLUED) pdl_launch_dependents();
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(bar, 1);
     fence_mbar_init();
   }
   const uint32_t j0 = __ldg(p.cta + k), j1 = __ldg(p.cta + k + 1);
   const uint64_t q0 = uint64_t(b) * p.nminor;
   __syncthreads();  // the barrier init is visible to every waiter
   if (threadIdx.x == 0) {
-    pdl_wait();  // the slice comes from the previous pass
+    if (GLUED) {
+      const unsigned target = p.gen * __ldg(blk_expect + b);
+      while (ld_acquire_gpu(blk_ready + b) < target) {
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    } else {
+      pdl_wait();  // the slice comes from the previous pass
+    }
     const uint32_t total = round_up16(uint64_t(len) * 4);  // both operands carry 16-byte slack
-    mbar_arrive_expect_tx(&bar, total);
+    mbar_arrive_expect_tx(bar, total);
     for (uint32_t off = 0; off < total; off += 32768)
       bulk_g2s(reinterpret_cast<char*>(cs) + off, reinterpret_cast<const char*>(p.slice + r0) + off,
-               min(32768u, total - off), &bar);
+               min(32768u, total - off), bar);
   }
   const uint32_t S0 = __ldg(p.segptr + q0 + j0), S1 = __ldg(p.segptr + q0 + j1);
   bool ready = false;  // the first tiles' loads overlap the slice's bulk copy
@@ -467,7 +496,7 @@ __global__ void __launch_bounds__(kNT, 1) blocked_pass_kernel(PassArgs p) {
       },
       [&](const WinC& q, float* pr) {
         if (!ready) {
-          mbar_wait(&bar, 0);
+          mbar_wait(bar, 0);
           ready = true;
         }
         pr[0] = q.v0.x * cs[q.r.x & 0xffffu], pr[1] = q.v0.y * cs[q.r.x >> 16];
@@ -479,7 +508,7 @@ __global__ void __launch_bounds__(kNT, 1) blocked_pass_kernel(PassArgs p) {
       [&](int32_t X, float z) { part[static_cast<uint32_t>(X)] = z; },
       [&](int32_t, int32_t) {},
       sc);
-  if (!ready && threadIdx.x == 0) mbar_wait(&bar, 0);  // the bulk copy must land before exit
+  if (!ready && threadIdx.x == 0) mbar_wait(bar, 0);  // the bulk copy must land before exit
   __syncthreads();
   const unsigned target = p.gen * p.nblk;
   if (threadIdx.x == 0) {
@@ -542,6 +571,40 @@ __global__ void __launch_bounds__(kNT, 1) blocked_pass_kernel(PassArgs p) {
   }
 }
 
+template <int MODE, int TASK, bool SMAP>
+__global__ void __launch_bounds__(kNT, 1) blocked_pass_kernel(PassArgs p) {
+  extern __shared__ __align__(16) float cs[];
+  __shared__ CtaScratch sc;
+  __shared__ uint64_t bar;
+  blocked_phase<MODE, TASK, SMAP, false>(p, blockIdx.x, cs, sc, &bar, nullptr, nullptr);
+}
+
+// K23g: the whole full-batch step in ONE launch when the model fits in SMEM:
+// CTA x runs K2s's slot range x, releases the row blocks its rows belong to
+// (blk_ready, monotonic: gen launches), then runs K3s's work item x once
+// every margin CTA of that item's row block has released it. Same streams,
+// same sums, same order as K2s -> K3s; no kernel boundary between them (the
+// dynamic SMEM holds the model, then the coefficient slice). Every CTA must
+// be resident: grid = SMs, one CTA per SM.
+template <int TASK, bool RMAP, bool SMAP>
+__global__ void __launch_bounds__(kNT, 1)
+    glued_step_kernel(K2sArgs ka, PassArgs pa, const uint32_t* cta_row, uint32_t rb, unsigned* blk_ready,
+                      const unsigned* blk_expect) {
+  extern __shared__ __align__(16) float smem[];
+  __shared__ CtaScratch sc;
+  __shared__ uint64_t bar_a, bar_b;
+  k2s_phase<TASK, RMAP>(ka, smem, sc, &bar_a);
+  __syncthreads();  // every coefficient of this CTA's rows is written
+  if (threadIdx.x == 0) {
+    const uint32_t r0 = __ldg(cta_row + blockIdx.x), r1 = __ldg(cta_row + blockIdx.x + 1);
+    if (r1 > r0)
+      for (uint32_t bb = r0 / rb; bb <= (r1 - 1) / rb; ++bb)
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(blk_ready + bb) : "memory");
+  }
+  if (blockIdx.x < pa.nblk * pa.cpb)
+    blocked_phase<kPassGrad, TASK, SMAP, true>(pa, blockIdx.x, smem, sc, &bar_b, blk_ready, blk_expect);
+}
+
 // ---- preparation (once per upload / refresh) ---------------------------------
 
 __global__ void row_heads_kernel(const uint32_t* __restrict__ rowptr, uint32_t n, uint32_t* bm,
@@ -571,12 +634,13 @@ __global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t
 // CTA k of the margin pass starts at the first row starting at or after
 // k*nnz/nc (a slot position).
 __global__ void cta_slot_kernel(const uint32_t* __restrict__ rowptr, uint32_t n, uint32_t nc,
-                                uint32_t* cta_slot) {
+                                uint32_t* cta_slot, uint32_t* cta_row) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k > nc) return;
   const uint64_t nnz = rowptr[n];
   if (k == nc) {
     cta_slot[k] = static_cast<uint32_t>(nnz);
+    cta_row[k] = n;
     return;
   }
   const uint32_t target = static_cast<uint32_t>(nnz * k / nc);
@@ -587,6 +651,18 @@ __global__ void cta_slot_kernel(const uint32_t* __restrict__ rowptr, uint32_t n,
     else lo = mid + 1;
   }
   cta_slot[k] = rowptr[lo];
+  cta_row[k] = lo;
+}
+
+// K23g: how many margin CTAs hold rows of each row block (x's rows are
+// [cta_row[x], cta_row[x+1])).
+__global__ void blk_expect_kernel(const uint32_t* __restrict__ cta_row, uint32_t nc, uint32_t rb,
+                                  unsigned* expect) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= nc) return;
+  const uint32_t r0 = cta_row[x], r1 = cta_row[x + 1];
+  if (r1 > r0)
+    for (uint32_t b = r0 / rb; b <= (r1 - 1) / rb; ++b) atomicAdd(expect + b, 1u);
 }
 
 __global__ void narrow_u16_kernel(const uint32_t* __restrict__ src, uint64_t n, uint16_t* dst) {
@@ -875,12 +951,22 @@ void sparse_prep(Dataset& ds) {
   }
   ds.cta_n = static_cast<uint32_t>(std::max(1, c.num_sms));
   ds.cta_slot.alloc(ds.cta_n + 1);
+  ds.cta_row.alloc(ds.cta_n + 1);
   prof_begin(c, "sparse_prep_kernel");
   cta_slot_kernel<<<grid_1d(ds.cta_n + 1), 256, 0, s>>>(ds.rowptr.p, static_cast<uint32_t>(n), ds.cta_n,
-                                                         ds.cta_slot.p);
+                                                         ds.cta_slot.p, ds.cta_row.p);
   launched(c, "sparse_prep_kernel");
 
   build_blocked(ds, false, ds.csc);
+  if (!ds.wide) {  // K23g's row-block readiness counts
+    ds.blk_ready.alloc(ds.csc.nblk);
+    ds.blk_ready.zero(s);
+    ds.blk_expect.alloc(ds.csc.nblk);
+    ds.blk_expect.zero(s);
+    prof_begin(c, "sparse_prep_kernel");
+    blk_expect_kernel<<<grid_1d(ds.cta_n), 256, 0, s>>>(ds.cta_row.p, ds.cta_n, ds.csc.rb, ds.blk_expect.p);
+    launched(c, "sparse_prep_kernel");
+  }
   // Models too large for shared memory: the margin pass runs blocked too.
   if (ds.wide) {
     build_blocked(ds, true, ds.wmajor);
@@ -953,28 +1039,54 @@ void sparse_full_step(Dataset& ds, Model& m, const StepArgs& a) {
                              "k2w_margin_kernel");
   } else {  // K2s (d < 65,536 here: the 16-bit ids exist)
     const size_t model_bytes = round_up16(uint64_t(d + 1) * 4);
+    const K2sArgs ka{ds.val.p, ds.cidx16.p, ds.rbm.p, ds.rbm_pre.p, ds.cta_slot.p,
+                     ds.rows_empty ? ds.row_of_ord.p : nullptr, ds.labels.p, static_cast<uint32_t>(ds.n), m.w32.p, d,
+                     ds.coef.p};
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.blockDim = dim3(kNT);
+    cfg.stream = c.stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = rebuilt ? 0 : 1;
+    Blocked& B = ds.csc;
+    const size_t gsmem = std::max<size_t>(model_bytes, round_up16(uint64_t(B.rb) * 4));
+    // K23g: both passes in one launch whenever every work item of the
+    // gradient pass has a CTA (more row blocks than SMs: K2s -> K3s below).
+    if (B.nblk * B.cpb <= ds.cta_n && ds.cta_n == static_cast<uint32_t>(c.num_sms)) {
+      void (*kern)(K2sArgs, PassArgs, const uint32_t*, uint32_t, unsigned*, const unsigned*);
+      const bool rm = ds.rows_empty, sm = B.segs_empty;
+      if (a.task == kTaskLR)
+        kern = rm ? (sm ? glued_step_kernel<kTaskLR, true, true> : glued_step_kernel<kTaskLR, true, false>)
+                  : (sm ? glued_step_kernel<kTaskLR, false, true> : glued_step_kernel<kTaskLR, false, false>);
+      else
+        kern = rm ? (sm ? glued_step_kernel<kTaskSVM, true, true> : glued_step_kernel<kTaskSVM, true, false>)
+                  : (sm ? glued_step_kernel<kTaskSVM, false, true> : glued_step_kernel<kTaskSVM, false, false>);
+      set_max_dyn_smem(reinterpret_cast<const void*>(kern), gsmem, "cudaFuncSetAttribute(k23g)");
+      if (blocks_per_sm(reinterpret_cast<const void*>(kern), kNT, gsmem) >= 1) {
+        m.part32.alloc(uint64_t(B.nblk) * d + 1);
+        const PassArgs pa{B.val.p, B.id.p, B.bm.p, B.bm_pre.p, B.segptr.p, B.cta.p, B.cpb, B.nblk, d, B.rb,
+                          static_cast<uint32_t>(ds.n), ds.coef.p, B.segs_empty ? B.ord_of_seg.p : nullptr,
+                          m.part32.p, B.tickets.p, ++B.gen, 1, aa, ds.labels.p, ds.coef.p};
+        cfg.gridDim = dim3(ds.cta_n);
+        cfg.dynamicSmemBytes = gsmem;
+        prof_begin(c, "k23g_step_kernel");
+        check(cudaLaunchKernelEx(&cfg, kern, ka, pa, static_cast<const uint32_t*>(ds.cta_row.p), B.rb,
+                                 ds.blk_ready.p, static_cast<const unsigned*>(ds.blk_expect.p)),
+              "cudaLaunchKernelEx(k23g)");
+        launched(c, "k23g_step_kernel");
+        return;
+      }
+    }
     auto kern = a.task == kTaskLR
                     ? (ds.rows_empty ? k2s_margin_kernel<kTaskLR, true> : k2s_margin_kernel<kTaskLR, false>)
                     : (ds.rows_empty ? k2s_margin_kernel<kTaskSVM, true> : k2s_margin_kernel<kTaskSVM, false>);
     set_max_dyn_smem(reinterpret_cast<const void*>(kern), model_bytes, "cudaFuncSetAttribute(k2s)");
     prof_begin(c, "k2s_margin_kernel");
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.gridDim = dim3(ds.cta_n);
-    cfg.blockDim = dim3(kNT);
     cfg.dynamicSmemBytes = model_bytes;
-    cfg.stream = c.stream;
-    cfg.attrs = attr;
-    cfg.numAttrs = rebuilt ? 0 : 1;
-    check(cudaLaunchKernelEx(&cfg, kern, static_cast<const float*>(ds.val.p),
-                             static_cast<const uint16_t*>(ds.cidx16.p), static_cast<const uint32_t*>(ds.rbm.p),
-                             static_cast<const uint32_t*>(ds.rbm_pre.p), static_cast<const uint32_t*>(ds.cta_slot.p),
-                             static_cast<const uint32_t*>(ds.rows_empty ? ds.row_of_ord.p : nullptr),
-                             static_cast<const float*>(ds.labels.p), static_cast<uint32_t>(ds.n),
-                             static_cast<const float*>(m.w32.p), d, ds.coef.p),
-          "cudaLaunchKernelEx(k2s)");
+    check(cudaLaunchKernelEx(&cfg, kern, ka), "cudaLaunchKernelEx(k2s)");
     launched(c, "k2s_margin_kernel");
   }
   // K3s: the gradient pass and the update.
