@@ -934,7 +934,10 @@ void launch_dense_full_LF(Dataset& ds, Model& m, const StepArgs& a) {
   // Rows per tile: ~32 KB, a multiple of the rows all consumer warps take per
   // pass (balanced warps) and of 4 (16-byte bulk-copy granularity).
   const int unit = std::max(4, WC * RS);
-  constexpr int tile_bytes = 32768;  // 16-96 KB measured equal (profiles/round1_dense_tile_sweep.jsonl)
+  // Tile bytes (profiles/round2_dense_tile_sweep.jsonl): 96 KB (two stages)
+  // for rows of >= 1 KB — C5's 25M x 1000 shard 14.8 -> 13.5 ms — and 64 KB
+  // (three stages) for short rows (covtype 34.8 -> 32.8 us).
+  const int tile_bytes = row_bytes >= 1024 ? 98304 : 65536;
   int R = std::max(unit, ((tile_bytes / row_bytes) / unit) * unit);
   R = (R + 3) & ~3;
   DenseFullParams p{};

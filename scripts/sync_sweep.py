@@ -22,6 +22,7 @@ CFG = {
     "rcv1": lambda: (S.fixtures.sparse_classification(677399, 47236, 73.16, 20250813), S.Task.LR, 1e-6),
     "news20": lambda: (S.fixtures.sparse_classification(19996, 1355191, 455.0, 20250814), S.Task.SVM, 1e-5),
     "dense1000": lambda: (S.fixtures.dense_classification(200000, 1000, 7), S.Task.LR, 1e-7),
+    "dense256": lambda: (S.fixtures.dense_classification(300000, 256, 9), S.Task.SVM, 1e-6),
 }
 
 
