@@ -1,10 +1,12 @@
-"""Full-batch sparse step: one-launch K23f vs the two-launch K2s + K3s chain.
+"""B = N epoch timer used for the late round-2 A/B runs of the full-batch step.
 
-Run once per mode with SGDB_FUSED_AB=0 / 1 in the environment (the mode is
-fixed when the dataset is uploaded). Per shape: median device-timed epoch at
-B = N (L2 flushed, written then read, before each), the kernel breakdown, and
-the fp64 model after 5 epochs saved to gpurun_out/fused_ab_<mode>_<shape>.npy
-for the cross-mode comparison (`--compare`).
+The variant under test is chosen outside this script (the library is swapped
+between runs, or a since-removed switch selected it); SGDB_FUSED_AB only labels
+the run. Per shape: median device-timed epoch at B = N (L2 flushed, written then
+read, before each), the kernel breakdown, and the fp64 model after 5 epochs
+saved to gpurun_out/fused_ab_<label>_<shape>.npy; `--compare` reports the
+model difference between labels 0 and 1. Results: profiles/round2_*_ab.jsonl,
+profiles/round2_fused_step_experiment.jsonl, round2_dense_tile_sweep.jsonl.
 """
 import json
 import os
