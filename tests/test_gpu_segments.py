@@ -1,4 +1,5 @@
-"""Edge cases of the full-batch sparse passes (K2s / K2w / K3s, kernels_sparse.cu).
+"""Edge cases of the full-batch sparse passes (K2s / K2w / K3s, kernels_sparse.cu;
+with the model in SMEM, K2s and K3s run as the phases of one launch, K23g).
 
 The margin pass and the blocked-CSC gradient pass walk each warp's nonzeros
 in 256-slot tiles, find segment boundaries in a head bitmap and recover
@@ -245,3 +246,30 @@ def test_full_batch_block_boundaries(sgdb, dev, orc, n, d):
         g = S.sync.batch_gradient(S.Task(task), ds, None, w, device=dev)
         og = orc.batch_gradient(ds, task, None, w)
         assert rel_l2(g, og) <= 1e-5, (n, d, task, rel_l2(g, og))
+
+
+@pytest.mark.parametrize("d,n,kernels", [
+    (600, 5_000, {"k23g_step_kernel"}),                       # model in SMEM: one launch
+    (100_000, 5_000, {"k2w_margin_kernel", "k3s_grad_kernel"}),  # wide model: two launches
+])
+def test_full_batch_step_kernels(sgdb, dev, orc, d, n, kernels):
+    """Which kernels one full-batch step launches (the library's per-launch
+    profiler), and that the step's model equals the oracle's: the one-launch
+    K23g for models that fit in SMEM, K2w -> K3s otherwise. (More row blocks
+    than SMs take K2s -> K3s: test_more_row_blocks_than_sms.)"""
+    S = sgdb
+    rng = np.random.default_rng(21)
+    ds = _csr(S, np.minimum((rng.pareto(2.0, n) + 1) * 6, 400).astype(int).tolist(), d, 22)
+    w0 = rng.normal(0, 0.3, d)
+    dds = S.DeviceDataset(dev, ds)
+    m = S.DeviceModel(dev, d, init=w0)
+    S.sync_epoch(dds, m, S.Task.LR, 0.05, None, n)  # builds the structures
+    m.set(w0)
+    dev.set_profiling(True)
+    S.sync_epoch(dds, m, S.Task.LR, 0.05, None, n)
+    stats = dev.kernel_stats()
+    dev.set_profiling(False)
+    step = {k for k in stats if k.startswith(("k2", "k3"))}
+    assert step == kernels, stats
+    om, _, _ = orc.sync_train(ds, 0, 0.05, n, 1, 5, init=w0)
+    assert rel_l2(m.get(), om[0]) <= 1e-5
