@@ -1033,6 +1033,7 @@ void launch_dense_loss_LF(Dataset& ds, Model& m, int task) {
 template <class Fn>
 void dispatch_dense(uint64_t d, Fn&& fn) {
   if (d <= 32) fn.template operator()<4, 8>();
+  else if (d <= 56) fn.template operator()<4, 14>();
   else if (d <= 64) fn.template operator()<8, 8>();
   else if (d <= 128) fn.template operator()<16, 8>();
   else if (d <= 256) fn.template operator()<32, 8>();
