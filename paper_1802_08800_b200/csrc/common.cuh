@@ -6,6 +6,15 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Device-side bounds checks of the check build (make XFLAGS=-DSGDB_CHECKS):
+// a failed check traps the kernel (cudaErrorAssert). Compiled out otherwise.
+#ifdef SGDB_CHECKS
+#include <cassert>
+#define SGDB_CHECK(c) assert(c)
+#else
+#define SGDB_CHECK(c) ((void)0)
+#endif
+
 namespace sgdb::dev {
 
 constexpr int kTaskLR = 0;

@@ -357,11 +357,18 @@ __device__ __forceinline__ void k2s_phase(const K2sArgs& a, float* ws, CtaScratc
         j[4] = q.j.z & 0xffffu, j[5] = q.j.z >> 16, j[6] = q.j.w & 0xffffu, j[7] = q.j.w >> 16;
         const float x[8] = {q.v0.x, q.v0.y, q.v0.z, q.v0.w, q.v1.x, q.v1.y, q.v1.z, q.v1.w};
 #pragma unroll
-        for (int u = 0; u < 8; ++u) p[u] = x[u] * ws[j[u]];
+        for (int u = 0; u < 8; ++u) {
+          SGDB_CHECK(j[u] <= a.d);
+          p[u] = x[u] * ws[j[u]];
+        }
       },
-      [&](int32_t X, float z) { coef[RMAP ? __ldg(row_of_ord + X) : static_cast<uint32_t>(X)] = z; },
+      [&](int32_t X, float z) {
+        SGDB_CHECK(X >= 0 && (RMAP || static_cast<uint32_t>(X) < a.n));
+        coef[RMAP ? __ldg(row_of_ord + X) : static_cast<uint32_t>(X)] = z;
+      },
       [&](int32_t X, float z) {
         const uint32_t r = RMAP ? __ldg(row_of_ord + X) : static_cast<uint32_t>(X);
+        SGDB_CHECK(r < a.n);
         coef[r] = coef_fast<TASK>(z, __ldg(y + r));
       },
       [&](int32_t lo, int32_t hi) {
@@ -456,6 +463,7 @@ template <int MODE, int TASK, bool SMAP, bool GLUED>
 __device__ __forceinline__ void blocked_phase(const PassArgs& p, uint32_t item, float* cs, CtaScratch& sc,
                                               uint64_t* bar, const unsigned* blk_ready, const unsigned* blk_expect) {
   const uint32_t b = item / p.cpb, k = item % p.cpb;
+  SGDB_CHECK(b < p.nblk && b * p.rb < p.nmajor);
   const uint32_t r0 = b * p.rb, len = min(p.rb, p.nmajor - r0);  // rb % 8 == 0: 32-byte aligned slice
   // PDL: the blocked stream is static, so the first tiles' loads go out
   // while the previous pass drains; thread 0 waits for it before
@@ -471,6 +479,7 @@ __device__ __forceinline__ void blocked_phase(const PassArgs& p, uint32_t item, 
   if (threadIdx.x == 0) {
     if (GLUED) {
       const unsigned target = p.gen * __ldg(blk_expect + b);
+      SGDB_CHECK(__ldg(blk_expect + b) > 0);
       while (ld_acquire_gpu(blk_ready + b) < target) {
       }
       asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -499,13 +508,25 @@ __device__ __forceinline__ void blocked_phase(const PassArgs& p, uint32_t item, 
           mbar_wait(bar, 0);
           ready = true;
         }
+        // Inside the staged slice's SMEM (rb entries). Slots outside the
+        // warp's range (re-read windows, masked after the product) may carry
+        // another block's ids, so the bound is rb, not this block's len.
+        SGDB_CHECK((q.r.x & 0xffffu) < p.rb && (q.r.x >> 16) < p.rb && (q.r.y & 0xffffu) < p.rb &&
+                   (q.r.y >> 16) < p.rb && (q.r.z & 0xffffu) < p.rb && (q.r.z >> 16) < p.rb &&
+                   (q.r.w & 0xffffu) < p.rb && (q.r.w >> 16) < p.rb);
         pr[0] = q.v0.x * cs[q.r.x & 0xffffu], pr[1] = q.v0.y * cs[q.r.x >> 16];
         pr[2] = q.v0.z * cs[q.r.y & 0xffffu], pr[3] = q.v0.w * cs[q.r.y >> 16];
         pr[4] = q.v1.x * cs[q.r.z & 0xffffu], pr[5] = q.v1.y * cs[q.r.z >> 16];
         pr[6] = q.v1.z * cs[q.r.w & 0xffffu], pr[7] = q.v1.w * cs[q.r.w >> 16];
       },
-      [&](int32_t X, float z) { part[static_cast<uint32_t>(X)] = z; },
-      [&](int32_t X, float z) { part[static_cast<uint32_t>(X)] = z; },
+      [&](int32_t X, float z) {
+        SGDB_CHECK(X >= 0 && uint64_t(X) < uint64_t(p.nblk) * p.nminor);
+        part[static_cast<uint32_t>(X)] = z;
+      },
+      [&](int32_t X, float z) {
+        SGDB_CHECK(X >= 0 && uint64_t(X) < uint64_t(p.nblk) * p.nminor);
+        part[static_cast<uint32_t>(X)] = z;
+      },
       [&](int32_t, int32_t) {},
       sc);
   if (!ready && threadIdx.x == 0) mbar_wait(bar, 0);  // the bulk copy must land before exit
@@ -598,8 +619,10 @@ __global__ void __launch_bounds__(kNT, 1)
   if (threadIdx.x == 0) {
     const uint32_t r0 = __ldg(cta_row + blockIdx.x), r1 = __ldg(cta_row + blockIdx.x + 1);
     if (r1 > r0)
-      for (uint32_t bb = r0 / rb; bb <= (r1 - 1) / rb; ++bb)
+      for (uint32_t bb = r0 / rb; bb <= (r1 - 1) / rb; ++bb) {
+        SGDB_CHECK(bb < pa.nblk);
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(blk_ready + bb) : "memory");
+      }
   }
   if (blockIdx.x < pa.nblk * pa.cpb)
     blocked_phase<kPassGrad, TASK, SMAP, true>(pa, blockIdx.x, smem, sc, &bar_b, blk_ready, blk_expect);
