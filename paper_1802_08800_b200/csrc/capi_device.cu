@@ -182,7 +182,7 @@ void model_init(sgdb_model* m, Ctx* c, uint64_t d) {
   m->ctx = c;
   m->d = d;
   m->w32.alloc(((d + 1) + 3) & ~uint64_t(3));  // whole 16-byte groups (bulk copies)
-  m->w64.alloc(std::max<uint64_t>(1, d));
+  m->w64.alloc(std::max<uint64_t>(1, d) + 2);  // +2: whole 16-byte units for L2 bulk prefetches
   m->g64.alloc(std::max<uint64_t>(1, d));
   m->ticket.alloc(1);
   m->finite.alloc(1);
