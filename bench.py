@@ -330,7 +330,8 @@ def run_ours(args):
                    "l2": "inputs (697 MB) larger than L2, and L2 flushed before every step "
                          "(256 MiB written then read back: cold, clean L2; outside the event window)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "frac": achieved / peak, "frac_of_nominal_8TBps": achieved / 8000.0,
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": name, "kernel_ms": kern_ms, "kernel_share_of_step": share,
                      "algorithmic_bytes_per_launch": alg[name], "peak_source": peak_src,
                      "kernels_ms": {k: round(v, 5) for k, v in per.items()},
